@@ -1,0 +1,160 @@
+/*
+ * fic_b200.h — the C-ABI drop-in boundary of the B200 fractal (PIFS) codec.
+ *
+ * Every entry point takes plain C types (pointers + sizes), returns an int32
+ * error code and never throws.  0 means success; a nonzero code k in 1..18 is
+ * (fic::Errc ordinal + 1) of the reference enum (proj/include/fic/error.hpp:10-29),
+ * so a C++ or Python wrapper can rebuild `CodecError(Errc(k-1), detail)` with the
+ * same "Name: detail" text (proj/src/error.cpp:30-41); the detail string of the
+ * last failure on the calling thread is returned by fic_last_error().
+ *
+ * The reference has no C-ABI today; each function below names the reference
+ * interface whose body it replaces.  All compute entry points run on the
+ * calling thread's current CUDA device (cudaGetDevice) and block until their
+ * results are in the caller's buffers, like the reference calls they replace.
+ * There is no CPU fallback: without a usable CUDA device they fail with
+ * FIC_ERR_CUDA.
+ */
+#ifndef FIC_B200_H
+#define FIC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes: Errc ordinal + 1 (proj/include/fic/error.hpp:10-29) ---- */
+enum {
+  FIC_OK = 0,
+  FIC_ERR_MALFORMED_HEADER = 1,
+  FIC_ERR_UNSUPPORTED_MAXVAL = 2,
+  FIC_ERR_TRUNCATED_DATA = 3,
+  FIC_ERR_NOT_SQUARE = 4,
+  FIC_ERR_NOT_POWER_OF_TWO = 5,
+  FIC_ERR_INDIVISIBLE_BY_RANGE = 6,
+  FIC_ERR_TOO_SMALL_FOR_DOMAIN = 7,
+  FIC_ERR_ODD_SIDE = 8,
+  FIC_ERR_SIDE_MISMATCH = 9,
+  FIC_ERR_OUT_OF_BOUNDS = 10,
+  FIC_ERR_NO_VALID_POSITIONS = 11,
+  FIC_ERR_OUT_OF_RANGE = 12,
+  FIC_ERR_GEOMETRY = 13,
+  FIC_ERR_SCALE_MISMATCH = 14,
+  FIC_ERR_DIMENSION_MISMATCH = 15,
+  FIC_ERR_NON_CONTRACTIVE = 16,
+  FIC_ERR_BAD_PARAMS = 17,
+  FIC_ERR_IO = 18,
+  /* not part of the reference enum: device-side failures */
+  FIC_ERR_CUDA = 100,
+  FIC_ERR_INTERNAL = 101
+};
+
+/* CodecParams (proj/include/fic/params.hpp:8-24). */
+typedef struct fic_params {
+  int32_t n;          /* range side, power of two >= 2 */
+  int32_t step;       /* domain grid spacing; 0 = track n */
+  int32_t s_bits;     /* 1..16 */
+  int32_t o_bits;     /* 1..16 */
+  double s_max;       /* snapped to milli precision by normalisation */
+  double shadow_eps;  /* >= 0 */
+} fic_params;
+
+/* RangeMapping (proj/include/fic/encoded_image.hpp:16-26), 32 bytes, fixed layout.
+ * (x, y) is the domain origin in pixels; sym is the normative isometry index
+ * (proj/include/fic/transforms.hpp:31-40). */
+typedef struct fic_mapping {
+  int32_t x;
+  int32_t y;
+  int32_t sym;
+  uint32_t qs;
+  uint32_t qo;
+  int32_t reserved; /* always 0 */
+  double residual;  /* collage error contribution, bit-exact with the reference */
+} fic_mapping;
+
+/* EncodeStats (proj/include/fic/encoder.hpp:49-53). */
+typedef struct fic_stats {
+  uint64_t candidates_tested;
+  uint64_t shadow_ranges;
+  uint64_t shadow_codeblocks;
+} fic_stats;
+
+/* Initial raster kinds of DecodeParams (proj/include/fic/decoder.hpp:29). */
+enum { FIC_INITIAL_MID_GRAY = 0, FIC_INITIAL_BLACK = 1, FIC_INITIAL_SUPPLIED = 2 };
+
+/* ---- diagnostics ---- */
+const char* fic_last_error(void);          /* detail text of the last failure on this thread */
+const char* fic_errc_name(int32_t code);   /* errc_name (proj/src/error.cpp:5-27); "Ok" for 0 */
+const char* fic_version(void);
+
+/* ---- host-side validation (no device work) ---- */
+/* CodecParams::normalized (proj/src/params.cpp:9-23). */
+int32_t fic_normalize_params(const fic_params* in, fic_params* out);
+/* validate_geometry (proj/src/image.cpp:138-149). */
+int32_t fic_validate_geometry(int32_t width, int32_t height, const fic_params* params);
+
+/* ---- encoder (proj/include/fic/encoder.hpp:61-78) ---- */
+/* encode_sequential (proj/src/encoder.cpp:344-366): `out` holds (width/n)^2 records,
+ * row-major over the range grid (range row outer).  `stats` may be NULL. */
+int32_t fic_encode(const uint8_t* image, int32_t width, int32_t height, const fic_params* params,
+                   fic_mapping* out, fic_stats* stats);
+/* encode_parallel (proj/src/encoder.cpp:368-427): same result for every worker count and
+ * chunk geometry; workers/chunk keep their validation (BadParams) and are otherwise unused. */
+int32_t fic_encode_parallel(const uint8_t* image, int32_t width, int32_t height,
+                            const fic_params* params, int32_t workers, int32_t chunk_w,
+                            int32_t chunk_h, fic_mapping* out, fic_stats* stats);
+/* encode_range (proj/src/encoder.cpp:332-342): one range at pixel origin (x, y). */
+int32_t fic_encode_range(const uint8_t* image, int32_t width, int32_t height, int32_t x, int32_t y,
+                         const fic_params* params, fic_mapping* out, fic_stats* stats);
+/* Range-sharded encode of one image (north_star multi-GPU path): encodes range rows
+ * [row_begin, row_end) of the range grid only; `out` holds (row_end-row_begin)*(width/n)
+ * records.  Stats cover the encoded rows only. */
+int32_t fic_encode_rows(const uint8_t* image, int32_t width, int32_t height,
+                        const fic_params* params, int32_t row_begin, int32_t row_end,
+                        fic_mapping* out, fic_stats* stats);
+/* Batch of `count` equal-sized images stored back to back (cfg5 volume); `out` holds
+ * count * (side/n)^2 records; `stats` (may be NULL) is the sum over images. */
+int32_t fic_encode_batch(const uint8_t* images, int32_t count, int32_t width, int32_t height,
+                         const fic_params* params, fic_mapping* out, fic_stats* stats);
+/* Device-resident encode for benchmarks: `d_image` and `d_out` are device pointers on the
+ * current device, work is enqueued on `stream` (cudaStream_t, NULL = default stream) and the
+ * call returns without synchronising.  Stats are computed on the host (they depend only on
+ * moments) and are final on return.  Use fic_encode for the drop-in path. */
+int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height,
+                          const fic_params* params, fic_mapping* d_out, fic_stats* stats,
+                          void* stream);
+
+/* ---- decoder (proj/include/fic/decoder.hpp:45-63) ---- */
+/* decode_step (proj/src/decoder.cpp:39-79) on fp64 rasters of (width*scale)^2 pixels. */
+int32_t fic_decode_step(const double* current, int32_t cur_width, int32_t cur_height,
+                        const fic_mapping* maps, int32_t width, int32_t height,
+                        const fic_params* params, int32_t scale, double* next);
+/* decode_traced (proj/src/decoder.cpp:113-128).  `out` holds (width*scale)^2 bytes;
+ * `step_rmse` (may be NULL) holds `iterations` doubles; `has_eps`=0 disables the early stop. */
+int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const fic_params* params,
+                   int32_t scale, int32_t iterations, int32_t initial_kind, const uint8_t* supplied,
+                   int32_t supplied_width, int32_t supplied_height, int32_t has_eps,
+                   double convergence_eps, uint8_t* out, double* step_rmse,
+                   int32_t* iterations_run);
+/* collage_error (proj/src/decoder.cpp:134-140). */
+int32_t fic_collage_error(const uint8_t* image, int32_t img_width, int32_t img_height,
+                          const fic_mapping* maps, int32_t width, int32_t height,
+                          const fic_params* params, double* out);
+/* decoded_error_bound (proj/src/decoder.cpp:142-146); host only. */
+int32_t fic_decoded_error_bound(double collage_rmse, double s_max, double* out);
+
+/* ---- instrumentation ---- */
+/* Number of this library's kernels launched since load (all devices). */
+uint64_t fic_kernel_launch_count(void);
+/* Average device time (ms, CUDA events on the launching stream) of the matcher kernel
+ * over the calls since the last reset, and the number of timed launches. */
+int32_t fic_matcher_timing(double* avg_ms, uint64_t* launches, int32_t reset);
+/* Enable/disable per-launch matcher timing (adds two events per encode). */
+void fic_set_matcher_timing(int32_t enabled);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FIC_B200_H */

@@ -1,0 +1,287 @@
+"""Python surface of the codec — the `fic` module API (proj/python/bindings/module.cpp:42-189,
+proj/python/fic/__init__.py) re-hosted on the C-ABI of libfic_b200.so.
+
+Same names, argument meanings and error behaviour as the reference bindings:
+`CodecError` carries the reference's "Name: detail" text, `CodecParams(...)` normalises
+on construction (module.cpp:49-62), `encode` validates workers/chunk only when
+workers > 1 (module.cpp:101-102), `decode` accepts 'mid-gray' | 'black' | uint8 array
+(module.cpp:109-140).  Extensions beyond the reference surface (stats, ranges, row
+shards, batches, traced decode) are marked as such.
+"""
+import ctypes
+
+import numpy as np
+
+from . import abi
+from ._lib import lib
+from .abi import MAPPING_DTYPE, FicParams, FicStats, ptr
+
+
+class CodecError(RuntimeError):
+    """fic.CodecError (module.cpp:45): message is "<Errc name>: <detail>"."""
+
+    def __init__(self, code, detail=""):
+        self.code = int(code)
+        self.name = abi.errc_name(self.code)
+        msg = self.name if not detail else f"{self.name}: {detail}"
+        super().__init__(msg)
+
+
+def _check(rc):
+    if rc != 0:
+        raise CodecError(rc, lib().fic_last_error().decode(errors="replace"))
+
+
+class CodecParams:
+    """CodecParams (proj/include/fic/params.hpp:8-24), normalised at construction."""
+
+    __slots__ = ("_p",)
+
+    def __init__(self, n=4, step=0, s_bits=5, o_bits=7, s_max=1.0, shadow_eps=0.0):
+        raw = abi.make_params(n, step, s_bits, o_bits, s_max, shadow_eps)
+        out = FicParams()
+        _check(lib().fic_normalize_params(ctypes.byref(raw), ctypes.byref(out)))
+        self._p = out
+
+    @classmethod
+    def _from_struct(cls, p):
+        obj = cls.__new__(cls)
+        obj._p = p
+        return obj
+
+    n = property(lambda self: self._p.n)
+    step = property(lambda self: self._p.step)
+    s_bits = property(lambda self: self._p.s_bits)
+    o_bits = property(lambda self: self._p.o_bits)
+    s_max = property(lambda self: self._p.s_max)
+    shadow_eps = property(lambda self: self._p.shadow_eps)
+
+    @property
+    def struct(self):
+        return self._p
+
+    def __eq__(self, other):
+        return isinstance(other, CodecParams) and all(
+            getattr(self, f) == getattr(other, f) for f in ("n", "step", "s_bits", "o_bits", "s_max", "shadow_eps"))
+
+    def __repr__(self):  # module.cpp:69-73 (std::to_string -> 6 decimals)
+        return (f"CodecParams(n={self.n}, step={self.step}, s_bits={self.s_bits}, o_bits={self.o_bits}, "
+                f"s_max={self.s_max:.6f})")
+
+
+class EncodedImage:
+    """EncodedImage (proj/include/fic/encoded_image.hpp:30-41): header + row-major mappings.
+
+    `mappings` is a numpy array of MAPPING_DTYPE records (x, y, sym, qs, qo, reserved,
+    residual); `stats` (extension) holds EncodeStats of the encode that produced it."""
+
+    def __init__(self, width, height, params, mappings, stats=None):
+        self.width = int(width)
+        self.height = int(height)
+        self.params = params
+        self.mappings = mappings
+        self.stats = stats
+
+    @property
+    def mapping_count(self):
+        return int(len(self.mappings))
+
+    def serialize(self):
+        from .fic1 import serialize
+        return serialize(self)
+
+    @staticmethod
+    def deserialize(data):
+        from .fic1 import deserialize
+        return deserialize(data)
+
+    def __eq__(self, other):  # RangeMapping equality ignores the residual (encoded_image.hpp:23-25)
+        if not isinstance(other, EncodedImage):
+            return NotImplemented
+        keys = ["x", "y", "sym", "qs", "qo"]
+        return (self.width == other.width and self.height == other.height and self.params == other.params
+                and len(self.mappings) == len(other.mappings)
+                and all(np.array_equal(self.mappings[k], other.mappings[k]) for k in keys))
+
+    def __repr__(self):
+        return f"EncodedImage({self.width}x{self.height}, {self.mapping_count} mappings)"
+
+
+def _u8_2d(image):
+    arr = np.ascontiguousarray(np.asarray(image), dtype=np.uint8)
+    if arr.ndim != 2:
+        raise ValueError("expected a 2D uint8 array (height x width)")
+    return arr
+
+
+def _range_count(h, w, p):
+    return (w // p.n) * (h // p.n) if p.n > 0 else 0
+
+
+def encode(image, params=None, workers=1, chunk=(16, 16)):
+    """Full-search PIFS encode (module.cpp:94-107 -> encode_sequential / encode_parallel)."""
+    params = CodecParams() if params is None else params
+    img = _u8_2d(image)
+    h, w = img.shape
+    out = np.zeros(max(_range_count(h, w, params), 1), MAPPING_DTYPE)
+    st = FicStats()
+    L = lib()
+    if workers > 1:
+        rc = L.fic_encode_parallel(ptr(img), w, h, ctypes.byref(params.struct), int(workers), int(chunk[0]),
+                                   int(chunk[1]), ptr(out), ctypes.byref(st))
+    else:
+        rc = L.fic_encode(ptr(img), w, h, ctypes.byref(params.struct), ptr(out), ctypes.byref(st))
+    _check(rc)
+    return EncodedImage(w, h, params, out[: _range_count(h, w, params)], st.as_dict())
+
+
+def encode_with_stats(image, params=None):
+    """(extension) encode plus EncodeStats (proj/include/fic/encoder.hpp:49-53) as a dict."""
+    enc = encode(image, params)
+    return enc, enc.stats
+
+
+def encode_range(image, x, y, params=None):
+    """(extension) encode_range (proj/src/encoder.cpp:332-342): (record, stats)."""
+    params = CodecParams() if params is None else params
+    img = _u8_2d(image)
+    h, w = img.shape
+    out = np.zeros(1, MAPPING_DTYPE)
+    st = FicStats()
+    _check(lib().fic_encode_range(ptr(img), w, h, int(x), int(y), ctypes.byref(params.struct), ptr(out),
+                                  ctypes.byref(st)))
+    return out[0], st.as_dict()
+
+
+def encode_rows(image, row_begin, row_end, params=None):
+    """(extension) encode range rows [row_begin, row_end) only — the per-rank shard of the
+    multi-GPU encoder.  Returns (records, stats)."""
+    params = CodecParams() if params is None else params
+    img = _u8_2d(image)
+    h, w = img.shape
+    count = max(0, row_end - row_begin) * (w // params.n)
+    out = np.zeros(max(count, 1), MAPPING_DTYPE)
+    st = FicStats()
+    _check(lib().fic_encode_rows(ptr(img), w, h, ctypes.byref(params.struct), int(row_begin), int(row_end),
+                                 ptr(out), ctypes.byref(st)))
+    return out[:count], st.as_dict()
+
+
+def encode_batch(images, params=None):
+    """(extension) encode a (count, side, side) uint8 volume slice by slice; returns a list of
+    EncodedImage and the summed stats."""
+    params = CodecParams() if params is None else params
+    vol = np.ascontiguousarray(np.asarray(images), dtype=np.uint8)
+    if vol.ndim != 3:
+        raise ValueError("expected a 3D uint8 array (count x height x width)")
+    c, h, w = vol.shape
+    per = _range_count(h, w, params)
+    out = np.zeros(max(c * per, 1), MAPPING_DTYPE)
+    st = FicStats()
+    _check(lib().fic_encode_batch(ptr(vol), c, w, h, ctypes.byref(params.struct), ptr(out), ctypes.byref(st)))
+    return [EncodedImage(w, h, params, out[i * per:(i + 1) * per].copy()) for i in range(c)], st.as_dict()
+
+
+def _maps(enc):
+    m = np.ascontiguousarray(enc.mappings, MAPPING_DTYPE)
+    if len(m) != _range_count(enc.height, enc.width, enc.params):
+        raise CodecError(abi.ERRC_NAMES.index("BadParams") + 1, "mapping count does not cover the range grid")
+    return m
+
+
+def decode_traced(enc, scale=1, iterations=16, initial="mid-gray", convergence_eps=None):
+    """(extension) decode_traced (proj/src/decoder.cpp:113-128): (image, step_rmse, iterations_run)."""
+    maps = _maps(enc)
+    sup = None
+    sw = sh = 0
+    if isinstance(initial, str):
+        if initial not in abi.INITIAL_KINDS:
+            raise ValueError("initial must be 'mid-gray', 'black', or an array")
+        kind = abi.INITIAL_KINDS[initial]
+    else:
+        sup = _u8_2d(initial)
+        sh, sw = sup.shape
+        kind = abi.INITIAL_SUPPLIED
+    kw, kh = enc.width * max(scale, 0), enc.height * max(scale, 0)
+    out = np.empty((max(kh, 1), max(kw, 1)), np.uint8)
+    rm = np.zeros(max(iterations, 1), np.float64)
+    runs = ctypes.c_int32(0)
+    _check(lib().fic_decode(ptr(maps), enc.width, enc.height, ctypes.byref(enc.params.struct), int(scale),
+                            int(iterations), kind, ptr(sup), sw, sh, int(convergence_eps is not None),
+                            float(convergence_eps or 0.0), ptr(out), ptr(rm), ctypes.byref(runs)))
+    return out, rm[: runs.value].copy(), runs.value
+
+
+def decode(enc, scale=1, iterations=16, initial="mid-gray", convergence_eps=None):
+    """Iterative decode at an integer magnification (module.cpp:109-140)."""
+    return decode_traced(enc, scale, iterations, initial, convergence_eps)[0]
+
+
+def decode_step(raster, enc, scale=1):
+    """(extension) one application of the stored transform to an fp64 raster (decoder.cpp:39-79)."""
+    cur = np.ascontiguousarray(raster, np.float64)
+    if cur.ndim != 2:
+        raise ValueError("expected a 2D float64 raster")
+    nxt = np.empty_like(cur)
+    maps = _maps(enc)
+    _check(lib().fic_decode_step(ptr(cur), cur.shape[1], cur.shape[0], ptr(maps), enc.width, enc.height,
+                                 ctypes.byref(enc.params.struct), int(scale), ptr(nxt)))
+    return nxt
+
+
+def collage_error(image, enc):
+    """RMSE between the image and one application of the stored transform (decoder.cpp:134-140)."""
+    img = _u8_2d(image)
+    maps = _maps(enc)
+    out = ctypes.c_double()
+    _check(lib().fic_collage_error(ptr(img), img.shape[1], img.shape[0], ptr(maps), enc.width, enc.height,
+                                   ctypes.byref(enc.params.struct), ctypes.byref(out)))
+    return out.value
+
+
+def decoded_error_bound(collage_rmse, s_max):
+    """collage_rmse / (1 - s_max); NonContractive when s_max >= 1 (decoder.cpp:142-146)."""
+    out = ctypes.c_double()
+    _check(lib().fic_decoded_error_bound(float(collage_rmse), float(s_max), ctypes.byref(out)))
+    return out.value
+
+
+def validate_geometry(image, params=None):
+    """validate_geometry (proj/src/image.cpp:138-149)."""
+    params = CodecParams() if params is None else params
+    img = _u8_2d(image)
+    _check(lib().fic_validate_geometry(img.shape[1], img.shape[0], ctypes.byref(params.struct)))
+
+
+def rmse(a, b):
+    """Integer-exact SSE -> RMSE (proj/src/metrics.cpp:8-17).  Host utility."""
+    a, b = _u8_2d(a), _u8_2d(b)
+    if a.shape != b.shape:
+        raise CodecError(abi.ERRC_NAMES.index("DimensionMismatch") + 1, "image geometry differs")
+    d = a.astype(np.int64) - b.astype(np.int64)
+    return float(np.sqrt(float(np.sum(d * d)) / float(a.size)))
+
+
+def psnr(a, b):
+    """20*log10(255/rmse); inf for identical images (proj/src/metrics.cpp:19-23)."""
+    e = rmse(a, b)
+    if e == 0.0:
+        return float("inf")
+    return float(20.0 * np.log10(255.0 / e))
+
+
+def kernel_launch_count():
+    """(extension) number of this library's kernels launched so far."""
+    return int(lib().fic_kernel_launch_count())
+
+
+def matcher_timing(reset=False):
+    """(extension) (average matcher ms, timed launches) since the last reset."""
+    ms = ctypes.c_double()
+    n = ctypes.c_uint64()
+    lib().fic_matcher_timing(ctypes.byref(ms), ctypes.byref(n), int(reset))
+    return ms.value, n.value
+
+
+def set_matcher_timing(enabled):
+    lib().fic_set_matcher_timing(int(bool(enabled)))

@@ -1,0 +1,616 @@
+// fic_api.cu — the C-ABI (include/fic_b200.h) and its host-side orchestration.
+//
+// Validation and error semantics follow the reference entry points they replace
+// (proj/src/encoder.cpp:323-427, proj/src/decoder.cpp:39-146, proj/src/params.cpp:9-23,
+// proj/src/image.cpp:138-149); all compute runs in the kernels of this directory.
+// There is no CPU fallback: every failure of the CUDA runtime surfaces as FIC_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ficb {
+// kernels (pool.cu, matcher_*.cu, decoder.cu)
+void launch_pool_build(const unsigned char*, const Geometry&, unsigned char*, DomainMetaF*, DomainMetaI*,
+                       unsigned long long*, cudaStream_t);
+void launch_range_pass(const unsigned char*, const Geometry&, RangeMeta*, unsigned long long*, cudaStream_t);
+void launch_matcher_simt(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
+                         const DomainMetaI*, const RangeMeta*, int, int, Partial*, cudaStream_t);
+cudaError_t launch_matcher_tc(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
+                              const DomainMetaI*, const RangeMeta*, int, int, Partial*, cudaStream_t);
+bool tc_supported(const Geometry&);
+void launch_finalize(const unsigned char*, const Geometry&, const RangeMeta*, const Partial*, int, fic_mapping*,
+                     cudaStream_t);
+struct RangeXform {
+  double s, o;
+  int dx, dy;
+  int sym;
+  int pad;
+};
+int decode_blocks(long long);
+void launch_xform(const fic_mapping*, int, int, const Geometry&, RangeXform*, cudaStream_t);
+void launch_decode_step(const double*, double*, const RangeXform*, int, int, int, double*, cudaStream_t);
+void launch_rmse_finish(const double*, int, long long, double*, cudaStream_t);
+void launch_raster_init(double*, long long, int, const unsigned char*, cudaStream_t);
+void launch_quantize_raster(const double*, long long, unsigned char*, cudaStream_t);
+}  // namespace ficb
+
+using namespace ficb;
+
+namespace {
+
+const char* const kErrcNames[] = {"MalformedHeader", "UnsupportedMaxval", "TruncatedData", "NotSquare",
+                                  "NotPowerOfTwo", "IndivisibleByRange", "TooSmallForDomain", "OddSide",
+                                  "SideMismatch", "OutOfBounds", "NoValidPositions", "OutOfRange",
+                                  "GeometryError", "ScaleMismatch", "DimensionMismatch", "NonContractive",
+                                  "BadParams", "IoError"};
+
+thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
+std::atomic<int> g_timing{0};
+std::mutex g_timing_mu;
+double g_timing_ms = 0.0;
+unsigned long long g_timing_n = 0;
+
+int32_t fail(int32_t code, const std::string& detail) {
+  g_err = detail;
+  return code;
+}
+
+struct CudaFail {
+  cudaError_t e;
+  const char* what;
+};
+
+#define CK(call)                                  \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) throw CudaFail{e_, #call}; \
+  } while (0)
+
+bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// CodecParams::normalized (proj/src/params.cpp:9-23)
+int32_t normalize(const fic_params* in, fic_params* out) {
+  if (!in) return fail(FIC_ERR_BAD_PARAMS, "null params");
+  fic_params p = *in;
+  if (p.n < 2 || !is_pow2(p.n)) return fail(FIC_ERR_BAD_PARAMS, "n must be a power of two >= 2, got " + std::to_string(p.n));
+  if (p.step == 0) p.step = p.n;
+  if (p.step < 1) return fail(FIC_ERR_BAD_PARAMS, "step must be >= 1");
+  if (p.s_bits < 1 || p.s_bits > 16) return fail(FIC_ERR_BAD_PARAMS, "s_bits must be in [1, 16]");
+  if (p.o_bits < 1 || p.o_bits > 16) return fail(FIC_ERR_BAD_PARAMS, "o_bits must be in [1, 16]");
+  if (!(p.s_max > 0.0)) return fail(FIC_ERR_BAD_PARAMS, "s_max must be positive");
+  if (p.s_max > 65.535) return fail(FIC_ERR_BAD_PARAMS, "s_max exceeds the header's milli-precision range");
+  p.s_max = (double)std::lround(p.s_max * 1000.0) / 1000.0;
+  if (!(p.s_max > 0.0)) return fail(FIC_ERR_BAD_PARAMS, "s_max rounds to zero at milli precision");
+  if (p.shadow_eps < 0.0) return fail(FIC_ERR_BAD_PARAMS, "shadow_eps must be non-negative");
+  *out = p;
+  return FIC_OK;
+}
+
+// validate_geometry (proj/src/image.cpp:138-149), params already normalised
+int32_t geometry_check(int w, int h, const fic_params& p) {
+  if (w != h) return fail(FIC_ERR_NOT_SQUARE, std::to_string(w) + "x" + std::to_string(h));
+  if (w <= 0 || !is_pow2(w)) return fail(FIC_ERR_NOT_POWER_OF_TWO, "side " + std::to_string(w));
+  if (w % p.n != 0)
+    return fail(FIC_ERR_INDIVISIBLE_BY_RANGE, "side " + std::to_string(w) + ", n " + std::to_string(p.n));
+  if (w < 2 * p.n)
+    return fail(FIC_ERR_TOO_SMALL_FOR_DOMAIN,
+                "side " + std::to_string(w) + " cannot hold a " + std::to_string(2 * p.n) + "-wide domain");
+  return FIC_OK;
+}
+
+Geometry make_geometry(int w, int h, const fic_params& p) {
+  Geometry g{};
+  g.W = w;
+  g.H = h;
+  g.n = p.n;
+  g.N = p.n * p.n;
+  g.K = ((g.N + 15) / 16) * 16;
+  g.step = p.step;
+  g.PX = w >= 2 * p.n ? (w - 2 * p.n) / p.step + 1 : 0;
+  g.PY = h >= 2 * p.n ? (h - 2 * p.n) / p.step + 1 : 0;
+  g.D = g.PX * g.PY;
+  g.D_pad = ((g.D + kDomainsPerTile - 1) / kDomainsPerTile) * kDomainsPerTile;
+  g.RX = w / p.n;
+  g.R = (w / p.n) * (h / p.n);
+  g.row_begin = 0;
+  g.single_x0 = -1;
+  g.single_y0 = -1;
+  const char* dbg = std::getenv("FIC_DEBUG");
+  g.flags = dbg ? std::atoi(dbg) : 0;
+  g.s_bits = p.s_bits;
+  g.o_bits = p.o_bits;
+  g.s_max = p.s_max;
+  g.shadow_eps = p.shadow_eps;
+  return g;
+}
+
+// Growable device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) CK(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+      size_t want = bytes + bytes / 4 + 256;
+      CK(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return p;
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) CK(cudaFreeHost(p));
+      p = nullptr;
+      cap = 0;
+      size_t want = bytes + bytes / 4 + 256;
+      CK(cudaMallocHost(&p, want));
+      cap = want;
+    }
+    return p;
+  }
+};
+
+// One workspace per device; calls on a device serialise on its mutex.
+struct Workspace {
+  int device = -1;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out;
+  HostBuf h_img, h_out, h_counters, h_raster, h_rmse;
+  std::mutex mu;
+};
+
+std::mutex g_ws_mu;
+std::vector<Workspace*> g_ws;
+
+Workspace& workspace() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_ws_mu);
+  if ((int)g_ws.size() <= dev) g_ws.resize(dev + 1, nullptr);
+  if (!g_ws[dev]) {
+    Workspace* w = new Workspace();
+    w->device = dev;
+    CK(cudaDeviceGetAttribute(&w->sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&w->ev0));
+    CK(cudaEventCreate(&w->ev1));
+    g_ws[dev] = w;
+  }
+  return *g_ws[dev];
+}
+
+int matcher_mode(const Geometry& g) {
+  const char* env = std::getenv("FIC_MATCHER");
+  const bool want_simt = env && std::strcmp(env, "simt") == 0;
+  return (!want_simt && tc_supported(g)) ? 1 : 0;  // 1 = tcgen05
+}
+
+// Enqueue the whole encode of the region described by g: K1 pool, range pass, K2
+// matcher, finalize.  counters[0] = flat domains, counters[1] = shadow ranges.
+void enqueue_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fic_mapping* d_out,
+                    unsigned long long* d_counters, cudaStream_t st) {
+  auto* pool = static_cast<unsigned char*>(ws.pool.get((size_t)g.D_pad * g.K * 16));
+  auto* mf = static_cast<DomainMetaF*>(ws.meta_f.get((size_t)g.D_pad * sizeof(DomainMetaF)));
+  auto* mi = static_cast<DomainMetaI*>(ws.meta_i.get((size_t)g.D_pad * sizeof(DomainMetaI)));
+  auto* rm = static_cast<RangeMeta*>(ws.rmeta.get((size_t)g.R * sizeof(RangeMeta)));
+  const int n_tiles = g.D_pad / kDomainsPerTile;
+  const int m_tiles = (g.R + kRangesPerTile - 1) / kRangesPerTile;
+  const int mode = matcher_mode(g);
+  int n_chunks;
+  if (mode == 1)
+    n_chunks = m_tiles >= ws.sms ? 1 : ws.sms / m_tiles;
+  else
+    n_chunks = (ws.sms * 8 + m_tiles - 1) / m_tiles;
+  n_chunks = std::max(1, std::min(n_chunks, n_tiles));
+  const int tiles_per_chunk = (n_tiles + n_chunks - 1) / n_chunks;
+  n_chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+  const int n_slots = mode == 1 ? 2 * n_chunks : n_chunks;
+  auto* parts = static_cast<Partial*>(ws.partials.get((size_t)n_slots * g.R * sizeof(Partial)));
+
+  CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
+  launch_pool_build(d_img, g, pool, mf, mi, d_counters, st);
+  launch_range_pass(d_img, g, rm, d_counters + 1, st);
+  const bool timed = g_timing.load() != 0;
+  if (timed) CK(cudaEventRecord(ws.ev0, st));
+  if (mode == 1) {
+    CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, st));
+  } else {
+    launch_matcher_simt(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, st);
+  }
+  if (timed) CK(cudaEventRecord(ws.ev1, st));
+  launch_finalize(d_img, g, rm, parts, n_slots, d_out, st);
+  CK(cudaGetLastError());
+  g_launches += 4;
+}
+
+void collect_timing(Workspace& ws) {
+  if (!g_timing.load()) return;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, ws.ev0, ws.ev1) == cudaSuccess) {
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    g_timing_ms += ms;
+    g_timing_n += 1;
+  }
+}
+
+void fill_stats(fic_stats* stats, const Geometry& g, unsigned long long flat, unsigned long long shadow) {
+  if (!stats) return;
+  const unsigned long long active = (unsigned long long)g.R - shadow;
+  stats->candidates_tested = 8ull * active * ((unsigned long long)g.D - flat);
+  stats->shadow_ranges = shadow;
+  stats->shadow_codeblocks = 8ull * active * flat;
+}
+
+template <class F>
+int32_t guarded(F&& f) {
+  try {
+    return f();
+  } catch (const CudaFail& c) {
+    return fail(FIC_ERR_CUDA, std::string(cudaGetErrorName(c.e)) + " (" + cudaGetErrorString(c.e) + ") at " + c.what);
+  } catch (const std::bad_alloc&) {
+    return fail(FIC_ERR_INTERNAL, "host allocation failed");
+  }
+}
+
+// Encode `g` of the host image into host `out` (g.R records).
+int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, fic_stats* stats) {
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    const size_t img_bytes = (size_t)g.W * g.H;
+    auto* h_img = static_cast<unsigned char*>(ws.h_img.get(img_bytes));
+    std::memcpy(h_img, image, img_bytes);
+    auto* d_img = static_cast<unsigned char*>(ws.img.get(img_bytes));
+    auto* d_out = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
+    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
+    auto* h_out = static_cast<fic_mapping*>(ws.h_out.get((size_t)g.R * sizeof(fic_mapping)));
+    auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * sizeof(unsigned long long)));
+    CK(cudaMemcpyAsync(d_img, h_img, img_bytes, cudaMemcpyHostToDevice, ws.stream));
+    enqueue_encode(ws, d_img, g, d_out, d_cnt, ws.stream);
+    CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaMemcpyAsync(h_cnt, d_cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+    collect_timing(ws);
+    std::memcpy(out, h_out, (size_t)g.R * sizeof(fic_mapping));
+    fill_stats(stats, g, h_cnt[0], h_cnt[1]);
+    return FIC_OK;
+  });
+}
+
+// dequantize range check of decode_step (format.hpp:34-40) plus window bounds
+int32_t check_mappings(const fic_mapping* maps, int w, int h, const fic_params& p) {
+  const unsigned smc = (1u << p.s_bits) - 1u, omc = (1u << p.o_bits) - 1u;
+  const long count = (long)(w / p.n) * (h / p.n);
+  for (long i = 0; i < count; ++i) {
+    const fic_mapping& m = maps[i];
+    if (m.qs > smc) return fail(FIC_ERR_OUT_OF_RANGE, "code " + std::to_string(m.qs) + " exceeds " + std::to_string(smc));
+    if (m.qo > omc) return fail(FIC_ERR_OUT_OF_RANGE, "code " + std::to_string(m.qo) + " exceeds " + std::to_string(omc));
+    if (m.sym < 0 || m.sym > 7) return fail(FIC_ERR_OUT_OF_RANGE, "symmetry index " + std::to_string(m.sym));
+    if (m.x < 0 || m.y < 0 || m.x + 2 * p.n > w || m.y + 2 * p.n > h)
+      return fail(FIC_ERR_OUT_OF_BOUNDS, std::to_string(2 * p.n) + "-wide window at (" + std::to_string(m.x) + ", " +
+                                             std::to_string(m.y) + ")");
+  }
+  return FIC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fic_last_error(void) { return g_err.c_str(); }
+
+const char* fic_errc_name(int32_t code) {
+  if (code == 0) return "Ok";
+  if (code >= 1 && code <= 18) return kErrcNames[code - 1];
+  if (code == FIC_ERR_CUDA) return "CudaError";
+  return "InternalError";
+}
+
+const char* fic_version(void) { return "fic_b200 0.1 (sm_100a)"; }
+
+int32_t fic_normalize_params(const fic_params* in, fic_params* out) {
+  fic_params p;
+  const int32_t e = normalize(in, &p);
+  if (e) return e;
+  if (out) *out = p;
+  return FIC_OK;
+}
+
+int32_t fic_validate_geometry(int32_t width, int32_t height, const fic_params* params) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  return geometry_check(width, height, p);
+}
+
+int32_t fic_encode(const uint8_t* image, int32_t width, int32_t height, const fic_params* params, fic_mapping* out,
+                   fic_stats* stats) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  if (!image || !out) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  return encode_host(image, make_geometry(width, height, p), out, stats);
+}
+
+int32_t fic_encode_parallel(const uint8_t* image, int32_t width, int32_t height, const fic_params* params,
+                            int32_t workers, int32_t chunk_w, int32_t chunk_h, fic_mapping* out, fic_stats* stats) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  if (workers < 1) return fail(FIC_ERR_BAD_PARAMS, "workers must be >= 1");
+  if (chunk_w < 1 || chunk_h < 1) return fail(FIC_ERR_BAD_PARAMS, "chunk geometry must be >= 1x1");
+  if (!image || !out) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  return encode_host(image, make_geometry(width, height, p), out, stats);
+}
+
+int32_t fic_encode_range(const uint8_t* image, int32_t width, int32_t height, int32_t x, int32_t y,
+                         const fic_params* params, fic_mapping* out, fic_stats* stats) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  // check_range_origin (encoder.cpp:323-328)
+  if (x % p.n != 0 || y % p.n != 0 || x < 0 || y < 0 || x + p.n > width || y + p.n > height)
+    return fail(FIC_ERR_GEOMETRY, "range origin (" + std::to_string(x) + ", " + std::to_string(y) + ") not on the grid");
+  Geometry g = make_geometry(width, height, p);
+  if (g.D == 0) return fail(FIC_ERR_NO_VALID_POSITIONS, "no domain fits the image");  // encoder.cpp:132
+  if (!image || !out) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  g.R = 1;
+  g.RX = 1;
+  g.single_x0 = x;
+  g.single_y0 = y;
+  return encode_host(image, g, out, stats);
+}
+
+int32_t fic_encode_rows(const uint8_t* image, int32_t width, int32_t height, const fic_params* params,
+                        int32_t row_begin, int32_t row_end, fic_mapping* out, fic_stats* stats) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  Geometry g = make_geometry(width, height, p);
+  const int rows = height / p.n;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end)
+    return fail(FIC_ERR_BAD_PARAMS, "range rows [" + std::to_string(row_begin) + ", " + std::to_string(row_end) +
+                                        ") outside [0, " + std::to_string(rows) + ")");
+  if (!image || (!out && row_end > row_begin)) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  if (row_end == row_begin) {
+    if (stats) *stats = fic_stats{0, 0, 0};
+    return FIC_OK;
+  }
+  g.row_begin = row_begin;
+  g.R = (row_end - row_begin) * g.RX;
+  return encode_host(image, g, out, stats);
+}
+
+int32_t fic_encode_batch(const uint8_t* images, int32_t count, int32_t width, int32_t height,
+                         const fic_params* params, fic_mapping* out, fic_stats* stats) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  if (count < 0) return fail(FIC_ERR_BAD_PARAMS, "negative batch size");
+  const Geometry g = make_geometry(width, height, p);
+  fic_stats total{0, 0, 0};
+  for (int i = 0; i < count; ++i) {
+    fic_stats s{0, 0, 0};
+    e = encode_host(images + (size_t)i * width * height, g, out + (size_t)i * g.R, &s);
+    if (e) return e;
+    total.candidates_tested += s.candidates_tested;
+    total.shadow_ranges += s.shadow_ranges;
+    total.shadow_codeblocks += s.shadow_codeblocks;
+  }
+  if (stats) *stats = total;
+  return FIC_OK;
+}
+
+int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height, const fic_params* params,
+                          fic_mapping* d_out, fic_stats* stats, void* stream) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  const Geometry g = make_geometry(width, height, p);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
+    enqueue_encode(ws, d_image, g, d_out, d_cnt, st);
+    if (stats) {
+      unsigned long long h[2];
+      CK(cudaMemcpyAsync(h, d_cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      fill_stats(stats, g, h[0], h[1]);
+    }
+    if (g_timing.load()) {
+      CK(cudaStreamSynchronize(st));
+      collect_timing(ws);
+    }
+    return FIC_OK;
+  });
+}
+
+int32_t fic_decode_step(const double* current, int32_t cur_width, int32_t cur_height, const fic_mapping* maps,
+                        int32_t width, int32_t height, const fic_params* params, int32_t scale, double* next) {
+  if (scale < 1) return fail(FIC_ERR_BAD_PARAMS, "scale must be >= 1");
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  const int out_w = width * scale, out_h = height * scale;
+  if (cur_width != out_w || cur_height != out_h)
+    return fail(FIC_ERR_SCALE_MISMATCH, "raster is " + std::to_string(cur_width) + "x" + std::to_string(cur_height) +
+                                            ", expected " + std::to_string(out_w) + "x" + std::to_string(out_h));
+  if (width != height || width % p.n != 0) return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
+  if ((e = check_mappings(maps, width, height, p))) return e;
+  const Geometry g = make_geometry(width, height, p);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    const long long cnt = (long long)out_w * out_h;
+    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
+    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)g.R * sizeof(RangeXform)));
+    auto* a = static_cast<double*>(ws.ra.get((size_t)cnt * 8));
+    auto* b = static_cast<double*>(ws.rb.get((size_t)cnt * 8));
+    CK(cudaMemcpyAsync(d_maps, maps, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
+    CK(cudaMemcpyAsync(a, current, (size_t)cnt * 8, cudaMemcpyHostToDevice, ws.stream));
+    launch_xform(d_maps, g.R, scale, g, xf, ws.stream);
+    launch_decode_step(a, b, xf, out_w, p.n * scale, g.RX, nullptr, ws.stream);
+    CK(cudaGetLastError());
+    g_launches += 2;
+    CK(cudaMemcpyAsync(next, b, (size_t)cnt * 8, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+    return FIC_OK;
+  });
+}
+
+int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const fic_params* params, int32_t scale,
+                   int32_t iterations, int32_t initial_kind, const uint8_t* supplied, int32_t supplied_width,
+                   int32_t supplied_height, int32_t has_eps, double convergence_eps, uint8_t* out, double* step_rmse,
+                   int32_t* iterations_run) {
+  // decode_traced (decoder.cpp:113-128) validation order
+  if (scale < 1) return fail(FIC_ERR_BAD_PARAMS, "scale must be >= 1");
+  if (iterations < 1) return fail(FIC_ERR_BAD_PARAMS, "iterations must be >= 1");
+  const int out_w = width * scale, out_h = height * scale;
+  if (initial_kind == FIC_INITIAL_SUPPLIED) {
+    if (!supplied) return fail(FIC_ERR_BAD_PARAMS, "no supplied initial image");
+    if (supplied_width != out_w || supplied_height != out_h)
+      return fail(FIC_ERR_SCALE_MISMATCH, "supplied initial image has the wrong geometry");
+  } else if (initial_kind != FIC_INITIAL_MID_GRAY && initial_kind != FIC_INITIAL_BLACK) {
+    return fail(FIC_ERR_BAD_PARAMS, "initial raster kind");
+  }
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if (width != height || width <= 0 || width % p.n != 0)
+    return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
+  if ((e = check_mappings(maps, width, height, p))) return e;
+  const Geometry g = make_geometry(width, height, p);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    const long long cnt = (long long)out_w * out_h;
+    const int blocks = decode_blocks(cnt);
+    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
+    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)g.R * sizeof(RangeXform)));
+    auto* a = static_cast<double*>(ws.ra.get((size_t)cnt * 8));
+    auto* b = static_cast<double*>(ws.rb.get((size_t)cnt * 8));
+    auto* part = static_cast<double*>(ws.partial_sums.get((size_t)blocks * 8));
+    auto* d_rmse = static_cast<double*>(ws.rmse.get((size_t)iterations * 8));
+    auto* d_u8 = static_cast<unsigned char*>(ws.u8out.get((size_t)cnt));
+    auto* h_rmse = static_cast<double*>(ws.h_rmse.get((size_t)iterations * 8));
+    CK(cudaMemcpyAsync(d_maps, maps, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
+    const unsigned char* d_sup = nullptr;
+    if (initial_kind == FIC_INITIAL_SUPPLIED) {
+      CK(cudaMemcpyAsync(d_u8, supplied, (size_t)cnt, cudaMemcpyHostToDevice, ws.stream));
+      d_sup = d_u8;
+    }
+    launch_raster_init(a, cnt, initial_kind, d_sup, ws.stream);
+    launch_xform(d_maps, g.R, scale, g, xf, ws.stream);
+    g_launches += 2;
+    int runs = 0;
+    for (int it = 0; it < iterations; ++it) {
+      launch_decode_step(a, b, xf, out_w, p.n * scale, g.RX, part, ws.stream);
+      launch_rmse_finish(part, blocks, cnt, d_rmse + it, ws.stream);
+      g_launches += 2;
+      std::swap(a, b);
+      ++runs;
+      if (has_eps) {
+        CK(cudaMemcpyAsync(h_rmse + it, d_rmse + it, 8, cudaMemcpyDeviceToHost, ws.stream));
+        CK(cudaStreamSynchronize(ws.stream));
+        if (h_rmse[it] < convergence_eps) break;
+      }
+    }
+    launch_quantize_raster(a, cnt, d_u8, ws.stream);
+    g_launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h_rmse, d_rmse, (size_t)runs * 8, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaMemcpyAsync(out, d_u8, (size_t)cnt, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+    if (step_rmse) std::memcpy(step_rmse, h_rmse, (size_t)runs * 8);
+    if (iterations_run) *iterations_run = runs;
+    return FIC_OK;
+  });
+}
+
+int32_t fic_collage_error(const uint8_t* image, int32_t img_width, int32_t img_height, const fic_mapping* maps,
+                          int32_t width, int32_t height, const fic_params* params, double* out) {
+  if (img_width != width || img_height != height)
+    return fail(FIC_ERR_DIMENSION_MISMATCH, "image does not match the encoding's geometry");
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if (width != height || width <= 0 || width % p.n != 0)
+    return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
+  if ((e = check_mappings(maps, width, height, p))) return e;
+  const Geometry g = make_geometry(width, height, p);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    const long long cnt = (long long)width * height;
+    const int blocks = decode_blocks(cnt);
+    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
+    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)g.R * sizeof(RangeXform)));
+    auto* a = static_cast<double*>(ws.ra.get((size_t)cnt * 8));
+    auto* b = static_cast<double*>(ws.rb.get((size_t)cnt * 8));
+    auto* part = static_cast<double*>(ws.partial_sums.get((size_t)blocks * 8));
+    auto* d_rmse = static_cast<double*>(ws.rmse.get(8));
+    auto* d_u8 = static_cast<unsigned char*>(ws.u8out.get((size_t)cnt));
+    CK(cudaMemcpyAsync(d_maps, maps, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
+    CK(cudaMemcpyAsync(d_u8, image, (size_t)cnt, cudaMemcpyHostToDevice, ws.stream));
+    launch_raster_init(a, cnt, FIC_INITIAL_SUPPLIED, d_u8, ws.stream);
+    launch_xform(d_maps, g.R, 1, g, xf, ws.stream);
+    launch_decode_step(a, b, xf, width, p.n, g.RX, part, ws.stream);
+    launch_rmse_finish(part, blocks, cnt, d_rmse, ws.stream);
+    g_launches += 4;
+    CK(cudaGetLastError());
+    double r = 0;
+    CK(cudaMemcpyAsync(&r, d_rmse, 8, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+    *out = r;
+    return FIC_OK;
+  });
+}
+
+int32_t fic_decoded_error_bound(double collage_rmse, double s_max, double* out) {
+  if (s_max >= 1.0) return fail(FIC_ERR_NON_CONTRACTIVE, "s_max " + std::to_string(s_max) + " admits no attractor bound");
+  if (out) *out = collage_rmse / (1.0 - s_max);
+  return FIC_OK;
+}
+
+uint64_t fic_kernel_launch_count(void) { return g_launches.load(); }
+
+int32_t fic_matcher_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
+  std::lock_guard<std::mutex> lock(g_timing_mu);
+  if (avg_ms) *avg_ms = g_timing_n ? g_timing_ms / (double)g_timing_n : 0.0;
+  if (launches) *launches = g_timing_n;
+  if (reset) {
+    g_timing_ms = 0.0;
+    g_timing_n = 0;
+  }
+  return FIC_OK;
+}
+
+void fic_set_matcher_timing(int32_t enabled) { g_timing.store(enabled ? 1 : 0); }
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+"""GPU parity of the iterated decoder (K3) against the oracle.
+
+Every fp64 raster value is computed in the reference's operation order, so rasters
+and the final uint8 image are bit-exact; step RMSE uses a fixed-order tree reduction
+instead of the reference's sequential sum, so it is checked to 1e-12 relative.
+"""
+import numpy as np
+import pytest
+
+import paper_1404_0774_b200 as fic
+from paper_1404_0774_b200 import images
+
+pytestmark = pytest.mark.gpu
+
+
+def _enc(oracle, img, **pv):
+    maps, _ = oracle.encode(img, pv)
+    return fic.EncodedImage(img.shape[1], img.shape[0], fic.CodecParams(**pv), maps)
+
+
+@pytest.mark.parametrize("scale", [1, 2, 3])
+def test_decode_step_bit_exact(oracle, scale):
+    img = oracle.smooth_image(32, 61)
+    enc = _enc(oracle, img, s_max=0.9)
+    rng = np.random.default_rng(5)
+    cur = rng.uniform(-20, 300, size=(32 * scale, 32 * scale))
+    got = fic.decode_step(cur, enc, scale)
+    want = oracle.decode_step(cur, enc.mappings, 32, dict(s_max=0.9), scale)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("initial", ["mid-gray", "black", "supplied"])
+@pytest.mark.parametrize("scale", [1, 2])
+def test_decode_bit_exact(oracle, initial, scale):
+    img = oracle.smooth_image(64, 64)
+    enc = _enc(oracle, img, n=4, step=2)
+    init = initial
+    if initial == "supplied":
+        init = oracle.noise_image(64 * scale, 9)
+    out, rm, runs = fic.decode_traced(enc, scale=scale, iterations=10, initial=init)
+    wout, wrm, wruns = oracle.decode(enc.mappings, 64, dict(n=4, step=2), scale, 10, init)
+    assert np.array_equal(out, wout)
+    assert runs == wruns == 10
+    np.testing.assert_allclose(rm, wrm, rtol=1e-12, atol=1e-300)
+
+
+def test_cfg1_decode_psnr(oracle):
+    img = images.phantom(256, 1404001)
+    pv = dict(n=8, step=8)
+    enc = fic.encode(img, fic.CodecParams(**pv))
+    out = fic.decode(enc, iterations=10)
+    wmaps, _ = oracle.encode_threaded(img, pv)
+    wout, _, _ = oracle.decode(wmaps, 256, pv, 1, 10)
+    assert np.array_equal(out, wout)
+    assert abs(fic.psnr(img, out) - oracle.psnr(img, wout)) < 0.01
+
+
+def test_early_stop_and_constants(oracle):
+    # test_decoder.cpp:90-98: one step reaches the fixed point, the second proves it
+    img = np.full((16, 16), 200, np.uint8)
+    enc = fic.encode(img)
+    _, rm, runs = fic.decode_traced(enc, convergence_eps=1e-12)
+    assert runs == 2
+    # representable constants decode exactly in one iteration (test_decoder.cpp:27-35)
+    for v in (0, 255):
+        img = np.full((16, 16), v, np.uint8)
+        assert np.array_equal(fic.decode(fic.encode(img), iterations=1), img)
+
+
+def test_collage_error(oracle):
+    img = oracle.noise_image(16, 65)
+    enc = fic.encode(img)
+    expected = np.sqrt(np.sum(enc.mappings["residual"]) / img.size)
+    ce = fic.collage_error(img, enc)
+    assert ce == pytest.approx(expected, rel=1e-6)
+    assert ce == pytest.approx(oracle.collage_error(img, enc.mappings, {}), rel=1e-12)
+
+
+def test_monotone_step_rmse(oracle):
+    img = oracle.smooth_image(32, 64)
+    enc = fic.encode(img, fic.CodecParams(s_max=0.9))
+    _, rm, runs = fic.decode_traced(enc)
+    assert runs == 16
+    assert all(rm[t + 1] <= rm[t] + 1e-9 for t in range(1, len(rm) - 1))
+
+
+def test_decode_errors():
+    img = np.zeros((16, 16), np.uint8)
+    img[::2] = 255
+    enc = fic.encode(img)
+    with pytest.raises(fic.CodecError, match="BadParams"):
+        fic.decode(enc, scale=0)
+    with pytest.raises(fic.CodecError, match="BadParams"):
+        fic.decode(enc, iterations=0)
+    with pytest.raises(fic.CodecError, match="ScaleMismatch"):
+        fic.decode(enc, initial=np.zeros((8, 8), np.uint8))
+    with pytest.raises(fic.CodecError, match="DimensionMismatch"):
+        fic.collage_error(np.zeros((32, 32), np.uint8), enc)
+    with pytest.raises(fic.CodecError, match="NonContractive"):
+        fic.decoded_error_bound(1.0, 1.0)
