@@ -1,0 +1,330 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 fractal encoder — BASELINE.json's metric:
+range-domain comparisons/sec (and encode ms/image) vs the CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+Workload (N=1): cfg2 = BASELINE.json configs[1], a 512x512 synthetic CT slice, 8x8 ranges,
+domain stride 4, 8 isometries, full search.  A "step" encodes one image: pool build (K1),
+range pass, tcgen05 matcher (K2), finalize — with the image resident in HBM (`value`) or
+through the public API with host buffers (`e2e`, H2D + D2H inside the timed region).
+Under torchrun (N>1) every rank encodes its own slice (weak scaling, like cfg5's
+slice sharding) and the code records are gathered to rank 0 with NCCL inside the step.
+
+The unit of work is one comparison = one (range, domain, isometry) candidate, counted as
+EncodeStats.candidates_tested (proj/include/fic/encoder.hpp:50), identical for CPU and GPU.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "range-domain comparisons/sec and encode ms/image at 1/2/4/8 B200 vs CPU ref"
+UNIT = "comparisons/s"
+CONFIG_TEXT = {
+    "cfg1": "256x256 synthetic phantom, 8x8 ranges, 16x16 domains stride 8, 8 isometries, full search",
+    "cfg2": "512x512 CT-slice-shaped synthetic image, 8x8 ranges, domain stride 4, 8 isometries, full search",
+    "cfg3": "512x512 synthetic image, 4x4 ranges, 8x8 domains stride 2, 8 isometries, full search",
+    "cfg4": "2048x2048 X-ray-shaped synthetic image, 8x8 ranges, domain stride 2, 8 isometries, full search",
+}
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def make_image(cfg, rank=0):
+    from paper_1404_0774_b200 import images
+    gen, n, step = images.CONFIGS[cfg]
+    if rank == 0 or cfg not in ("cfg2", "cfg3"):
+        img = gen()
+    else:  # weak scaling: each rank its own slice of the cfg5-style volume
+        img = images.ct_slice(512, 1404002 + rank, rank / 512.0)
+    return img, n, step
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        time.sleep(0.15)
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 1590.0, 6650.0, "fallback"
+
+
+def traffic_for(cfg):
+    """dram bytes per matcher launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "matcher_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg)
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(img, n, step, target_ranges, threads):
+    """The reference's own encoder (oracle/_ref/libfic_ref.so, compiled from its sources) on a
+    bounded, evenly strided sample of ranges via encode_range (encoder.cpp:332-342 — the same
+    per-range search encode_parallel runs), spread over `threads` host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import Reference
+    ref = Reference()
+    side = img.shape[0]
+    R = (side // n) ** 2
+    stride = max(1, R // target_ranges)
+    idx = np.arange(0, R, stride)[:target_ranges]
+    pv = dict(n=n, step=step)
+
+    def work(chunk):
+        c = 0
+        for r in chunk:
+            _, st = ref.encode_range(img, int(r % (side // n)) * n, int(r // (side // n)) * n, pv)
+            c += st["candidates_tested"]
+        return c
+
+    chunks = [idx[i::threads] for i in range(threads)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        comps = sum(ex.map(work, chunks))
+    dt = time.perf_counter() - t0
+    return comps, dt, len(idx), R
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    img, n, step = make_image(args.config)
+    threads = os.cpu_count() or 1
+    target = args.ref_ranges
+    vals = []
+    for i in range(args.warmup + args.steps):
+        comps, dt, used, R = cpu_reference_sample(img, n, step, target, threads)
+        if i >= args.warmup:
+            vals.append((comps, dt))
+    comps = sum(c for c, _ in vals)
+    secs = sum(d for _, d in vals)
+    value = comps / secs
+    sample = f"{used} of {R} ranges (evenly strided) per step via the reference encode_range, {threads} threads"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / len(vals) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic", "config": {"workload": CONFIG_TEXT[args.config], "cfg": args.config, "n": n, "step": step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "encode_ms_per_image_extrapolated": (R / used) * (secs / len(vals)) * 1e3,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1404_0774_b200 as fic
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    fic.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    img, n, step = make_image(args.config, rank)
+    side = img.shape[0]
+    R = (side // n) ** 2
+    params = fic.CodecParams(n=n, step=step)
+    stream = torch.cuda.current_stream()
+    d_img = torch.from_numpy(img).cuda()
+    d_out = torch.empty(R * 32, dtype=torch.uint8, device="cuda")
+    gather = torch.empty(world * R * 32, dtype=torch.uint8, device="cuda") if world > 1 else None
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    stats = fic.encode_device(d_img.data_ptr(), side, side, d_out.data_ptr(), params, stream.cuda_stream, stats=True)
+    comps = stats["candidates_tested"]
+
+    def step_fn():
+        fic.encode_device(d_img.data_ptr(), side, side, d_out.data_ptr(), params, stream.cuda_stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gather, d_out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step_fn()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region (per-step events, L2 flushed between steps) ----
+    fic.set_matcher_timing(True)
+    fic.matcher_timing(reset=True)
+    launches0 = fic.kernel_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            barrier()
+            torch.cuda.synchronize()
+            evs[i][0].record(stream)
+            step_fn()
+            evs[i][1].record(stream)
+            torch.cuda.synchronize()
+    launches = fic.kernel_launch_count() - launches0
+    matcher_ms, matcher_n = fic.matcher_timing(reset=True)
+    fic.set_matcher_timing(False)
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = comps * world * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end through the public API (host image in, host records out) ----
+    e2e_steps = max(args.steps, 5)
+    for _ in range(2):
+        fic.encode(img, params)
+    e2e_times = []
+    for i in range(e2e_steps):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        enc = fic.encode(img, params)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = comps * world * e2e_steps / float(e2e_s.item())
+
+    line = None
+    if rank == 0:
+        bf16, hbm, src = peaks()
+        flops = 2.0 * n * n * comps  # algorithmic ops per matcher launch: 2 n^2 per comparison
+        achieved = flops / (matcher_ms / 1e3) / 1e12 if matcher_ms > 0 else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp16(exact-int)+f64",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[args.config], "cfg": args.config, "image": f"{side}x{side}", "n": n,
+                       "step": step, "ranges": R, "domains": ((side - 2 * n) // step + 1) ** 2,
+                       "comparisons_per_image": comps, "l2": "flushed between timed steps (256 MB write)",
+                       "parallelism": f"weak: {world} rank(s) x 1 image, codes all-gathered over NCCL"
+                       if world > 1 else "1 GPU"},
+            "encode_ms_per_image": ms_per_step,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": side * side,
+                    "d2h_bytes_per_step": R * 32 + 16,
+                    "encode_ms_per_image": float(e2e_s.item()) / e2e_steps * 1e3,
+                    "api": "paper_1404_0774_b200.encode (C-ABI fic_encode)"},
+            "roofline": {"bound": "tensor", "kernel": "matcher_tc_kernel", "achieved": achieved, "peak": bf16,
+                         "unit": "TFLOP/s", "frac": (achieved / bf16) if achieved else None,
+                         "peak_source": f"{src} dense bf16/fp16 (the matcher issues kind::f16 MMAs)",
+                         "frac_of_int8_peak": (achieved / (2 * bf16)) if achieved else None,
+                         "matcher_ms": matcher_ms, "matcher_launches_timed": matcher_n,
+                         "ops_per_comparison": 2 * n * n, "traffic": traffic_for(args.config)},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if args.cpu_baseline:
+            threads = os.cpu_count() or 1
+            c_comps, c_dt, used, RR = cpu_reference_sample(img, n, step, args.ref_ranges, threads)
+            line["cpu_baseline"] = {
+                "value": c_comps / c_dt, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{used} of {RR} ranges (evenly strided) via the reference encode_range, {threads} threads",
+                "encode_ms_per_image_extrapolated": (RR / used) * c_dt * 1e3}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIG_TEXT))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-ranges", type=int, default=1024, help="ranges per CPU-reference sample")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

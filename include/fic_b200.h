@@ -144,6 +144,13 @@ int32_t fic_collage_error(const uint8_t* image, int32_t img_width, int32_t img_h
 /* decoded_error_bound (proj/src/decoder.cpp:142-146); host only. */
 int32_t fic_decoded_error_bound(double collage_rmse, double s_max, double* out);
 
+/* ---- device selection ---- */
+/* Make `device` the current CUDA device of the calling thread for this library's calls
+ * (the library links its own CUDA runtime, so a caller's framework-level device choice
+ * does not carry over).  Returns FIC_ERR_CUDA for an invalid ordinal. */
+int32_t fic_set_device(int32_t device);
+int32_t fic_device_count(int32_t* count);
+
 /* ---- instrumentation ---- */
 /* Number of this library's kernels launched since load (all devices). */
 uint64_t fic_kernel_launch_count(void);

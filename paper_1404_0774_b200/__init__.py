@@ -15,6 +15,7 @@ from .codec import (
     decoded_error_bound,
     encode,
     encode_batch,
+    encode_device,
     encode_range,
     encode_rows,
     encode_with_stats,
@@ -22,6 +23,7 @@ from .codec import (
     matcher_timing,
     psnr,
     rmse,
+    set_device,
     set_matcher_timing,
     validate_geometry,
 )
@@ -44,10 +46,12 @@ __all__ = [
     "decode_step",
     "decode_traced",
     "encode_batch",
+    "encode_device",
     "encode_range",
     "encode_rows",
     "encode_with_stats",
     "kernel_launch_count",
     "matcher_timing",
+    "set_device",
     "set_matcher_timing",
 ]

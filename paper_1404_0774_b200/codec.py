@@ -270,6 +270,23 @@ def psnr(a, b):
     return float(20.0 * np.log10(255.0 / e))
 
 
+def set_device(device):
+    """(extension) select the CUDA device for this thread's codec calls."""
+    _check(lib().fic_set_device(int(device)))
+
+
+def encode_device(d_image_ptr, width, height, d_out_ptr, params=None, stream=0, stats=False):
+    """(extension) device-resident encode: raw device pointers (e.g. torch tensor data_ptr())
+    of a uint8 image and a (width/n)^2 x 32-byte record buffer, enqueued on `stream`
+    (a cudaStream_t handle as int).  Returns stats when `stats` (synchronises)."""
+    params = CodecParams() if params is None else params
+    st = FicStats()
+    _check(lib().fic_encode_device(ctypes.c_void_p(d_image_ptr), int(width), int(height),
+                                   ctypes.byref(params.struct), ctypes.c_void_p(d_out_ptr),
+                                   ctypes.byref(st) if stats else None, ctypes.c_void_p(stream)))
+    return st.as_dict() if stats else None
+
+
 def kernel_launch_count():
     """(extension) number of this library's kernels launched so far."""
     return int(lib().fic_kernel_launch_count())

@@ -160,68 +160,135 @@ constexpr float kBoundSlack = 4.0f;
 // Range-side state held by one epilogue thread.
 struct RangeState {
   int x0, y0;         // range origin in pixels
+  int r;              // encoded-range index (row into the global best array)
   int sb;             // sum of pixels
   double ssb;         // range_var / N
   double best;        // best residual so far (own candidates)
-  double thr;         // min(best, other scanners' best) used for pruning
+  double thr;         // min(best, best any scanner has published) used for pruning
   float sqrtT;
   int bd, bs;         // best domain / isometry (-1 = none)
   unsigned bqs, bqo;
   bool active;        // non-shadow range inside the image
 };
 
-// Exact evaluation of the 8 isometries of domain d for one range, following
-// Searcher::search_impl (proj/src/encoder.cpp:236-287) operation by operation.
-// `acc` holds the 8 exact correlations sum_i q[perm_s(i)] * b_i.  Candidates are
-// visited in isometry order and replace the best only on strict `<`.
-static __device__ __noinline__ void evaluate_domain(RangeState& st, const Geometry& g, int d, const long long* acc,
-                                             const DomainMetaI* __restrict__ meta_i,
-                                             const unsigned char* __restrict__ pool,
-                                             const unsigned char* __restrict__ img) {
-  const DomainMetaI mi = meta_i[d];
-  if (mi.den < 0) return;  // flat code block: never a candidate (encoder.cpp:223-229)
-  const int N = g.N;
+// Shared pruning bar: every scanner publishes the residuals it achieves per range
+// (atomicMin on the IEEE bits: non-negative doubles order like unsigned integers), so
+// all CTAs and epilogue groups working on a range prune against the best value any of
+// them has reached.  Any achieved residual is a valid bar: a candidate whose lower
+// bound exceeds it cannot be the (R, domain, isometry)-lexicographic minimum.
+__device__ __forceinline__ void publish_best(unsigned long long* gbest, int r, double v) {
+  if (gbest) atomicMin(gbest + r, (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ void refresh_thr(RangeState& st, const unsigned long long* gbest, int N) {
+  if (!gbest || !st.active) return;
+  const double gb = __longlong_as_double((long long)__ldcg(gbest + st.r));
+  if (gb < st.thr) {
+    st.thr = gb;
+    st.sqrtT = prune_sqrtT(st.ssb, st.thr, N);
+  }
+}
+
+// Diagnostic counters (Geometry::flags bit 2): [0] domain groups tested, [1] groups
+// surviving the 8-isometry bound, [2] isometries passing the tight bound, [3] exact
+// residual evaluations.
+__device__ __forceinline__ void count(unsigned long long* c, int i, const Geometry& g) {
+  if ((g.flags & 4) && c) atomicAdd(c + i, 1ull);
+}
+
+// Reference-exact evaluation of one candidate (domain d, isometry s) for a range with
+// pixel sum sb and ssb = range_var/N, following Searcher::search_impl
+// (proj/src/encoder.cpp:236-280) operation by operation.  Returns its residual, or +inf
+// when a bound shows it cannot beat `thr` (an achieved residual; the screens are the
+// reference's own, with its +1e-3 margins, plus the unconstrained-LS bound).
+// NN > 0: N == NN and the range pixels come packed in `bpk` (pixel i in byte i%4 of
+// word i/4) so the residual loop is unrolled over 16-byte pool loads; NN == 0: any N,
+// pixels read from the image at (x0, y0).
+template <int NN>
+__device__ __forceinline__ double eval_candidate(const Geometry& g, int d, int s, long long acc, const DomainMetaI& mi,
+                                                 int sb, double ssb, double thr, const uint32_t* bpk,
+                                                 const unsigned char* __restrict__ pool,
+                                                 const unsigned char* __restrict__ img, int x0, int y0, unsigned& qs_out,
+                                                 unsigned& qo_out, unsigned long long* counters) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const int N = NN > 0 ? NN : g.N;
   const double count_d = (double)N;
   const double inv_count = 1.0 / count_d;
   const double den_d = (double)mi.den;
   const double sa_d = __dmul_rn((double)mi.sq, 0.25);
-  const long long sqsb = mi.sq * (long long)st.sb;
-  const double sb_d = (double)st.sb;
+  const double sb_d = (double)sb;
   const double smax = g.s_max;
-  for (int s = 0; s < kSyms; ++s) {
-    const long long accv = acc[s];
-    const long long num_q = (long long)N * accv - sqsb;
-    const double num_d = (double)num_q;
-    // Tight unconstrained-LS bound against the best residual any scanner holds.
-    {
-      const double rstar = st.ssb - (num_d * num_d) / (count_d * den_d);
-      if (!(g.flags & 2) && rstar >= st.thr + 1e-6 * (1.0 + st.thr)) continue;
+  const long long num_q = (long long)N * acc - mi.sq * (long long)sb;
+  const double num_d = (double)num_q;
+  if (!(g.flags & 2)) {  // tight unconstrained-LS bound
+    const double rstar = ssb - (num_d * num_d) / (count_d * den_d);
+    if (rstar >= thr + 1e-6 * (1.0 + thr)) return inf;
+  }
+  count(counters, 2, g);
+  const double s_raw = __ddiv_rn(__dmul_rn(4.0, num_d), den_d);
+  const double sc = clampd(s_raw, -smax, smax);
+  const unsigned qs = quantize(sc, smax, g.s_bits);
+  const double s_deq = dequantize(qs, smax, g.s_bits);
+  const double cov = __dmul_rn(__dmul_rn(num_d, 0.25), inv_count);
+  const double var_a = __dmul_rn(__dmul_rn(den_d, 0.0625), inv_count);
+  const double parabola =
+      __dadd_rn(__dsub_rn(ssb, __dmul_rn(__dmul_rn(2.0, s_deq), cov)), __dmul_rn(__dmul_rn(s_deq, s_deq), var_a));
+  if (!(g.flags & 2) && parabola >= thr + 1e-3) return inf;  // encoder.cpp:263
+  const double o = clampd(__dmul_rn(__dsub_rn(sb_d, __dmul_rn(sc, sa_d)), inv_count), -255.0, 255.0);
+  const unsigned qo = quantize(o, 255.0, g.o_bits);
+  const double o_deq = dequantize(qo, 255.0, g.o_bits);
+  const double o_gap = __dsub_rn(o_deq, __dmul_rn(__dsub_rn(sb_d, __dmul_rn(s_deq, sa_d)), inv_count));
+  const double screen = __dadd_rn(parabola, __dmul_rn(__dmul_rn(count_d, o_gap), o_gap));
+  if (!(g.flags & 2) && screen >= thr + 1e-3) return inf;  // encoder.cpp:272
+  count(counters, 3, g);
+  // Exact residual in range-pixel order (encoder.cpp:274-280).
+  double r_val = 0.0;
+  if constexpr (NN > 0) {
+    const unsigned char* col = pool + (long long)d * (NN < 16 ? 16 : NN) * 16 + s * 16;
+#pragma unroll
+    for (int kc = 0; kc < (NN + 7) / 8; ++kc) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(col + kc * 128));
+      const __half* h = reinterpret_cast<const __half*>(&v);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int i = kc * 8 + t;
+        if (i < NN) {
+          const double ai = __dmul_rn((double)__half2float(h[t]), 0.25);
+          const double bi = (double)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+          const double dd = __dsub_rn(__dadd_rn(__dmul_rn(s_deq, ai), o_deq), bi);
+          r_val = __dadd_rn(r_val, __dmul_rn(dd, dd));
+        }
+      }
     }
-    const double s_raw = __ddiv_rn(__dmul_rn(4.0, num_d), den_d);
-    const double sc = clampd(s_raw, -smax, smax);
-    const unsigned qs = quantize(sc, smax, g.s_bits);
-    const double s_deq = dequantize(qs, smax, g.s_bits);
-    const double cov = __dmul_rn(__dmul_rn(num_d, 0.25), inv_count);
-    const double var_a = __dmul_rn(__dmul_rn(den_d, 0.0625), inv_count);
-    const double parabola =
-        __dadd_rn(__dsub_rn(st.ssb, __dmul_rn(__dmul_rn(2.0, s_deq), cov)), __dmul_rn(__dmul_rn(s_deq, s_deq), var_a));
-    if (!(g.flags & 2) && parabola >= st.thr + 1e-3) continue;  // encoder.cpp:263 (any achieved R is a valid bar)
-    const double o = clampd(__dmul_rn(__dsub_rn(sb_d, __dmul_rn(sc, sa_d)), inv_count), -255.0, 255.0);
-    const unsigned qo = quantize(o, 255.0, g.o_bits);
-    const double o_deq = dequantize(qo, 255.0, g.o_bits);
-    const double o_gap = __dsub_rn(o_deq, __dmul_rn(__dsub_rn(sb_d, __dmul_rn(s_deq, sa_d)), inv_count));
-    const double screen = __dadd_rn(parabola, __dmul_rn(__dmul_rn(count_d, o_gap), o_gap));
-    if (!(g.flags & 2) && screen >= st.thr + 1e-3) continue;  // encoder.cpp:272
-    // Exact residual in range-pixel order (encoder.cpp:274-280).
-    double r_val = 0.0;
+  } else {
     const int n = g.n;
     for (int i = 0; i < N; ++i) {
       const __half qh = *reinterpret_cast<const __half*>(pool + pool_offset(d, s, i, g.K));
       const double ai = __dmul_rn((double)__half2float(qh), 0.25);
-      const double bi = (double)img[(long long)(st.y0 + i / n) * g.W + st.x0 + (i % n)];
+      const double bi = (double)img[(long long)(y0 + i / n) * g.W + x0 + (i % n)];
       const double dd = __dsub_rn(__dadd_rn(__dmul_rn(s_deq, ai), o_deq), bi);
       r_val = __dadd_rn(r_val, __dmul_rn(dd, dd));
     }
+  }
+  qs_out = qs;
+  qo_out = qo;
+  return r_val;
+}
+
+// The 8 isometries of domain d for the range held in `st`, in isometry order, each
+// replacing the best only on strict `<` (encoder.cpp:281).
+template <int NN>
+static __device__ __noinline__ void evaluate_domain(RangeState& st, const Geometry& g, int d, const long long* acc,
+                                                    const DomainMetaI* __restrict__ meta_i,
+                                                    const unsigned char* __restrict__ pool,
+                                                    const unsigned char* __restrict__ img, const uint32_t* bpk,
+                                                    unsigned long long* gbest, unsigned long long* counters) {
+  const DomainMetaI mi = meta_i[d];
+  if (mi.den < 0) return;  // flat code block: never a candidate (encoder.cpp:223-229)
+  for (int s = 0; s < kSyms; ++s) {
+    unsigned qs = 0, qo = 0;
+    const double r_val =
+        eval_candidate<NN>(g, d, s, acc[s], mi, st.sb, st.ssb, st.thr, bpk, pool, img, st.x0, st.y0, qs, qo, counters);
     if (r_val < st.best) {
       st.best = r_val;
       st.bd = d;
@@ -230,9 +297,26 @@ static __device__ __noinline__ void evaluate_domain(RangeState& st, const Geomet
       st.bqo = qo;
       if (r_val < st.thr) {
         st.thr = r_val;
-        st.sqrtT = prune_sqrtT(st.ssb, st.thr, N);
+        st.sqrtT = prune_sqrtT(st.ssb, st.thr, NN > 0 ? NN : g.N);
+        publish_best(gbest, st.r, r_val);
       }
     }
+  }
+}
+
+// Range pixels of (x0, y0) packed 4 per word (NN pixels, NN % 4 == 0).
+template <int NN>
+__device__ __forceinline__ void load_range_packed(const unsigned char* __restrict__ img, const Geometry& g, int x0,
+                                                  int y0, uint32_t* bpk) {
+#pragma unroll
+  for (int w = 0; w < NN / 4; ++w) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = w * 4 + b;
+      v |= (uint32_t)img[(long long)(y0 + i / g.n) * g.W + x0 + i % g.n] << (8 * b);
+    }
+    bpk[w] = v;
   }
 }
 

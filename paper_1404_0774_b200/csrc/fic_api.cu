@@ -23,9 +23,13 @@ void launch_pool_build(const unsigned char*, const Geometry&, unsigned char*, Do
                        unsigned long long*, cudaStream_t);
 void launch_range_pass(const unsigned char*, const Geometry&, RangeMeta*, unsigned long long*, cudaStream_t);
 void launch_matcher_simt(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
-                         const DomainMetaI*, const RangeMeta*, int, int, Partial*, cudaStream_t);
+                         const DomainMetaI*, const RangeMeta*, int, int, Partial*, unsigned long long*,
+                         unsigned long long*, cudaStream_t);
 cudaError_t launch_matcher_tc(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
-                              const DomainMetaI*, const RangeMeta*, int, int, Partial*, cudaStream_t);
+                              const DomainMetaI*, const RangeMeta*, int, int, Partial*, unsigned long long*,
+                              unsigned long long*, cudaStream_t);
+void launch_seed(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaI*, const RangeMeta*,
+                 unsigned long long*, cudaStream_t);
 bool tc_supported(const Geometry&);
 void launch_finalize(const unsigned char*, const Geometry&, const RangeMeta*, const Partial*, int, fic_mapping*,
                      cudaStream_t);
@@ -173,7 +177,8 @@ struct Workspace {
   int sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out;
+  DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
+      diag;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse;
   std::mutex mu;
 };
@@ -225,21 +230,35 @@ void enqueue_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g
   n_chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
   const int n_slots = mode == 1 ? 2 * n_chunks : n_chunks;
   auto* parts = static_cast<Partial*>(ws.partials.get((size_t)n_slots * g.R * sizeof(Partial)));
+  auto* gbest = static_cast<unsigned long long*>(ws.gbest.get((size_t)g.R * sizeof(unsigned long long)));
+  unsigned long long* diag = nullptr;
+  if (g.flags & 4) {
+    diag = static_cast<unsigned long long*>(ws.diag.get(8 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), st));
+  }
 
   CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
   launch_pool_build(d_img, g, pool, mf, mi, d_counters, st);
   launch_range_pass(d_img, g, rm, d_counters + 1, st);
+  launch_seed(d_img, g, pool, mi, rm, gbest, st);
   const bool timed = g_timing.load() != 0;
   if (timed) CK(cudaEventRecord(ws.ev0, st));
   if (mode == 1) {
-    CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, st));
+    CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, gbest, diag, st));
   } else {
-    launch_matcher_simt(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, st);
+    launch_matcher_simt(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, gbest, diag, st);
   }
   if (timed) CK(cudaEventRecord(ws.ev1, st));
   launch_finalize(d_img, g, rm, parts, n_slots, d_out, st);
   CK(cudaGetLastError());
-  g_launches += 4;
+  g_launches += 5;
+  if (diag) {
+    unsigned long long h[8];
+    CK(cudaMemcpyAsync(h, diag, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[fic diag] R=%d D=%d chunks=%d groups=%llu survive=%llu (%.4f%%) tight=%llu exact=%llu\n",
+                 g.R, g.D, n_chunks, h[0], h[1], h[0] ? 100.0 * h[1] / h[0] : 0.0, h[2], h[3]);
+  }
 }
 
 void collect_timing(Workspace& ws) {
@@ -595,6 +614,20 @@ int32_t fic_collage_error(const uint8_t* image, int32_t img_width, int32_t img_h
 int32_t fic_decoded_error_bound(double collage_rmse, double s_max, double* out) {
   if (s_max >= 1.0) return fail(FIC_ERR_NON_CONTRACTIVE, "s_max " + std::to_string(s_max) + " admits no attractor bound");
   if (out) *out = collage_rmse / (1.0 - s_max);
+  return FIC_OK;
+}
+
+int32_t fic_set_device(int32_t device) {
+  const cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(FIC_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return FIC_OK;
+}
+
+int32_t fic_device_count(int32_t* count) {
+  int c = 0;
+  const cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) return fail(FIC_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  if (count) *count = c;
   return FIC_OK;
 }
 

@@ -14,36 +14,41 @@ constexpr int kStageBytes = 16384;
 
 // n <= 8: acc in fp32 is exact (64 * 1020 * 255 < 2^24); b lives in registers and the
 // 8-isometry group test runs before any exact work.
-template <int K>
+template <int NN>
 __global__ void __launch_bounds__(kSimtThreads)
 matcher_simt_small(const unsigned char* __restrict__ img, Geometry g, const unsigned char* __restrict__ pool,
                    const DomainMetaF* __restrict__ meta_f, const DomainMetaI* __restrict__ meta_i,
-                   const RangeMeta* __restrict__ rmeta, int tiles_per_chunk, Partial* __restrict__ partials) {
+                   const RangeMeta* __restrict__ rmeta, int tiles_per_chunk, Partial* __restrict__ partials,
+                   unsigned long long* __restrict__ gbest, unsigned long long* __restrict__ counters) {
+  constexpr int K = NN < 16 ? 16 : NN;
   __shared__ __align__(16) unsigned char stage[kStageBytes];
   constexpr int kDomBytes = K * 16;
   constexpr int kStageDomains = kStageBytes / kDomBytes;
   const int tid = threadIdx.x;
   const int r = blockIdx.x * kSimtThreads + tid;
   RangeState st;
+  st.r = r;
   st.active = false;
   st.best = st.thr = __longlong_as_double(0x7ff0000000000000ll);
   st.bd = -1;
   st.bs = 0;
   st.bqs = st.bqo = 0;
   st.sqrtT = -1e30f;
-  float b[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) b[k] = 0.f;
+  st.x0 = st.y0 = 0;
+  st.sb = 0;
+  st.ssb = 0.0;
   if (r < g.R) {
     const RangeMeta m = rmeta[r];
     range_origin(g, r, st.x0, st.y0);
     st.sb = m.sb;
     st.ssb = (double)m.var / (double)g.N;
     st.active = !m.shadow;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (k < g.N) b[k] = (float)img[(long long)(st.y0 + k / g.n) * g.W + st.x0 + k % g.n];
   }
+  uint32_t bpk[NN / 4];
+  load_range_packed<NN>(img, g, st.x0, st.y0, bpk);
+  float b[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) b[k] = k < NN ? (float)((bpk[k >> 2] >> (8 * (k & 3))) & 0xFFu) : 0.f;
   const float sb_f = (float)st.sb;
   const int t0 = blockIdx.y * tiles_per_chunk;
   const int d_begin = t0 * kDomainsPerTile;
@@ -58,6 +63,7 @@ matcher_simt_small(const unsigned char* __restrict__ img, Geometry g, const unsi
     }
     __syncthreads();
     if (!st.active) continue;
+    refresh_thr(st, gbest, NN);
     for (int j = 0; j < nd; ++j) {
       const int d = d0 + j;
       const unsigned char* blk = stage + j * kDomBytes;
@@ -82,11 +88,13 @@ matcher_simt_small(const unsigned char* __restrict__ img, Geometry g, const unsi
       uint32_t bits[kSyms];
 #pragma unroll
       for (int s = 0; s < kSyms; ++s) bits[s] = __float_as_uint(acc[s]);
+      count(counters, 0, g);
       if (!(g.flags & 1) && group_pruned(bits, mf.a, mf.e, sb_f, st.sqrtT)) continue;
+      count(counters, 1, g);
       long long acc_ll[kSyms];
 #pragma unroll
       for (int s = 0; s < kSyms; ++s) acc_ll[s] = (long long)acc[s];
-      evaluate_domain(st, g, d, acc_ll, meta_i, pool, img);
+      evaluate_domain<NN>(st, g, d, acc_ll, meta_i, pool, img, bpk, gbest, counters);
     }
   }
   if (r < g.R) partials[(long long)blockIdx.y * g.R + r] = Partial{st.best, st.bd, st.bs, st.bqs, st.bqo};
@@ -94,14 +102,34 @@ matcher_simt_small(const unsigned char* __restrict__ img, Geometry g, const unsi
 
 // Any n: exact integer correlations read straight from the pool and the image
 // (fp32 partial sums over <= 64 terms are exact; they are folded into int64).
+__device__ __forceinline__ void exact_acc_generic(const Geometry& g, const unsigned char* __restrict__ pool,
+                                                  const unsigned char* __restrict__ img, int x0, int y0, int d,
+                                                  long long* acc) {
+  for (int s = 0; s < kSyms; ++s) {
+    long long total = 0;
+    for (int k0 = 0; k0 < g.N; k0 += 64) {
+      float part = 0.f;
+      for (int k = k0; k < min(g.N, k0 + 64); ++k) {
+        const float q = __half2float(*reinterpret_cast<const __half*>(pool + pool_offset(d, s, k, g.K)));
+        const float bv = (float)img[(long long)(y0 + k / g.n) * g.W + x0 + k % g.n];
+        part = __fmaf_rn(q, bv, part);
+      }
+      total += (long long)part;
+    }
+    acc[s] = total;
+  }
+}
+
 __global__ void __launch_bounds__(kSimtThreads)
 matcher_simt_generic(const unsigned char* __restrict__ img, Geometry g, const unsigned char* __restrict__ pool,
                      const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
-                     int tiles_per_chunk, Partial* __restrict__ partials) {
+                     int tiles_per_chunk, Partial* __restrict__ partials, unsigned long long* __restrict__ gbest,
+                     unsigned long long* __restrict__ counters) {
   const int r = blockIdx.x * kSimtThreads + threadIdx.x;
   if (r >= g.R) return;
   RangeState st;
   const RangeMeta m = rmeta[r];
+  st.r = r;
   range_origin(g, r, st.x0, st.y0);
   st.sb = m.sb;
   st.ssb = (double)m.var / (double)g.N;
@@ -117,21 +145,11 @@ matcher_simt_generic(const unsigned char* __restrict__ img, Geometry g, const un
   if (st.active) {
     for (int d = d_begin; d < d_end; ++d) {
       if (meta_i[d].den < 0) continue;
+      if ((d & 31) == 0) refresh_thr(st, gbest, g.N);
       long long acc[kSyms];
-      for (int s = 0; s < kSyms; ++s) {
-        long long total = 0;
-        for (int k0 = 0; k0 < g.N; k0 += 64) {
-          float part = 0.f;
-          for (int k = k0; k < min(g.N, k0 + 64); ++k) {
-            const float q = __half2float(*reinterpret_cast<const __half*>(pool + pool_offset(d, s, k, g.K)));
-            const float bv = (float)img[(long long)(st.y0 + k / g.n) * g.W + st.x0 + k % g.n];
-            part = __fmaf_rn(q, bv, part);
-          }
-          total += (long long)part;
-        }
-        acc[s] = total;
-      }
-      evaluate_domain(st, g, d, acc, meta_i, pool, img);
+      exact_acc_generic(g, pool, img, st.x0, st.y0, d, acc);
+      count(counters, 1, g);
+      evaluate_domain<0>(st, g, d, acc, meta_i, pool, img, nullptr, gbest, counters);
     }
   }
   partials[(long long)blockIdx.y * g.R + r] = Partial{st.best, st.bd, st.bs, st.bqs, st.bqo};
@@ -139,14 +157,77 @@ matcher_simt_generic(const unsigned char* __restrict__ img, Geometry g, const un
 
 void launch_matcher_simt(const unsigned char* img, const Geometry& g, const unsigned char* pool,
                          const DomainMetaF* meta_f, const DomainMetaI* meta_i, const RangeMeta* rmeta,
-                         int n_chunks, int tiles_per_chunk, Partial* partials, cudaStream_t st) {
+                         int n_chunks, int tiles_per_chunk, Partial* partials, unsigned long long* gbest,
+                         unsigned long long* counters, cudaStream_t st) {
   dim3 grid((g.R + kSimtThreads - 1) / kSimtThreads, n_chunks);
-  if (g.K == 16)
-    matcher_simt_small<16><<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk, partials);
-  else if (g.K == 64)
-    matcher_simt_small<64><<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk, partials);
+  if (g.N == 4)
+    matcher_simt_small<4><<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk,
+                                                         partials, gbest, counters);
+  else if (g.N == 16)
+    matcher_simt_small<16><<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk,
+                                                          partials, gbest, counters);
+  else if (g.N == 64)
+    matcher_simt_small<64><<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk,
+                                                          partials, gbest, counters);
   else
-    matcher_simt_generic<<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_i, rmeta, tiles_per_chunk, partials);
+    matcher_simt_generic<<<grid, kSimtThreads, 0, st>>>(img, g, pool, meta_i, rmeta, tiles_per_chunk, partials,
+                                                        gbest, counters);
+}
+
+// Seeds the shared pruning bar of every range with the best residual among the 8
+// isometries of the domains on the grid points around the range's own 2x-scaled
+// neighbourhood (the self-similar candidates that usually fit well).  Only the bar is
+// seeded — the matcher re-finds and records these candidates itself — so the emitted
+// codes do not depend on the seed, only how much the first tiles prune.
+template <int NN>
+__global__ void seed_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned char* __restrict__ pool,
+                            const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
+                            unsigned long long* __restrict__ gbest) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= g.R) return;
+  RangeState st;
+  const RangeMeta m = rmeta[r];
+  st.r = r;
+  range_origin(g, r, st.x0, st.y0);
+  st.sb = m.sb;
+  st.ssb = (double)m.var / (double)g.N;
+  st.active = !m.shadow;
+  st.best = st.thr = __longlong_as_double(0x7ff0000000000000ll);
+  st.bd = -1;
+  st.bs = 0;
+  st.bqs = st.bqo = 0;
+  st.sqrtT = -1e30f;
+  if (st.active && g.D > 0) {
+    constexpr int NW = NN > 0 ? NN / 4 : 1;
+    uint32_t bpk[NW];
+    if constexpr (NN > 0) load_range_packed<NN>(img, g, st.x0, st.y0, bpk);
+    const int cx = st.x0 - g.n / 2, cy = st.y0 - g.n / 2;
+    const int xi0 = min(max(cx / g.step, 0), g.PX - 1), yi0 = min(max(cy / g.step, 0), g.PY - 1);
+    for (int dx = -1; dx <= 1; ++dx) {
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int xi = xi0 + dx, yi = yi0 + dy;
+        if (xi < 0 || yi < 0 || xi >= g.PX || yi >= g.PY) continue;
+        const int d = xi * g.PY + yi;
+        long long acc[kSyms];
+        exact_acc_generic(g, pool, img, st.x0, st.y0, d, acc);
+        evaluate_domain<NN>(st, g, d, acc, meta_i, pool, img, bpk, nullptr, nullptr);
+      }
+    }
+  }
+  gbest[r] = (unsigned long long)__double_as_longlong(st.best);
+}
+
+void launch_seed(const unsigned char* img, const Geometry& g, const unsigned char* pool, const DomainMetaI* meta_i,
+                 const RangeMeta* rmeta, unsigned long long* gbest, cudaStream_t st) {
+  const int blocks = (g.R + 127) / 128;
+  if (g.N == 4)
+    seed_kernel<4><<<blocks, 128, 0, st>>>(img, g, pool, meta_i, rmeta, gbest);
+  else if (g.N == 16)
+    seed_kernel<16><<<blocks, 128, 0, st>>>(img, g, pool, meta_i, rmeta, gbest);
+  else if (g.N == 64)
+    seed_kernel<64><<<blocks, 128, 0, st>>>(img, g, pool, meta_i, rmeta, gbest);
+  else
+    seed_kernel<0><<<blocks, 128, 0, st>>>(img, g, pool, meta_i, rmeta, gbest);
 }
 
 // Merge the per-scanner partial results of every range (lexicographic (R, domain,

@@ -29,8 +29,20 @@ constexpr int kTcStages = 4;
 constexpr int kTileCols = kDomainsPerTile * kSyms;  // 256
 constexpr uint32_t kTmemCols = 512;
 
+// Per-epilogue-warp survivor queue: domain groups whose 8-isometry bound did not prune
+// them, with their 8 correlations, processed 32 at a time (one per lane) so the fp64
+// reference evaluation runs with the whole warp busy instead of one lane at a time.
+struct QEntry {
+  int d;
+  int owner;            // lane (= range) the group belongs to
+  uint32_t acc[kSyms];  // fp32 bits of the exact correlations
+  int pad[2];
+};
+constexpr int kQCap = 64;
+constexpr int kEpiWarps = 8;
+
 struct TcSmemLayout {
-  uint32_t a_bytes, b_bytes, a_off, b_off, bar_off, best_off, total;
+  uint32_t a_bytes, b_bytes, a_off, b_off, bar_off, best_off, q_off, meta_off, total;
 };
 
 __host__ __device__ inline TcSmemLayout tc_smem_layout(int K) {
@@ -41,16 +53,104 @@ __host__ __device__ inline TcSmemLayout tc_smem_layout(int K) {
   L.b_off = (L.a_bytes + 1023) & ~1023u;
   L.bar_off = L.b_off + kTcStages * L.b_bytes;
   L.best_off = L.bar_off + 256;
-  L.total = L.best_off + 2 * kRangesPerTile * 8 + 1024;  // + alignment slack
+  L.q_off = L.best_off;
+  L.meta_off = L.q_off + kEpiWarps * kQCap * sizeof(QEntry);
+  L.total = L.meta_off + kEpiWarps * kDomainsPerTile * sizeof(DomainMetaF) + 1024;  // + alignment slack
   return L;
 }
 
-template <int K>
+
+// Evaluates the queued groups 32 at a time (lane i takes entry base+i, whatever range it
+// belongs to: the owner's state is fetched with shuffles), then merges the results into
+// the owners in queue order.  Per owner, entries are queued in increasing domain order
+// and each entry's isometries are tried in order, so strict-< updates reproduce the
+// reference's first-minimum tie-breaking.
+template <int NN>
+__device__ __noinline__ void flush_queue(QEntry* queue, int qcount, RangeState& st, const Geometry& g,
+                                         const DomainMetaF* __restrict__ meta_f,
+                                         const DomainMetaI* __restrict__ meta_i,
+                                         const unsigned char* __restrict__ pool,
+                                         const unsigned char* __restrict__ img, unsigned long long* gbest,
+                                         unsigned long long* counters, int lane) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  __syncwarp();
+  for (int base = 0; base < qcount; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < qcount;
+    QEntry e;
+    if (valid) e = queue[i];
+    const int owner = valid ? e.owner : lane;
+    const double o_ssb = __shfl_sync(0xffffffffu, st.ssb, owner);
+    const double o_thr = __shfl_sync(0xffffffffu, st.thr, owner);
+    const int o_sb = __shfl_sync(0xffffffffu, st.sb, owner);
+    const float o_sqrtT = __shfl_sync(0xffffffffu, st.sqrtT, owner);
+    const int o_x0 = __shfl_sync(0xffffffffu, st.x0, owner);
+    const int o_y0 = __shfl_sync(0xffffffffu, st.y0, owner);
+    double R = inf;
+    int rs = 0;
+    unsigned rqs = 0, rqo = 0;
+    if (valid) {
+      count(counters, 1, g);
+      const DomainMetaI mi = meta_i[e.d];
+      if (mi.den >= 0) {
+        const DomainMetaF mf = meta_f[e.d];
+        uint32_t bpk[NN / 4];
+        load_range_packed<NN>(img, g, o_x0, o_y0, bpk);
+        const float center = mf.a * (float)o_sb;
+        const float rad = __fmaf_rn(mf.e, o_sqrtT, -kBoundSlack);
+        double thr = o_thr;
+        for (int s = 0; s < kSyms; ++s) {
+          const float av = __uint_as_float(e.acc[s]);
+          if (!(g.flags & 1) && (av - center <= rad) && (center - av <= rad)) continue;  // per-isometry bound
+          unsigned qs = 0, qo = 0;
+          const double rv = eval_candidate<NN>(g, e.d, s, (long long)av, mi, o_sb, o_ssb, thr, bpk, pool, img,
+                                               o_x0, o_y0, qs, qo, counters);
+          if (rv < R) {
+            R = rv;
+            rs = s;
+            rqs = qs;
+            rqo = qo;
+            if (rv < thr) thr = rv;
+          }
+        }
+      }
+    }
+    // merge into the owners, in queue order
+    uint32_t found = __ballot_sync(0xffffffffu, R < inf);
+    while (found) {
+      const int k = __ffs(found) - 1;
+      found &= found - 1;
+      const double Rk = __shfl_sync(0xffffffffu, R, k);
+      const int ok = __shfl_sync(0xffffffffu, owner, k);
+      const int dk = __shfl_sync(0xffffffffu, valid ? e.d : 0, k);
+      const int sk = __shfl_sync(0xffffffffu, rs, k);
+      const unsigned qsk = __shfl_sync(0xffffffffu, rqs, k);
+      const unsigned qok = __shfl_sync(0xffffffffu, rqo, k);
+      if (lane == ok && Rk < st.best) {
+        st.best = Rk;
+        st.bd = dk;
+        st.bs = sk;
+        st.bqs = qsk;
+        st.bqo = qok;
+      }
+    }
+    if (st.best < st.thr) {
+      st.thr = st.best;
+      st.sqrtT = prune_sqrtT(st.ssb, st.thr, NN);
+      publish_best(gbest, st.r, st.best);
+    }
+  }
+  __syncwarp();
+}
+
+template <int NN>
 __global__ void __launch_bounds__(kTcThreads, 1)
 matcher_tc_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned char* __restrict__ pool,
                   const DomainMetaF* __restrict__ meta_f, const DomainMetaI* __restrict__ meta_i,
                   const RangeMeta* __restrict__ rmeta, int tiles_per_chunk, int n_tiles,
-                  Partial* __restrict__ partials) {
+                  Partial* __restrict__ partials, unsigned long long* __restrict__ gbest,
+                  unsigned long long* __restrict__ counters) {
+  constexpr int K = NN < 16 ? 16 : NN;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const TcSmemLayout L = tc_smem_layout(K);
@@ -61,7 +161,6 @@ matcher_tc_kernel(const unsigned char* __restrict__ img, Geometry g, const unsig
   uint64_t* tfull_bar = empty_bar + kTcStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  volatile double* shared_best = reinterpret_cast<volatile double*>(smem + L.best_off);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tile = blockIdx.x;
@@ -109,8 +208,6 @@ matcher_tc_kernel(const unsigned char* __restrict__ img, Geometry g, const unsig
       *reinterpret_cast<uint4*>(sA + (row >> 3) * K * 16 + kc * 128 + (row & 7) * 16) =
           make_uint4(w[0], w[1], w[2], w[3]);
     }
-    shared_best[row] = __longlong_as_double(0x7ff0000000000000ll);
-    shared_best[kRangesPerTile + row] = __longlong_as_double(0x7ff0000000000000ll);
   }
   ptx::fence_proxy_async_smem();  // generic-proxy writes of A -> visible to the tensor core
   ptx::tc_fence_before();
@@ -159,7 +256,10 @@ matcher_tc_kernel(const unsigned char* __restrict__ img, Geometry g, const unsig
     const int quarter = warp & 3;            // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     const int r = m_tile * kRangesPerTile + row;
+    QEntry* queue = reinterpret_cast<QEntry*>(smem + L.q_off) + (warp - 4) * kQCap;
+    DomainMetaF* smeta = reinterpret_cast<DomainMetaF*>(smem + L.meta_off) + (warp - 4) * kDomainsPerTile;
     RangeState st;
+    st.r = r;
     st.best = st.thr = __longlong_as_double(0x7ff0000000000000ll);
     st.bd = -1;
     st.bs = 0;
@@ -178,45 +278,70 @@ matcher_tc_kernel(const unsigned char* __restrict__ img, Geometry g, const unsig
     st.sqrtT = st.active ? -1e30f : 1e30f;  // inactive lanes prune everything
     const float sb_f = (float)st.sb;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    int qcount = 0;  // warp-uniform
 
     for (int i = wg; i < ntiles; i += 2) {
       const uint32_t bph = (i >> 1) & 1;
       const int d0 = (t_begin + i) * kDomainsPerTile;
-      // metadata of this tile's 32 domains, one per lane, broadcast by shuffles
-      const DomainMetaF my_meta = meta_f[d0 + lane];
-      if (st.active) {
-        const double ob = shared_best[(wg ^ 1) * kRangesPerTile + row];
-        if (ob < st.thr) {
-          st.thr = ob;
-          st.sqrtT = prune_sqrtT(st.ssb, st.thr, g.N);
-        }
-      }
+      __syncwarp();
+      smeta[lane] = meta_f[d0 + lane];
+      refresh_thr(st, gbest, NN);
+      __syncwarp();
       ptx::mbar_wait(&tfull_bar[wg], bph);
       ptx::tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < kTileCols / 32; ++c) {
-        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge after divergent survivors
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + lane_addr + wg * kTileCols + c * 32, v);
+      for (int h = 0; h < kTileCols / 64; ++h) {
+        __syncwarp();  // tcgen05.ld is .sync.aligned
+        uint32_t v[64];
+        ptx::tmem_ld_32x32b_x32(tmem_base + lane_addr + wg * kTileCols + h * 64, v);
+        ptx::tmem_ld_32x32b_x32(tmem_base + lane_addr + wg * kTileCols + h * 64 + 32, v + 32);
         ptx::tmem_ld_wait();
+        // 8-isometry group bound for 8 domains, branch-free
+        uint32_t gmask = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int dl = c * 4 + j;
-          const float a = __shfl_sync(0xffffffffu, my_meta.a, dl);
-          const float e = __shfl_sync(0xffffffffu, my_meta.e, dl);
-          if ((g.flags & 1) || !group_pruned(v + 8 * j, a, e, sb_f, st.sqrtT)) {
-            long long acc[kSyms];
+        for (int j = 0; j < 8; ++j) {
+          const float* f = reinterpret_cast<const float*>(v + 8 * j);
+          const float mx = fmaxf(fmaxf(fmaxf(f[0], f[1]), fmaxf(f[2], f[3])), fmaxf(fmaxf(f[4], f[5]), fmaxf(f[6], f[7])));
+          const float mn = fminf(fminf(fminf(f[0], f[1]), fminf(f[2], f[3])), fminf(fminf(f[4], f[5]), fminf(f[6], f[7])));
+          const DomainMetaF m = smeta[h * 8 + j];
+          const float center = m.a * sb_f;
+          const float rad = __fmaf_rn(m.e, st.sqrtT, -kBoundSlack);
+          const bool keep = (mx - center > rad) | (center - mn > rad);
+          gmask |= (uint32_t)keep << j;
+        }
+        if (g.flags & 1) gmask = st.active ? 0xFFu : 0u;
+        if (__any_sync(0xffffffffu, gmask != 0)) {
+          // push surviving groups (domain-major, lane-minor) onto the warp's queue
 #pragma unroll
-            for (int s = 0; s < kSyms; ++s) acc[s] = (long long)__uint_as_float(v[8 * j + s]);
-            evaluate_domain(st, g, d0 + dl, acc, meta_i, pool, img);
+          for (int j = 0; j < 8; ++j) {
+            const bool mine = (gmask >> j) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+            if (bal == 0) continue;
+            const int cnt = __popc(bal);
+            if (qcount + cnt > kQCap) {
+              flush_queue<NN>(queue, qcount, st, g, meta_f, meta_i, pool, img, gbest, counters, lane);
+              qcount = 0;
+            }
+            if (mine) {
+              QEntry* e = queue + qcount + __popc(bal & ((1u << lane) - 1u));
+              e->d = d0 + h * 8 + j;
+              e->owner = lane;
+              *reinterpret_cast<uint4*>(e->acc) = make_uint4(v[8 * j], v[8 * j + 1], v[8 * j + 2], v[8 * j + 3]);
+              *reinterpret_cast<uint4*>(e->acc + 4) = make_uint4(v[8 * j + 4], v[8 * j + 5], v[8 * j + 6], v[8 * j + 7]);
+            }
+            qcount += cnt;
           }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty_bar[wg]);
-      if (st.active) shared_best[wg * kRangesPerTile + row] = st.best;
+      if (lane == 0) ptx::mbar_arrive(&tempty_bar[wg]);  // accumulator free for the MMA
+      if (qcount >= 32) {
+        flush_queue<NN>(queue, qcount, st, g, meta_f, meta_i, pool, img, gbest, counters, lane);
+        qcount = 0;
+      }
     }
+    if (qcount > 0) flush_queue<NN>(queue, qcount, st, g, meta_f, meta_i, pool, img, gbest, counters, lane);
     if (r < g.R)
       partials[(long long)(blockIdx.y * 2 + wg) * g.R + r] = Partial{st.best, st.bd, st.bs, st.bqs, st.bqo};
   }
@@ -235,27 +360,33 @@ size_t tc_smem_bytes(int K) {
   return L.total < 118 * 1024 ? 118 * 1024 : L.total;
 }
 
-bool tc_supported(const Geometry& g) { return g.K == 16 || g.K == 64; }
+bool tc_supported(const Geometry& g) { return g.N == 4 || g.N == 16 || g.N == 64; }
 
-cudaError_t launch_matcher_tc(const unsigned char* img, const Geometry& g, const unsigned char* pool,
-                              const DomainMetaF* meta_f, const DomainMetaI* meta_i, const RangeMeta* rmeta,
-                              int n_chunks, int tiles_per_chunk, Partial* partials, cudaStream_t st) {
+template <int NN>
+static cudaError_t launch_tc(const unsigned char* img, const Geometry& g, const unsigned char* pool,
+                             const DomainMetaF* meta_f, const DomainMetaI* meta_i, const RangeMeta* rmeta,
+                             int n_chunks, int tiles_per_chunk, Partial* partials, unsigned long long* gbest,
+                             unsigned long long* counters, cudaStream_t st) {
   const int n_tiles = g.D_pad / kDomainsPerTile;
   dim3 grid((g.R + kRangesPerTile - 1) / kRangesPerTile, n_chunks);
   const size_t smem = tc_smem_bytes(g.K);
-  cudaError_t e;
-  if (g.K == 16) {
-    e = cudaFuncSetAttribute(matcher_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    matcher_tc_kernel<16><<<grid, kTcThreads, smem, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk,
-                                                          n_tiles, partials);
-  } else {
-    e = cudaFuncSetAttribute(matcher_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    matcher_tc_kernel<64><<<grid, kTcThreads, smem, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk,
-                                                          n_tiles, partials);
-  }
+  const cudaError_t e =
+      cudaFuncSetAttribute(matcher_tc_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  matcher_tc_kernel<NN><<<grid, kTcThreads, smem, st>>>(img, g, pool, meta_f, meta_i, rmeta, tiles_per_chunk,
+                                                        n_tiles, partials, gbest, counters);
   return cudaGetLastError();
+}
+
+cudaError_t launch_matcher_tc(const unsigned char* img, const Geometry& g, const unsigned char* pool,
+                              const DomainMetaF* meta_f, const DomainMetaI* meta_i, const RangeMeta* rmeta,
+                              int n_chunks, int tiles_per_chunk, Partial* partials, unsigned long long* gbest,
+                              unsigned long long* counters, cudaStream_t st) {
+  if (g.N == 4)
+    return launch_tc<4>(img, g, pool, meta_f, meta_i, rmeta, n_chunks, tiles_per_chunk, partials, gbest, counters, st);
+  if (g.N == 16)
+    return launch_tc<16>(img, g, pool, meta_f, meta_i, rmeta, n_chunks, tiles_per_chunk, partials, gbest, counters, st);
+  return launch_tc<64>(img, g, pool, meta_f, meta_i, rmeta, n_chunks, tiles_per_chunk, partials, gbest, counters, st);
 }
 
 }  // namespace ficb
