@@ -11,7 +11,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libfic_b200.so")
+LIB = os.environ.get("FIC_LIB") or os.path.join(HERE, "libfic_b200.so")
 SOURCES = ["fic_api.cu", "pool.cu", "matcher_simt.cu", "matcher_tc.cu", "decoder.cu"]
 HEADERS = ["common.cuh", "tc_ptx.cuh", os.path.join("..", "..", "include", "fic_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -31,7 +31,7 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "_obj")
+    objdir = os.path.join(HERE, "_obj" + ("_" + os.path.basename(LIB) if os.environ.get("FIC_LIB") else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -196,6 +196,42 @@ __device__ __forceinline__ void count(unsigned long long* c, int i, const Geomet
   if ((g.flags & 4) && c) atomicAdd(c + i, 1ull);
 }
 
+// Range pixels of (x0, y0) packed 4 per word (NN pixels, NN % 4 == 0).
+template <int NN>
+__device__ __forceinline__ void load_range_packed(const unsigned char* __restrict__ img, const Geometry& g, int x0,
+                                                  int y0, uint32_t* bpk) {
+#pragma unroll
+  for (int w = 0; w < NN / 4; ++w) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = w * 4 + b;
+      v |= (uint32_t)img[(long long)(y0 + i / g.n) * g.W + x0 + i % g.n] << (8 * b);
+    }
+    bpk[w] = v;
+  }
+}
+
+// Same packing with 32/16-bit loads: 4 consecutive pixels of a range row per word
+// (n >= 4: range rows are 4-byte aligned since x0 is a multiple of n), or two 2-pixel
+// rows per word (n == 2).
+template <int NN>
+__device__ __forceinline__ void load_range_words(const unsigned char* __restrict__ img, const Geometry& g, int x0,
+                                                 int y0, uint32_t* bpk) {
+  constexpr int n = NN == 4 ? 2 : (NN == 16 ? 4 : 8);
+#pragma unroll
+  for (int w = 0; w < NN / 4; ++w) {
+    if constexpr (n >= 4) {
+      const int i = 4 * w;
+      bpk[w] = *reinterpret_cast<const uint32_t*>(img + (long long)(y0 + i / n) * g.W + x0 + i % n);
+    } else {
+      const uint32_t lo = *reinterpret_cast<const unsigned short*>(img + (long long)(y0 + 2 * w) * g.W + x0);
+      const uint32_t hi = *reinterpret_cast<const unsigned short*>(img + (long long)(y0 + 2 * w + 1) * g.W + x0);
+      bpk[w] = lo | (hi << 16);
+    }
+  }
+}
+
 // Reference-exact evaluation of one candidate (domain d, isometry s) for a range with
 // pixel sum sb and ssb = range_var/N, following Searcher::search_impl
 // (proj/src/encoder.cpp:236-280) operation by operation.  Returns its residual, or +inf
@@ -244,6 +280,11 @@ __device__ __forceinline__ double eval_candidate(const Geometry& g, int d, int s
   // Exact residual in range-pixel order (encoder.cpp:274-280).
   double r_val = 0.0;
   if constexpr (NN > 0) {
+    uint32_t lb[NN / 4];
+    if (bpk == nullptr) {  // range pixels fetched only when a candidate reaches the exact loop
+      load_range_words<NN>(img, g, x0, y0, lb);
+      bpk = lb;
+    }
     const unsigned char* col = pool + (long long)d * (NN < 16 ? 16 : NN) * 16 + s * 16;
 #pragma unroll
     for (int kc = 0; kc < (NN + 7) / 8; ++kc) {
@@ -301,22 +342,6 @@ static __device__ __noinline__ void evaluate_domain(RangeState& st, const Geomet
         publish_best(gbest, st.r, r_val);
       }
     }
-  }
-}
-
-// Range pixels of (x0, y0) packed 4 per word (NN pixels, NN % 4 == 0).
-template <int NN>
-__device__ __forceinline__ void load_range_packed(const unsigned char* __restrict__ img, const Geometry& g, int x0,
-                                                  int y0, uint32_t* bpk) {
-#pragma unroll
-  for (int w = 0; w < NN / 4; ++w) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = w * 4 + b;
-      v |= (uint32_t)img[(long long)(y0 + i / g.n) * g.W + x0 + i % g.n] << (8 * b);
-    }
-    bpk[w] = v;
   }
 }
 

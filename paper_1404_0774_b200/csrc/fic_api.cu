@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -26,11 +27,13 @@ void launch_matcher_simt(const unsigned char*, const Geometry&, const unsigned c
                          const DomainMetaI*, const RangeMeta*, int, int, Partial*, unsigned long long*,
                          unsigned long long*, cudaStream_t);
 cudaError_t launch_matcher_tc(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
-                              const DomainMetaI*, const RangeMeta*, int, int, Partial*, unsigned long long*,
+                              const DomainMetaI*, const RangeMeta*, int, int, int, Partial*, unsigned long long*,
                               unsigned long long*, cudaStream_t);
 void launch_seed(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaI*, const RangeMeta*,
                  unsigned long long*, cudaStream_t);
 bool tc_supported(const Geometry&);
+int tc_rows_per_cta();
+int tc_tile_domains();
 void launch_finalize(const unsigned char*, const Geometry&, const RangeMeta*, const Partial*, int, fic_mapping*,
                      cudaStream_t);
 struct RangeXform {
@@ -178,7 +181,7 @@ struct Workspace {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag;
+      diag, scratch;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse;
   std::mutex mu;
 };
@@ -203,6 +206,26 @@ Workspace& workspace() {
   return *g_ws[dev];
 }
 
+// Split n_tiles into chunks so that m_tiles x chunks CTAs fill whole waves: minimise
+// waves * (tiles per CTA + a per-CTA startup allowance).  Returns {n_chunks, tiles_per_chunk}.
+std::pair<int, int> plan_chunks(int n_tiles, int m_tiles, long long wave) {
+  int n_chunks = 1;
+  double best_cost = 1e300;
+  for (int c = 1; c <= std::min(n_tiles, 256); ++c) {
+    const int tpc = (n_tiles + c - 1) / c;
+    const int cc = (n_tiles + tpc - 1) / tpc;
+    const long long ctas = (long long)m_tiles * cc;
+    const long long waves = (ctas + wave - 1) / wave;
+    const double cost = (double)waves * (tpc + 6);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      n_chunks = cc;
+    }
+  }
+  const int tpc = (n_tiles + n_chunks - 1) / n_chunks;
+  return {(n_tiles + tpc - 1) / tpc, tpc};
+}
+
 int matcher_mode(const Geometry& g) {
   const char* env = std::getenv("FIC_MATCHER");
   const bool want_simt = env && std::strcmp(env, "simt") == 0;
@@ -217,24 +240,21 @@ void enqueue_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g
   auto* mf = static_cast<DomainMetaF*>(ws.meta_f.get((size_t)g.D_pad * sizeof(DomainMetaF)));
   auto* mi = static_cast<DomainMetaI*>(ws.meta_i.get((size_t)g.D_pad * sizeof(DomainMetaI)));
   auto* rm = static_cast<RangeMeta*>(ws.rmeta.get((size_t)g.R * sizeof(RangeMeta)));
-  const int n_tiles = g.D_pad / kDomainsPerTile;
-  const int m_tiles = (g.R + kRangesPerTile - 1) / kRangesPerTile;
   const int mode = matcher_mode(g);
-  int n_chunks;
-  if (mode == 1)
-    n_chunks = m_tiles >= ws.sms ? 1 : ws.sms / m_tiles;
-  else
-    n_chunks = (ws.sms * 8 + m_tiles - 1) / m_tiles;
-  n_chunks = std::max(1, std::min(n_chunks, n_tiles));
-  const int tiles_per_chunk = (n_tiles + n_chunks - 1) / n_chunks;
-  n_chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+  const int rows_per_cta = mode == 1 ? tc_rows_per_cta() : 128;
+  const int tile_dom = mode == 1 ? tc_tile_domains() : kDomainsPerTile;
+  const int n_tiles = g.D_pad / tile_dom;
+  const int m_tiles = (g.R + rows_per_cta - 1) / rows_per_cta;
+  const long long wave = (long long)ws.sms * (mode == 1 ? 1 : 8);
+  const std::pair<int, int> plan = plan_chunks(n_tiles, m_tiles, wave);
+  const int n_chunks = plan.first, tiles_per_chunk = plan.second;
   const int n_slots = mode == 1 ? 2 * n_chunks : n_chunks;
   auto* parts = static_cast<Partial*>(ws.partials.get((size_t)n_slots * g.R * sizeof(Partial)));
   auto* gbest = static_cast<unsigned long long*>(ws.gbest.get((size_t)g.R * sizeof(unsigned long long)));
   unsigned long long* diag = nullptr;
-  if (g.flags & 4) {
-    diag = static_cast<unsigned long long*>(ws.diag.get(8 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(diag, 0, 8 * sizeof(unsigned long long), st));
+  if (g.flags & (4 | 32)) {
+    diag = static_cast<unsigned long long*>(ws.diag.get((8 + 256) * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(diag, 0, (8 + 256) * sizeof(unsigned long long), st));
   }
 
   CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
@@ -244,7 +264,20 @@ void enqueue_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g
   const bool timed = g_timing.load() != 0;
   if (timed) CK(cudaEventRecord(ws.ev0, st));
   if (mode == 1) {
-    CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, gbest, diag, st));
+    // Sparse pre-passes (every 512th, then every 32nd tile) tighten the shared pruning bar
+    // before the full scan, so the full scan's CTAs do not each start from a weak bar.
+    // Their partial results are scratch: the full scan re-finds every candidate.
+    const char* pp = std::getenv("FIC_PREPASS");
+    const bool prepass = !(pp && std::strcmp(pp, "0") == 0);
+    for (int step : {512, 32}) {
+      if (!prepass || n_tiles / step < 8) continue;
+      const int vt = (n_tiles + step - 1) / step;
+      const std::pair<int, int> pplan = plan_chunks(vt, m_tiles, wave);
+      auto* scratch = static_cast<Partial*>(ws.scratch.get((size_t)2 * pplan.first * g.R * sizeof(Partial)));
+      CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, pplan.first, pplan.second, step, scratch, gbest, nullptr, st));
+      g_launches += 1;
+    }
+    CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, 1, parts, gbest, diag, st));
   } else {
     launch_matcher_simt(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, gbest, diag, st);
   }
@@ -253,9 +286,17 @@ void enqueue_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g
   CK(cudaGetLastError());
   g_launches += 5;
   if (diag) {
-    unsigned long long h[8];
+    unsigned long long h[8 + 256];
     CK(cudaMemcpyAsync(h, diag, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (g.flags & 32) {
+      const unsigned long long t0 = h[8];
+      std::fprintf(stderr, "[fic trace] tile: producer-go mma-go epi-full epi-release (cycles from first producer-go)\n");
+      for (int i = 0; i < 64; ++i)
+        std::fprintf(stderr, "[fic trace] %2d %8lld %8lld %8lld %8lld\n", i, (long long)(h[8 + i] - t0),
+                     (long long)(h[8 + 64 + i] - t0), h[8 + 128 + i] ? (long long)(h[8 + 128 + i] - t0) : -1,
+                     h[8 + 192 + i] ? (long long)(h[8 + 192 + i] - t0) : -1);
+    }
     std::fprintf(stderr, "[fic diag] R=%d D=%d chunks=%d groups=%llu survive=%llu (%.4f%%) tight=%llu exact=%llu\n",
                  g.R, g.D, n_chunks, h[0], h[1], h[0] ? 100.0 * h[1] / h[0] : 0.0, h[2], h[3]);
   }
