@@ -26,14 +26,8 @@ void launch_range_pass(const unsigned char*, const Geometry&, RangeMeta*, unsign
 void launch_matcher_simt(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
                          const DomainMetaI*, const RangeMeta*, int, int, Partial*, unsigned long long*,
                          unsigned long long*, cudaStream_t);
-cudaError_t launch_matcher_tc(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaF*,
-                              const DomainMetaI*, const RangeMeta*, int, int, int, Partial*, unsigned long long*,
-                              unsigned long long*, cudaStream_t);
 void launch_seed(const unsigned char*, const Geometry&, const unsigned char*, const DomainMetaI*, const RangeMeta*,
                  unsigned long long*, cudaStream_t);
-bool tc_supported(const Geometry&);
-int tc_rows_per_cta();
-int tc_tile_domains();
 void launch_finalize(const unsigned char*, const Geometry&, const RangeMeta*, const Partial*, int, fic_mapping*,
                      cudaStream_t);
 struct RangeXform {
@@ -48,6 +42,33 @@ void launch_decode_step(const double*, double*, const RangeXform*, int, int, int
 void launch_rmse_finish(const double*, int, long long, double*, cudaStream_t);
 void launch_raster_init(double*, long long, int, const unsigned char*, cudaStream_t);
 void launch_quantize_raster(const double*, long long, unsigned char*, cudaStream_t);
+// scan.cu (tcgen05 path, n in {2, 4, 8})
+bool scan_supported(const Geometry&);
+int scan_tiles(const Geometry&);
+long long scan_pool_domains(const Geometry&);
+void launch_pool_v3(const unsigned char*, const Geometry&, __half*, unsigned short*, DomainMetaI*,
+                    unsigned long long*, cudaStream_t);
+void launch_fill_u64(unsigned long long*, long long, unsigned long long, cudaStream_t);
+void launch_seed_v3(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
+                    const RangeMeta*, unsigned long long*, const double*, cudaStream_t);
+size_t deq_table_entries(const Geometry&);
+void launch_deq_tables(const Geometry&, double*, cudaStream_t);
+int scan_grid(const Geometry&, int, int);
+cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const __half*, const RangeMeta*,
+                        const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long,
+                        cudaStream_t);
+int scan_padded_ranges(const Geometry&);
+void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
+size_t range_op_bytes(const Geometry&);
+void launch_range_op(const unsigned char*, const Geometry&, const RangeMeta*, unsigned char*, cudaStream_t);
+void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
+                 const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
+                 const double*, int, cudaStream_t);
+void launch_winner(const uint2*, const unsigned long long*, int, unsigned long long, const double*,
+                   const unsigned long long*, unsigned*, int, cudaStream_t);
+void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
+                   const RangeMeta*, const unsigned*, const unsigned long long*, fic_mapping*, unsigned long long*,
+                   cudaStream_t);
 }  // namespace ficb
 
 using namespace ficb;
@@ -74,6 +95,9 @@ int32_t fail(int32_t code, const std::string& detail) {
 
 struct CudaFail {
   cudaError_t e;
+  const char* what;
+};
+struct InternalFail {
   const char* what;
 };
 
@@ -181,8 +205,9 @@ struct Workspace {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag, scratch;
-  HostBuf h_img, h_out, h_counters, h_raster, h_rmse;
+      diag, scratch, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq;
+  HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
+  unsigned long long list_cap = 0;  // survivor-list capacity (entries), grown on overflow
   std::mutex mu;
 };
 
@@ -229,76 +254,197 @@ std::pair<int, int> plan_chunks(int n_tiles, int m_tiles, long long wave) {
 int matcher_mode(const Geometry& g) {
   const char* env = std::getenv("FIC_MATCHER");
   const bool want_simt = env && std::strcmp(env, "simt") == 0;
-  return (!want_simt && tc_supported(g)) ? 1 : 0;  // 1 = tcgen05
+  return (!want_simt && scan_supported(g)) ? 1 : 0;  // 1 = tcgen05 scan (scan.cu)
 }
 
-// Enqueue the whole encode of the region described by g: K1 pool, range pass, K2
-// matcher, finalize.  counters[0] = flat domains, counters[1] = shadow ranges.
-void enqueue_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fic_mapping* d_out,
-                    unsigned long long* d_counters, cudaStream_t st) {
+constexpr int kMaxLevels = 6;
+constexpr int kPartSlots = 256;      // per-level survivor counters, one per scan CTA (<= SMs)
+constexpr int kScanCountSlots = kMaxLevels * kPartSlots + 1;  // + record self-check failures
+constexpr int kSelfcheckSlot = kMaxLevels * kPartSlots;
+
+// Scan levels: sparse passes over every 8^k-th 128-domain tile (k >= 1, at least one tile)
+// seed the pruning bar, then the full scan.  Each level prunes with the bar the previous
+// ones achieved, so survivors per level stay near (level size / previous level size) x the
+// handful of candidates whose bound is within the quantisation slack of the optimum.
+std::vector<int> scan_levels(const Geometry& g) {
+  std::vector<int> lv;
+  const int tiles = scan_tiles(g);
+  const char* pp = std::getenv("FIC_PREPASS");
+  const bool prepass = !(pp && std::strcmp(pp, "0") == 0);
+  if (prepass)
+    for (int s = 4096; s >= 8; s /= 8)
+      if (tiles > s) lv.push_back(s);
+  lv.push_back(1);
+  return lv;
+}
+
+struct ScanBufs {
+  __half* upool;
+  unsigned short* qpool;
+  DomainMetaI* mi;
+  RangeMeta* rm;
+  unsigned long long* gbest;
+  unsigned* win;
+  unsigned long long* cnt;
+  unsigned char* ropnd;
+  float* thr;
+  double* deq;
+};
+
+ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
+  const long long Dt = scan_pool_domains(g);
+  ScanBufs b;
+  b.upool = static_cast<__half*>(ws.upool.get((size_t)Dt * g.K * 2));
+  b.qpool = static_cast<unsigned short*>(ws.qpool.get((size_t)Dt * 8 * g.N * 2));  // q8: [domain][isometry][N]
+  b.mi = static_cast<DomainMetaI*>(ws.meta_i.get((size_t)Dt * sizeof(DomainMetaI)));
+  b.rm = static_cast<RangeMeta*>(ws.rmeta.get((size_t)g.R * sizeof(RangeMeta)));
+  b.gbest = static_cast<unsigned long long*>(ws.gbest.get((size_t)g.R * sizeof(unsigned long long)));
+  b.win = static_cast<unsigned*>(ws.win.get((size_t)g.R * sizeof(unsigned)));
+  b.ropnd = static_cast<unsigned char*>(ws.ropnd.get(range_op_bytes(g)));
+  b.thr = static_cast<float*>(ws.thr.get((size_t)scan_padded_ranges(g) * sizeof(float)));
+  b.deq = static_cast<double*>(ws.deq.get(deq_table_entries(g) * sizeof(double)));
+  b.cnt = static_cast<unsigned long long*>(ws.scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
+  return b;
+}
+
+// One scan level: tensor-core scan appending survivors to per-CTA list partitions, then
+// their exact evaluation.  cnt: the level's kPartSlots counters.
+void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, int stride,
+                   unsigned long long* cnt, cudaStream_t st) {
+  auto* list = static_cast<uint2*>(ws.list.get((size_t)ws.list_cap * sizeof(uint2)));
+  auto* res = static_cast<double*>(ws.res.get((size_t)ws.list_cap * sizeof(double)));
+  const int parts = scan_grid(g, stride, ws.sms);
+  const unsigned long long part = ws.list_cap / (unsigned long long)parts;
+  launch_threshold(g, b.rm, b.gbest, b.thr, st);
+  CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, st));
+  launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, ws.sms, st);
+  g_launches += 3;
+}
+
+// The full level plus winner selection and records.  Its list must be complete; a
+// truncated one (count > cap) is detected by the caller, which re-runs this part only.
+void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, size_t level,
+                   fic_mapping* d_out, cudaStream_t st) {
+  unsigned long long* cnt = b.cnt + level * kPartSlots;
+  CK(cudaMemsetAsync(b.win, 0xFF, (size_t)g.R * sizeof(unsigned), st));
+  CK(cudaMemsetAsync(b.cnt + kSelfcheckSlot, 0, sizeof(unsigned long long), st));
+  enqueue_level(ws, d_img, g, b, 1, cnt, st);
+  const bool timed = g_timing.load() != 0;
+  if (timed) CK(cudaEventRecord(ws.ev1, st));
+  const int parts = scan_grid(g, 1, ws.sms);
+  launch_winner(static_cast<uint2*>(ws.list.p), cnt, parts, ws.list_cap / (unsigned long long)parts,
+                static_cast<double*>(ws.res.p), b.gbest, b.win, ws.sms, st);
+  launch_record(d_img, g, b.qpool, b.mi, b.rm, b.win, b.gbest, d_out, b.cnt + kSelfcheckSlot, st);
+  g_launches += 2;
+  CK(cudaGetLastError());
+}
+
+// tcgen05 path: K1 normalised pool, range pass, seed, sparse levels, final level.
+void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b,
+                         fic_mapping* d_out, unsigned long long* d_counters, cudaStream_t st) {
+  if (ws.list_cap == 0) ws.list_cap = std::max<unsigned long long>(1ull << 20, (unsigned long long)g.R * 8 * 64);
+  CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(b.cnt, 0, kScanCountSlots * sizeof(unsigned long long), st));
+  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);
+  launch_range_pass(d_img, g, b.rm, d_counters + 1, st);
+  launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
+  launch_deq_tables(g, b.deq, st);
+  launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
+  launch_range_op(d_img, g, b.rm, b.ropnd, st);
+  g_launches += 6;
+  if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
+  const std::vector<int> lv = scan_levels(g);
+  for (size_t l = 0; l + 1 < lv.size(); ++l) enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st);
+  enqueue_final(ws, d_img, g, b, lv.size() - 1, d_out, st);
+}
+
+// n >= 16 path (and FIC_MATCHER=simt): 8-isometry fp16 pool + CUDA-core matcher
+// (matcher_simt.cu), exact integer correlations.
+void enqueue_encode_simt(Workspace& ws, const unsigned char* d_img, const Geometry& g, fic_mapping* d_out,
+                         unsigned long long* d_counters, cudaStream_t st) {
   auto* pool = static_cast<unsigned char*>(ws.pool.get((size_t)g.D_pad * g.K * 16));
   auto* mf = static_cast<DomainMetaF*>(ws.meta_f.get((size_t)g.D_pad * sizeof(DomainMetaF)));
   auto* mi = static_cast<DomainMetaI*>(ws.meta_i.get((size_t)g.D_pad * sizeof(DomainMetaI)));
   auto* rm = static_cast<RangeMeta*>(ws.rmeta.get((size_t)g.R * sizeof(RangeMeta)));
-  const int mode = matcher_mode(g);
-  const int rows_per_cta = mode == 1 ? tc_rows_per_cta() : 128;
-  const int tile_dom = mode == 1 ? tc_tile_domains() : kDomainsPerTile;
-  const int n_tiles = g.D_pad / tile_dom;
+  const int rows_per_cta = 128;
+  const int n_tiles = g.D_pad / kDomainsPerTile;
   const int m_tiles = (g.R + rows_per_cta - 1) / rows_per_cta;
-  const long long wave = (long long)ws.sms * (mode == 1 ? 1 : 8);
-  const std::pair<int, int> plan = plan_chunks(n_tiles, m_tiles, wave);
+  const std::pair<int, int> plan = plan_chunks(n_tiles, m_tiles, (long long)ws.sms * 8);
   const int n_chunks = plan.first, tiles_per_chunk = plan.second;
-  const int n_slots = mode == 1 ? 2 * n_chunks : n_chunks;
-  auto* parts = static_cast<Partial*>(ws.partials.get((size_t)n_slots * g.R * sizeof(Partial)));
+  auto* parts = static_cast<Partial*>(ws.partials.get((size_t)n_chunks * g.R * sizeof(Partial)));
   auto* gbest = static_cast<unsigned long long*>(ws.gbest.get((size_t)g.R * sizeof(unsigned long long)));
   unsigned long long* diag = nullptr;
-  if (g.flags & (4 | 32)) {
+  if (g.flags & 4) {
     diag = static_cast<unsigned long long*>(ws.diag.get((8 + 256) * sizeof(unsigned long long)));
     CK(cudaMemsetAsync(diag, 0, (8 + 256) * sizeof(unsigned long long), st));
   }
-
   CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
   launch_pool_build(d_img, g, pool, mf, mi, d_counters, st);
   launch_range_pass(d_img, g, rm, d_counters + 1, st);
   launch_seed(d_img, g, pool, mi, rm, gbest, st);
   const bool timed = g_timing.load() != 0;
   if (timed) CK(cudaEventRecord(ws.ev0, st));
-  if (mode == 1) {
-    // Sparse pre-passes (every 512th, then every 32nd tile) tighten the shared pruning bar
-    // before the full scan, so the full scan's CTAs do not each start from a weak bar.
-    // Their partial results are scratch: the full scan re-finds every candidate.
-    const char* pp = std::getenv("FIC_PREPASS");
-    const bool prepass = !(pp && std::strcmp(pp, "0") == 0);
-    for (int step : {512, 32}) {
-      if (!prepass || n_tiles / step < 8) continue;
-      const int vt = (n_tiles + step - 1) / step;
-      const std::pair<int, int> pplan = plan_chunks(vt, m_tiles, wave);
-      auto* scratch = static_cast<Partial*>(ws.scratch.get((size_t)2 * pplan.first * g.R * sizeof(Partial)));
-      CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, pplan.first, pplan.second, step, scratch, gbest, nullptr, st));
-      g_launches += 1;
-    }
-    CK(launch_matcher_tc(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, 1, parts, gbest, diag, st));
-  } else {
-    launch_matcher_simt(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, gbest, diag, st);
-  }
+  launch_matcher_simt(d_img, g, pool, mf, mi, rm, n_chunks, tiles_per_chunk, parts, gbest, diag, st);
   if (timed) CK(cudaEventRecord(ws.ev1, st));
-  launch_finalize(d_img, g, rm, parts, n_slots, d_out, st);
+  launch_finalize(d_img, g, rm, parts, n_chunks, d_out, st);
   CK(cudaGetLastError());
   g_launches += 5;
   if (diag) {
     unsigned long long h[8 + 256];
     CK(cudaMemcpyAsync(h, diag, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (g.flags & 32) {
-      const unsigned long long t0 = h[8];
-      std::fprintf(stderr, "[fic trace] tile: producer-go mma-go epi-full epi-release (cycles from first producer-go)\n");
-      for (int i = 0; i < 64; ++i)
-        std::fprintf(stderr, "[fic trace] %2d %8lld %8lld %8lld %8lld\n", i, (long long)(h[8 + i] - t0),
-                     (long long)(h[8 + 64 + i] - t0), h[8 + 128 + i] ? (long long)(h[8 + 128 + i] - t0) : -1,
-                     h[8 + 192 + i] ? (long long)(h[8 + 192 + i] - t0) : -1);
+    std::fprintf(stderr, "[fic diag] simt R=%d D=%d chunks=%d groups=%llu survive=%llu tight=%llu exact=%llu\n", g.R,
+                 g.D, n_chunks, h[0], h[1], h[2], h[3]);
+  }
+}
+
+// Enqueue the whole encode of the region described by g and wait for it; a survivor list
+// that overflowed is grown to the count the scan reported and the encode is re-run.
+// counters[0] = flat domains, counters[1] = shadow ranges (copied to h_counters).
+void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fic_mapping* d_out,
+                unsigned long long* d_counters, unsigned long long* h_counters, cudaStream_t st) {
+  if (matcher_mode(g) == 0) {
+    enqueue_encode_simt(ws, d_img, g, d_out, d_counters, st);
+    if (h_counters)
+      CK(cudaMemcpyAsync(h_counters, d_counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return;
+  }
+  const ScanBufs b = scan_bufs(ws, g);
+  const size_t nl = scan_levels(g).size();
+  auto* hc = static_cast<unsigned long long*>(ws.h_scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
+  enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
+  for (int attempt = 0;; ++attempt) {
+    CK(cudaMemcpyAsync(hc, b.cnt, kScanCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (h_counters)
+      CK(cudaMemcpyAsync(h_counters, d_counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const std::vector<int> lv = scan_levels(g);
+    const int fparts = scan_grid(g, 1, ws.sms);
+    unsigned long long need = 0;  // largest partition of the full level
+    for (int c = 0; c < fparts; ++c) need = std::max(need, hc[(nl - 1) * kPartSlots + c]);
+    if (g.flags & 4) {
+      std::fprintf(stderr, "[fic diag] scan R=%d D=%d tiles=%d levels", g.R, g.D, scan_tiles(g));
+      for (size_t l = 0; l < nl; ++l) {
+        unsigned long long tot = 0, mx = 0;
+        const int parts = scan_grid(g, lv[l], ws.sms);
+        for (int c = 0; c < parts; ++c) {
+          tot += hc[l * kPartSlots + c];
+          mx = std::max(mx, hc[l * kPartSlots + c]);
+        }
+        std::fprintf(stderr, " %d:%llu(max part %llu)", lv[l], tot, mx);
+      }
+      std::fprintf(stderr, " part %llu selfcheck %llu\n", ws.list_cap / fparts, hc[kSelfcheckSlot]);
     }
-    std::fprintf(stderr, "[fic diag] R=%d D=%d chunks=%d groups=%llu survive=%llu (%.4f%%) tight=%llu exact=%llu\n",
-                 g.R, g.D, n_chunks, h[0], h[1], h[0] ? 100.0 * h[1] / h[0] : 0.0, h[2], h[3]);
+    if (need <= ws.list_cap / (unsigned long long)fparts) {
+      if (hc[kSelfcheckSlot] != 0) throw InternalFail{"scan self-check: a winner's residual differs from its bar"};
+      return;
+    }
+    // a partition of the full level's list was truncated: grow the list and re-run that
+    // level (the bar it achieved so far only lowers the survivor count)
+    if (attempt >= 4) throw InternalFail{"survivor list keeps overflowing"};
+    ws.list_cap = (need + need / 4 + 1024) * (unsigned long long)ws.sms;
+    enqueue_final(ws, d_img, g, b, nl - 1, d_out, st);
   }
 }
 
@@ -326,6 +472,8 @@ int32_t guarded(F&& f) {
     return f();
   } catch (const CudaFail& c) {
     return fail(FIC_ERR_CUDA, std::string(cudaGetErrorName(c.e)) + " (" + cudaGetErrorString(c.e) + ") at " + c.what);
+  } catch (const InternalFail& f) {
+    return fail(FIC_ERR_INTERNAL, f.what);
   } catch (const std::bad_alloc&) {
     return fail(FIC_ERR_INTERNAL, "host allocation failed");
   }
@@ -345,9 +493,8 @@ int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, f
     auto* h_out = static_cast<fic_mapping*>(ws.h_out.get((size_t)g.R * sizeof(fic_mapping)));
     auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * sizeof(unsigned long long)));
     CK(cudaMemcpyAsync(d_img, h_img, img_bytes, cudaMemcpyHostToDevice, ws.stream));
-    enqueue_encode(ws, d_img, g, d_out, d_cnt, ws.stream);
+    run_encode(ws, d_img, g, d_out, d_cnt, h_cnt, ws.stream);
     CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, ws.stream));
-    CK(cudaMemcpyAsync(h_cnt, d_cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
     collect_timing(ws);
     std::memcpy(out, h_out, (size_t)g.R * sizeof(fic_mapping));
@@ -496,17 +643,10 @@ int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height,
     std::lock_guard<std::mutex> lock(ws.mu);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
-    enqueue_encode(ws, d_image, g, d_out, d_cnt, st);
-    if (stats) {
-      unsigned long long h[2];
-      CK(cudaMemcpyAsync(h, d_cnt, sizeof h, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      fill_stats(stats, g, h[0], h[1]);
-    }
-    if (g_timing.load()) {
-      CK(cudaStreamSynchronize(st));
-      collect_timing(ws);
-    }
+    auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * sizeof(unsigned long long)));
+    run_encode(ws, d_image, g, d_out, d_cnt, h_cnt, st);
+    if (stats) fill_stats(stats, g, h_cnt[0], h_cnt[1]);
+    collect_timing(ws);
     return FIC_OK;
   });
 }

@@ -1,0 +1,1047 @@
+// scan.cu — the tcgen05 encoder path for n in {2, 4, 8}: normalised domain pool (K1),
+// the range x domain scan on the tensor cores (K2), the exact survivor evaluation and the
+// lexicographic winner / record pass.
+//
+// What the reference computes (Searcher::search_impl, proj/src/encoder.cpp:159-296) is,
+// for every range, the lexicographic minimum of (R, canonical domain index, isometry)
+// over all non-flat candidates, R being the exact quantised residual (encoder.cpp:236-287).
+// Its pruning stages never drop that minimum.  This path computes the same minimum with
+// a different, equally output-neutral pruning:
+//
+//  * K1 writes every domain once as a NORMALISED operand u_j = (N q_j - Sq) / sqrt(den)
+//    (fp16, |u_j| <= sqrt(N), sum u_j^2 = N), and the range side is the CENTRED range
+//    b_i - Sb/N (fp16), one operand row per isometry (the reference's pre-permuted range
+//    bv[s], encoder.cpp:183-190).  Their dot product is X = num / sqrt(den) with
+//    num = N*acc - Sq*Sb the reference's integer correlation (encoder.cpp:241), so the
+//    unconstrained least-squares lower bound of any quantised residual of the candidate,
+//    R* = ssb - num^2 / (N den), is ssb - X^2/N.
+//  * A candidate is dropped iff |X~| <= sqrt(N (ssb - bar - delta)) - err, where bar is an
+//    ACHIEVED residual of the same range and err bounds |X~ - X| (fp16 rounding of both
+//    operands, fp32 accumulation): then R >= R* > bar, so it cannot be the minimum.  The
+//    test needs only the range's own threshold: per accumulator column it is one 3-input
+//    |max| (FMNMX3) per two columns.
+//  * Survivors (range, isometry, domain) go to a global list; eval_kernel recomputes the
+//    exact integer correlation and runs the reference's fp64 arithmetic operation by
+//    operation, lowering the range's bar (atomicMin on the IEEE bits).  The scan runs as
+//    sparse levels (every 64th / 8th tile) and then in full, each level pruning with the
+//    bar the previous ones achieved.  Every candidate whose residual equals the final bar
+//    is in the full level's list; winner_kernel takes the smallest (domain, isometry)
+//    among them and record_kernel re-evaluates it into the RangeMapping record.
+#include <algorithm>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace ficb {
+
+constexpr int kScanRows = 256;                  // range-operand rows per CTA: 32 ranges x 8 isometries (MMA N)
+constexpr int kScanRanges = kScanRows / kSyms;  // 32
+constexpr int kPoolBlock = 128;                 // domains per pool-builder CTA (pool padding)
+constexpr int kScanTileDom = 128;               // domains per pool tile (MMA M = TMEM lanes)
+constexpr int kScanMaxStages = 16;
+constexpr int kScanEpiWarps = 16;
+constexpr int kScanThreads = (2 + kScanEpiWarps) * 32;
+constexpr uint32_t kScanTmemCols = 512;
+constexpr int kWarpBuf = 64;                    // survivor staging entries per epilogue warp
+constexpr int kSmemBudget = 220 * 1024;
+
+// Survivor list entry: (encoded range r * 8 + isometry, canonical domain).
+typedef uint2 SurvEntry;
+
+// ------------------------------------------------------------------ K1: normalised pool
+// One CTA per 128 domains.  Phase 1: one thread per domain contracts its 2n x 2n window
+// into 2x2 group sums q (encoder.cpp:205-219) and forms Sq, Sqq and den = N*Sqq - Sq^2
+// exactly; flat iff (double)den <= 16*shadow_eps (encoder.cpp:223).  Phase 2: all threads
+// write the tile's fp16 operand (UMMA K-major no-swizzle core matrices, 16-byte coalesced
+// chunks: [domain/8][k/8][domain%8][8 halves]) and the exact u16 q rows.
+__global__ void __launch_bounds__(kPoolBlock)
+pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __restrict__ upool,
+               unsigned short* __restrict__ qpool, DomainMetaI* __restrict__ meta_i,
+               unsigned long long* __restrict__ flat_count) {
+  extern __shared__ __align__(16) unsigned short sq_tile[];  // 128 x N contracted cells
+  __shared__ double s_inv[kPoolBlock];
+  __shared__ long long s_sum[kPoolBlock];
+  __shared__ unsigned char s_perm[kSyms * 64];
+  __shared__ unsigned s_flat;
+  const int t = threadIdx.x;
+  const int N = g.N, n = g.n, K = g.K;
+  const long long dbase = (long long)blockIdx.x * kPoolBlock;
+  if (t == 0) s_flat = 0;
+  for (int k = t; k < kSyms * N; k += kPoolBlock) {  // perm_s(i) (transforms.cpp:13-26)
+    const int s = k / N, i = k % N;
+    int sr, sc;
+    symmetry_source(s, i / n, i % n, n, sr, sc);
+    s_perm[k] = (unsigned char)(sr * n + sc);
+  }
+  // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step
+  for (int idx = t; idx < kPoolBlock * N; idx += kPoolBlock) {
+    const int dl = idx / N, j = idx % N;
+    const long long d = dbase + dl;
+    int v = 0;
+    if (d < g.D) {
+      int x, y;
+      domain_origin(g, (int)d, x, y);
+      const unsigned char* row0 = img + (long long)(y + 2 * (j / n)) * g.W + x + 2 * (j % n);
+      const unsigned char* row1 = row0 + g.W;
+      v = row0[0] + row0[1] + row1[0] + row1[1];
+    }
+    sq_tile[idx] = (unsigned short)v;
+  }
+  __syncthreads();
+  // moments of domain t: Sq, Sqq, den = N*Sqq - Sq^2 (exact), flat iff (double)den <= 16*shadow_eps (encoder.cpp:223)
+  {
+    const long long d = dbase + t;
+    long long s = 0, ss = 0;
+    for (int j = 0; j < N; ++j) {
+      const int v = sq_tile[t * N + ((j + t) % N)];  // rotated start: fewer bank conflicts
+      s += v;
+      ss += (long long)v * v;
+    }
+    if (d < g.D) {
+      const long long den = (long long)N * ss - s * s;
+      const bool flat = (double)den <= 16.0 * g.shadow_eps;
+      meta_i[d] = DomainMetaI{s, flat ? -1 : den};
+      s_inv[t] = flat ? 0.0 : 1.0 / sqrt((double)den);
+      if (flat) atomicAdd(&s_flat, 1u);
+    } else {
+      meta_i[d] = DomainMetaI{0, -1};
+      s_inv[t] = 0.0;
+    }
+    s_sum[t] = s;
+  }
+  __syncthreads();
+  if (t == 0 && s_flat) atomicAdd(flat_count, (unsigned long long)s_flat);
+  // phase 2a: fp16 normalised operand u = (N q - Sq) / sqrt(den), UMMA K-major no-swizzle
+  // core matrices, chunk c = ((dl/8) * (K/8) + k/8) * 8 + dl%8 (16-byte coalesced stores)
+  uint4* out = reinterpret_cast<uint4*>(upool + dbase * K);
+  const int kc_n = K / 8;
+  for (int c = t; c < kPoolBlock * kc_n; c += kPoolBlock) {
+    const int d8 = c & 7, kc = (c >> 3) % kc_n, dg = (c >> 3) / kc_n;
+    const int dl = dg * 8 + d8;
+    const double inv = s_inv[dl];
+    const double sN = (double)s_sum[dl];
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint32_t pair = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = kc * 8 + 2 * h + u;
+        float v = 0.f;
+        if (k < N) v = (float)(((double)N * (double)sq_tile[dl * N + k] - sN) * inv);
+        pair |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * u);
+      }
+      w[h] = pair;
+    }
+    out[c] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  // phase 2b: exact contracted cells per isometry, row (d, s)[i] = q[perm_s(i)] (u16): the
+  // survivor evaluation reads one contiguous row instead of gathering through the isometry
+  if (N >= 8) {
+    const int wpr = N / 8;  // 16-byte words per row
+    uint4* qdst = reinterpret_cast<uint4*>(qpool + dbase * kSyms * N);
+    for (int c = t; c < kPoolBlock * kSyms * wpr; c += kPoolBlock) {
+      const int w = c % wpr, row = c / wpr, sym = row & 7, dl = row >> 3;
+      const unsigned char* pr = s_perm + sym * N + w * 8;
+      const unsigned short* qs = sq_tile + dl * N;
+      uint32_t v[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) v[h] = (uint32_t)qs[pr[2 * h]] | ((uint32_t)qs[pr[2 * h + 1]] << 16);
+      qdst[c] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+  } else {  // N == 4: one 8-byte row per (domain, isometry)
+    uint2* qdst = reinterpret_cast<uint2*>(qpool + dbase * kSyms * N);
+    for (int row = t; row < kPoolBlock * kSyms; row += kPoolBlock) {
+      const int sym = row & 7, dl = row >> 3;
+      const unsigned char* pr = s_perm + sym * N;
+      const unsigned short* qs = sq_tile + dl * N;
+      qdst[row] = make_uint2((uint32_t)qs[pr[0]] | ((uint32_t)qs[pr[1]] << 16),
+                             (uint32_t)qs[pr[2]] | ((uint32_t)qs[pr[3]] << 16));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bound threshold
+// |X~| <= T  =>  R* >= bar + delta  (see the header).  err covers the fp16 rounding of both
+// operands (relative 2^-11 each, |sum u b| <= |u| |b| = sqrt(N * ssb)), the fp32
+// accumulation of K products (2^-21 relative each, generous) and fp16 subnormals.
+__device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, int K) {
+  const double t = (ssb - bar) - 1e-6 * (1.0 + bar);
+  if (!(t > 0.0)) return -1.f;  // no usable bar (also bar == +inf): everything survives
+  const double sqrtT = sqrt((double)N * t) * (1.0 - 1e-6);
+  const double err = (9.765625e-4 * 1.0005 + (double)K * 4.76837158203125e-7) * 1.05 * sqrt((double)N * ssb) + 0.01;
+  const double T = sqrtT - err;
+  return T > 0.0 ? __double2float_rd(T) : -1.f;
+}
+
+// ------------------------------------------------------------------ exact evaluation
+// One candidate of a range, given a_i = q[perm_s(i)] (its domain's contracted cells in the
+// isometry's order, i.e. range-pixel order, encoder.cpp:236-240) packed two u16 per word,
+// following encoder.cpp:241-280 operation by operation (round-to-nearest intrinsics, no
+// FMA).  Returns the residual, or +inf when a bound shows it cannot reach `thr` (tight LS
+// bound, then the reference's own screens with their +1e-3 margins).  Control flow does
+// not depend on the isometry.
+__device__ __forceinline__ int q_at(const uint32_t* qw, int i) { return (int)((qw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu); }
+
+template <int NN>
+__device__ __forceinline__ double eval_exact(const Geometry& g, const uint32_t* qw, const uint32_t* bpk, int sb,
+                                             double ssb, long long sqv, long long denv, double thr, bool screens,
+                                             unsigned& qs_out, unsigned& qo_out) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int acc = 0;
+#pragma unroll
+  for (int i = 0; i < NN; ++i) acc += q_at(qw, i) * (int)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+  const double count_d = (double)NN;
+  const double inv_count = 1.0 / count_d;
+  const double den_d = (double)denv;
+  const double sa_d = __dmul_rn((double)sqv, 0.25);
+  const double sb_d = (double)sb;
+  const double smax = g.s_max;
+  const long long num_q = (long long)NN * acc - sqv * (long long)sb;
+  const double num_d = (double)num_q;
+  if (screens) {
+    const double rstar = ssb - (num_d * num_d) / (count_d * den_d);
+    if (rstar >= thr + 1e-6 * (1.0 + thr)) return inf;
+  }
+  const double s_raw = __ddiv_rn(__dmul_rn(4.0, num_d), den_d);       // encoder.cpp:248
+  const double sc = clampd(s_raw, -smax, smax);                       // :249
+  const unsigned qs = quantize(sc, smax, g.s_bits);                   // :250
+  const double s_deq = dequantize(qs, smax, g.s_bits);                // :251
+  const double cov = __dmul_rn(__dmul_rn(num_d, 0.25), inv_count);    // :253-263
+  const double var_a = __dmul_rn(__dmul_rn(den_d, 0.0625), inv_count);
+  const double parabola =
+      __dadd_rn(__dsub_rn(ssb, __dmul_rn(__dmul_rn(2.0, s_deq), cov)), __dmul_rn(__dmul_rn(s_deq, s_deq), var_a));
+  if (screens && parabola >= thr + 1e-3) return inf;
+  const double o = clampd(__dmul_rn(__dsub_rn(sb_d, __dmul_rn(sc, sa_d)), inv_count), -255.0, 255.0);  // :265-267
+  const unsigned qo = quantize(o, 255.0, g.o_bits);
+  const double o_deq = dequantize(qo, 255.0, g.o_bits);
+  const double o_gap = __dsub_rn(o_deq, __dmul_rn(__dsub_rn(sb_d, __dmul_rn(s_deq, sa_d)), inv_count));
+  const double screen = __dadd_rn(parabola, __dmul_rn(__dmul_rn(count_d, o_gap), o_gap));
+  if (screens && screen >= thr + 1e-3) return inf;  // :272
+  double r_val = 0.0;                                 // :274-280, pixel order
+#pragma unroll
+  for (int i = 0; i < NN; ++i) {
+    const double ai = __dmul_rn((double)q_at(qw, i), 0.25);
+    const double bi = (double)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+    const double dd = __dsub_rn(__dadd_rn(__dmul_rn(s_deq, ai), o_deq), bi);
+    r_val = __dadd_rn(r_val, __dmul_rn(dd, dd));
+  }
+  qs_out = qs;
+  qo_out = qo;
+  return r_val;
+}
+
+// Dequantised values of every code (UniformQuantizer::dequantize, format.hpp:34-40), computed
+// once per encode with the same device function, so table lookups are bit-identical to it.
+struct DeqTables {
+  const double* s;  // 2^s_bits entries
+  const double* o;  // 2^o_bits entries
+};
+
+// The exact residual of encoder.cpp:274-280 (pixel order, each operation rounded) for given
+// dequantised s and o, operands read from memory in a rolled loop (out of line and light on
+// registers: only candidates that pass every screen get here).
+template <int NN>
+__device__ __noinline__ double residual_reload(const Geometry g, const unsigned short* __restrict__ qpool,
+                                               const unsigned char* __restrict__ img, int d, int s, int x0, int y0,
+                                               double s_deq, double o_deq) {
+  constexpr int n = NN == 4 ? 2 : (NN == 16 ? 4 : 8);
+  const unsigned short* qrow = qpool + ((long long)d * kSyms + s) * NN;
+  double r_val = 0.0;
+#pragma unroll 1
+  for (int i = 0; i < NN; ++i) {
+    const double ai = __dmul_rn((double)qrow[i], 0.25);
+    const double bi = (double)img[(long long)(y0 + i / n) * g.W + x0 + i % n];
+    const double dd = __dsub_rn(__dadd_rn(__dmul_rn(s_deq, ai), o_deq), bi);
+    r_val = __dadd_rn(r_val, __dmul_rn(dd, dd));
+  }
+  return r_val;
+}
+
+// eval_exact for the rare boundary cases of eval_fast, operands read from memory in rolled
+// loops (out of line, light on registers).  Same arithmetic as eval_exact.
+template <int NN>
+__device__ __noinline__ double eval_exact_reload(const Geometry g, const unsigned short* __restrict__ qpool,
+                                                 const unsigned char* __restrict__ img, int d, int s, int x0, int y0,
+                                                 int sb, double ssb, long long sqv, long long denv, double thr,
+                                                 bool screens, unsigned* qs_out, unsigned* qo_out) {
+  constexpr int n = NN == 4 ? 2 : (NN == 16 ? 4 : 8);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const unsigned short* qrow = qpool + ((long long)d * kSyms + s) * NN;
+  int acc = 0;
+#pragma unroll 1
+  for (int i = 0; i < NN; ++i) acc += (int)qrow[i] * (int)img[(long long)(y0 + i / n) * g.W + x0 + i % n];
+  const double count_d = (double)NN;
+  const double inv_count = 1.0 / count_d;
+  const double den_d = (double)denv;
+  const double sa_d = __dmul_rn((double)sqv, 0.25);
+  const double sb_d = (double)sb;
+  const double smax = g.s_max;
+  const long long num_q = (long long)NN * acc - sqv * (long long)sb;
+  const double num_d = (double)num_q;
+  if (screens) {
+    const double rstar = ssb - (num_d * num_d) / (count_d * den_d);
+    if (rstar >= thr + 1e-6 * (1.0 + thr)) return inf;
+  }
+  const double s_raw = __ddiv_rn(__dmul_rn(4.0, num_d), den_d);
+  const double sc = clampd(s_raw, -smax, smax);
+  const unsigned qs = quantize(sc, smax, g.s_bits);
+  const double s_deq = dequantize(qs, smax, g.s_bits);
+  const double cov = __dmul_rn(__dmul_rn(num_d, 0.25), inv_count);
+  const double var_a = __dmul_rn(__dmul_rn(den_d, 0.0625), inv_count);
+  const double parabola =
+      __dadd_rn(__dsub_rn(ssb, __dmul_rn(__dmul_rn(2.0, s_deq), cov)), __dmul_rn(__dmul_rn(s_deq, s_deq), var_a));
+  if (screens && parabola >= thr + 1e-3) return inf;
+  const double o = clampd(__dmul_rn(__dsub_rn(sb_d, __dmul_rn(sc, sa_d)), inv_count), -255.0, 255.0);
+  const unsigned qo = quantize(o, 255.0, g.o_bits);
+  const double o_deq = dequantize(qo, 255.0, g.o_bits);
+  const double o_gap = __dsub_rn(o_deq, __dmul_rn(__dsub_rn(sb_d, __dmul_rn(s_deq, sa_d)), inv_count));
+  const double screen = __dadd_rn(parabola, __dmul_rn(__dmul_rn(count_d, o_gap), o_gap));
+  if (screens && screen >= thr + 1e-3) return inf;
+  *qs_out = qs;
+  *qo_out = qo;
+  return residual_reload<NN>(g, qpool, img, d, s, x0, y0, s_deq, o_deq);
+}
+
+// floor(t + 0.5) of a scaled quantiser argument known to within ~1e-12, or -1 when it is
+// within 1e-9 of a rounding boundary (the caller then takes the exact path).
+__device__ __forceinline__ int safe_code(double scaled) {
+  const double t = scaled + 0.5;
+  const double f = floor(t);
+  const double fr = t - f;
+  return (fr < 1e-9 || fr > 1.0 - 1e-9) ? -1 : (int)f;
+}
+
+// Same result as eval_exact (bit-identical residual and codes, same +inf cases up to the
+// screens, which only ever reject candidates whose residual exceeds thr + 1e-3 - 1e-9),
+// but without IEEE divisions on the common path: s and o are quantised from reciprocal
+// products and the codes are checked to lie away from rounding boundaries (else the
+// exact operation-by-operation path is taken); the dequantised values come from tables.
+// upper_only: return an upper bound of the exact residual from the closed form
+// parabola(s_deq) + N*o_gap^2 (seeding the bar; no residual loop).
+template <int NN>
+__device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* qw, const uint32_t* bpk, int sb,
+                                            double ssb, long long sqv, long long denv, double thr, bool screens,
+                                            bool upper_only, const DeqTables& tab, const unsigned short* qpool,
+                                            const unsigned char* img, int d, int s, int x0, int y0,
+                                            unsigned& qs_out, unsigned& qo_out) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int acc = 0;
+#pragma unroll
+  for (int i = 0; i < NN; ++i) acc += q_at(qw, i) * (int)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+  const long long num_q = (long long)NN * acc - sqv * (long long)sb;
+  const double num_d = (double)num_q, den_d = (double)denv, sb_d = (double)sb;
+  const double smax = g.s_max;
+  const unsigned ms = (1u << g.s_bits) - 1u, mo = (1u << g.o_bits) - 1u;
+  // s_raw = 4 num / den, clamped; quantised away from boundaries
+  const double s_raw = 4.0 * num_d * (1.0 / den_d);
+  const double sc = fmin(fmax(s_raw, -smax), smax);
+  int qs;
+  if (num_q == 0) {
+    qs = 0;
+  } else {
+    const int c = safe_code((sc + smax) * (1.0 / (2.0 * smax)) * (double)ms);
+    if (c < 0 || fabs(fabs(s_raw) - smax) < 1e-12 * smax) goto exact;
+    qs = c < 1 ? 1 : (c > (int)ms ? (int)ms : c);
+  }
+  {
+    const double s_deq = tab.s[qs];
+    const double sa_d = (double)sqv * 0.25;
+    const double inv_count = 1.0 / (double)NN;
+    const double cov = num_d * 0.25 * inv_count;
+    const double var_a = den_d * 0.0625 * inv_count;
+    const double parabola = ssb - 2.0 * s_deq * cov + s_deq * s_deq * var_a;
+    if (screens && parabola >= thr + (1e-3 - 1e-9)) return inf;
+    const double o = fmin(fmax((sb_d - sc * sa_d) * inv_count, -255.0), 255.0);
+    if (fabs(o) < 1e-9) goto exact;  // quantize(0) is the special code 0
+    const int c = safe_code((o + 255.0) * (1.0 / 510.0) * (double)mo);
+    if (c < 0 || fabs(fabs(o) - 255.0) < 1e-9) goto exact;
+    const unsigned qo = c < 1 ? 1u : (c > (int)mo ? mo : (unsigned)c);
+    const double o_deq = tab.o[qo];
+    const double o_gap = o_deq - (sb_d - s_deq * sa_d) * inv_count;
+    const double screen = parabola + (double)NN * o_gap * o_gap;
+    if (upper_only) {
+      qs_out = qs;
+      qo_out = qo;
+      return screen * (1.0 + 1e-9) + 1e-6;
+    }
+    if (screens && screen >= thr + (1e-3 - 1e-9)) return inf;
+    qs_out = qs;
+    qo_out = qo;
+    return residual_reload<NN>(g, qpool, img, d, s, x0, y0, s_deq, o_deq);
+  }
+exact:
+  return eval_exact_reload<NN>(g, qpool, img, d, s, x0, y0, sb, ssb, sqv, denv, upper_only ? inf : thr,
+                               screens && !upper_only, &qs_out, &qo_out);
+}
+
+__global__ void deq_tables_kernel(Geometry g, double* ts, double* to) {
+  const int ns = 1 << g.s_bits, no = 1 << g.o_bits;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ns + no; c += gridDim.x * blockDim.x) {
+    if (c < ns) ts[c] = dequantize((unsigned)c, g.s_max, g.s_bits);
+    else to[c - ns] = dequantize((unsigned)(c - ns), 255.0, g.o_bits);
+  }
+}
+
+// The (domain d, isometry s) row of the q8 pool into registers.
+template <int NN>
+__device__ __forceinline__ void load_q8_row(const unsigned short* __restrict__ qpool, int d, int s, uint32_t* qw) {
+  const unsigned short* row = qpool + ((long long)d * kSyms + s) * NN;
+  if constexpr (NN >= 8) {
+#pragma unroll
+    for (int w = 0; w < NN / 8; ++w) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + w);
+      qw[4 * w] = v.x;
+      qw[4 * w + 1] = v.y;
+      qw[4 * w + 2] = v.z;
+      qw[4 * w + 3] = v.w;
+    }
+  } else {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(row));
+    qw[0] = v.x;
+    qw[1] = v.y;
+  }
+}
+
+__device__ __forceinline__ double load_bar(const unsigned long long* gbest, int r) {
+  return __longlong_as_double((long long)__ldcg(gbest + r));
+}
+
+// ------------------------------------------------------------------ seed
+// Exact evaluation of the 8 isometries of the (2h+1)^2 grid domains around each range's own
+// 2x-scaled neighbourhood (self-similar candidates that usually fit well) to give the
+// first scan level a bar.  One thread per (range, local domain, isometry).
+constexpr int kSeedHalf = 2;
+constexpr int kSeedSide = 2 * kSeedHalf + 1;
+constexpr int kSeedPerRange = kSeedSide * kSeedSide * kSyms;
+
+template <int NN>
+__global__ void __launch_bounds__(128)
+seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
+               const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
+               unsigned long long* __restrict__ gbest, DeqTables tab) {
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)g.R * kSeedPerRange) return;
+  const int r = (int)(tid / kSeedPerRange), k = (int)(tid % kSeedPerRange);
+  const int s = k % kSyms, w = k / kSyms;
+  const RangeMeta m = rmeta[r];
+  if (m.shadow || g.D == 0) return;
+  int x0, y0;
+  range_origin(g, r, x0, y0);
+  const int cx = x0 - g.n / 2, cy = y0 - g.n / 2;
+  const int xi0 = min(max(cx / g.step, 0), g.PX - 1), yi0 = min(max(cy / g.step, 0), g.PY - 1);
+  const int xi = xi0 + w / kSeedSide - kSeedHalf, yi = yi0 + w % kSeedSide - kSeedHalf;
+  if (xi < 0 || yi < 0 || xi >= g.PX || yi >= g.PY) return;
+  const int d = xi * g.PY + yi;
+  const DomainMetaI mi = meta_i[d];
+  if (mi.den < 0) return;
+  uint32_t qw[NN / 2], bpk[NN / 4];
+  load_q8_row<NN>(qpool, d, s, qw);
+  load_range_words<NN>(img, g, x0, y0, bpk);
+  unsigned qs, qo;
+  // an upper bound of the candidate's exact residual is a valid pruning bar
+  const double v = eval_fast<NN>(g, qw, bpk, m.sb, (double)m.var / (double)NN, mi.sq, mi.den,
+                                 __longlong_as_double(0x7ff0000000000000ll), false, true, tab, qpool, img, d, s, x0,
+                                 y0, qs, qo);
+  publish_best(gbest, r, v);
+}
+
+// ------------------------------------------------------------------ K2: tensor-core scan
+struct ScanSmem {
+  uint32_t r_bytes, p_bytes, stages, r_off, p_off, bar_off, wbuf_off, total;
+};
+
+// Shared memory: two range operands (256 rows x K fp16 each), a ring of pool tiles
+// (128 domains x K fp16), barriers, per-warp survivor staging.
+__host__ __device__ inline ScanSmem scan_smem_layout(int K) {
+  ScanSmem L;
+  L.r_bytes = kScanRows * K * 2;
+  L.p_bytes = kScanTileDom * K * 2;
+  L.r_off = 0;
+  L.p_off = 2 * L.r_bytes;
+  const uint32_t fixed = L.p_off + 512 + kScanEpiWarps * kWarpBuf * 8;
+  uint32_t st = (kSmemBudget - fixed) / L.p_bytes;
+  L.stages = st > kScanMaxStages ? kScanMaxStages : st;
+  L.bar_off = L.p_off + L.stages * L.p_bytes;
+  L.wbuf_off = L.bar_off + 512;
+  L.total = L.wbuf_off + kScanEpiWarps * kWarpBuf * 8;
+  return L;
+}
+
+// Work of one scan level.  A "segment" is (m-tile, level-tile range): the CTA keeps the
+// m-tile's range operand resident and streams the pool tiles of the range.  Full rounds:
+// CTA c takes m-tile r*G + c over all level tiles (all CTAs sweep the pool in step, so each
+// pool tile is read from L2 by every CTA within a short window).  The m-tiles left over
+// (M' < G) are split into k chunks of the tile range, ordered chunk-major, and the M'*k
+// units are shared out contiguously.
+struct ScanLevel {
+  int stride;     // tile stride of this level (1 = full scan)
+  int n_lvl;      // tiles in the level: ceil(n_tiles / stride)
+  int m_tiles;    // 256-row range tiles: ceil(R / 32)
+  int rounds;     // full rounds: m_tiles / G
+  int rem;        // m-tiles of the last round: m_tiles % G
+  int k;          // chunks per leftover m-tile
+};
+
+struct Segment {
+  int m, j0, j1;  // m-tile, level tiles [j0, j1)
+};
+
+__host__ __device__ inline int seg_count(const ScanLevel& lv, int c, int G) {
+  if (lv.rem == 0) return lv.rounds;
+  const long long U = (long long)lv.rem * lv.k;
+  return lv.rounds + (int)(U * (c + 1) / G - U * c / G);
+}
+
+__host__ __device__ inline Segment seg_at(const ScanLevel& lv, int c, int G, int s) {
+  Segment sg;
+  if (s < lv.rounds) {
+    sg.m = s * G + c;
+    sg.j0 = 0;
+    sg.j1 = lv.n_lvl;
+    return sg;
+  }
+  const long long U = (long long)lv.rem * lv.k;
+  const long long u = U * c / G + (s - lv.rounds);
+  const int chunk = (int)(u / lv.rem), mr = (int)(u % lv.rem);
+  sg.m = lv.rounds * G + mr;
+  sg.j0 = (int)((long long)lv.n_lvl * chunk / lv.k);
+  sg.j1 = (int)((long long)lv.n_lvl * (chunk + 1) / lv.k);
+  return sg;
+}
+
+// Range operand of m-tile `mt` into `sR` (threads [tid, tid + nthreads)): row
+// rl * 8 + s holds the centred range rl permuted by isometry s's inverse,
+// R[row][j] = b[i] - Sb/N with perm_s(i) = j, so sum_j u_j R[row][j] = sum_i u[perm_s(i)] (b_i - Sb/N).
+__device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict__ img, const Geometry& g,
+                             const RangeMeta* __restrict__ rmeta, int mt, int tid, int nthreads) {
+  const int K = g.K, N = g.N, n = g.n;
+  const int chunks = kScanRows * (K / 8);
+  for (int c = tid; c < chunks; c += nthreads) {
+    const int row = c / (K / 8), kc = c % (K / 8);
+    const int rl = row >> 3, s = row & 7;
+    const int r = mt * kScanRanges + rl;
+    const int sinv = s == 1 ? 3 : (s == 3 ? 1 : s);  // inverse isometries: 1 <-> 3, the others are involutions
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (r < g.R) {
+      int x0, y0;
+      range_origin(g, r, x0, y0);
+      const float mean = (float)rmeta[r].sb / (float)N;  // exact: N is a power of two
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int j = kc * 8 + h;
+        if (j < N) {
+          int ir, ic;
+          symmetry_source(sinv, j / n, j % n, n, ir, ic);  // i with perm_s(i) = j
+          const float v = (float)img[(long long)(y0 + ir) * g.W + x0 + ic] - mean;
+          w[h >> 1] |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * (h & 1));
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(sR + (row >> 3) * K * 16 + kc * 128 + (row & 7) * 16) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Per-range scan thresholds of a level (scan_threshold against the range's current bar);
+// padded to whole m-tiles.  Invalid and shadow ranges get +1e30 (never survive), flags & 1
+// (exhaustive debug mode) -1 (everything survives).
+__global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta,
+                                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr, int padded) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= padded) return;
+  float t = 1e30f;
+  if (r < g.R) {
+    const RangeMeta rm = rmeta[r];
+    if (!rm.shadow) t = (g.flags & 1) ? -1.f : scan_threshold((double)rm.var / (double)g.N, load_bar(gbest, r), g.N, g.K);
+  }
+  thr[r] = t;
+}
+
+// Range operands of every m-tile, built once per encode into global memory (one CTA per
+// m-tile, r_bytes each) so the scan loads them with one bulk copy per segment.
+__global__ void __launch_bounds__(256)
+range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
+                unsigned char* __restrict__ ropnd) {
+  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, blockIdx.x, threadIdx.x, 256);
+}
+
+// Warp-cooperative append: lane's entries (rowbase + bit, d) for the set bits of `mask`
+// go to the warp's staging buffer; full batches of 32 go to the CTA's list partition,
+// reserved with one shared-memory atomic (entries past the partition are counted, dropped).
+__device__ __forceinline__ void append_bits(uint32_t mask, uint32_t rowbase, uint32_t d, SurvEntry* wb, int& fill,
+                                            SurvEntry* __restrict__ list, unsigned long long* count,
+                                            unsigned long long cap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  while (true) {
+    const bool has = mask != 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, has);
+    if (!bal) break;
+    if (has) {
+      const int b = __ffs(mask) - 1;
+      mask &= mask - 1;
+      wb[fill + __popc(bal & lt)] = make_uint2(rowbase + (uint32_t)b, d);
+    }
+    fill += __popc(bal);
+    if (fill >= 32) {
+      __syncwarp();
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(count, 32ull);  // shared-memory counter
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + lane < cap) list[base + lane] = wb[lane];
+      SurvEntry tail = make_uint2(0, 0);
+      if (lane < fill - 32) tail = wb[32 + lane];
+      __syncwarp();
+      if (lane < fill - 32) wb[lane] = tail;
+      fill -= 32;
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ float absmax8(const uint32_t* v) {
+  const float* f = reinterpret_cast<const float*>(v);
+  return fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
+                     fmaxf(fabsf(f[4]), fabsf(f[5]))),
+               fmaxf(fabsf(f[6]), fabsf(f[7])));
+}
+
+// Tests one 32-column TMEM chunk (4 ranges x 8 isometries) of this lane's domain against
+// the 4 ranges' thresholds and appends the columns above them.
+__device__ __forceinline__ void test_chunk(const uint32_t* v, const float* T, uint32_t rowbase, uint32_t d,
+                                           SurvEntry* wb, int& fill, SurvEntry* __restrict__ list,
+                                           unsigned long long* count, unsigned long long cap) {
+  float gm[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gm[k] = absmax8(v + 8 * k);
+  const bool hit = (gm[0] > T[0]) | (gm[1] > T[1]) | (gm[2] > T[2]) | (gm[3] > T[3]);
+  if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t bits = 0;
+      if (gm[k] > T[k]) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > T[k]) << c;
+      }
+      if (__any_sync(0xffffffffu, bits != 0)) append_bits(bits, rowbase + 8u * k, d, wb, fill, list, count, cap);
+    }
+  }
+}
+
+// Persistent scan over the segments of ScanLevel (see there); 18 warps:
+//   warp 0        lane 0: bulk-copy producer, 128-domain pool tiles (contiguous 128*K*2 bytes) ->
+//                 smem ring; lane 1: range-operand loader, the segment's 256 x K operand (built
+//                 once per encode by range_op_kernel) -> one of two smem buffers
+//   warp 1        TMEM allocation; lane 0: MMA issuer, K/16 x tcgen05.mma M=128 (domains) x
+//                 N=256 (32 ranges x 8 isometries) x K=16 per tile into one of two 256-column
+//                 TMEM accumulators
+//   warps 2-17    epilogue: 16 warps (lane quarter x column quarter); for every tile a thread
+//                 owns one domain (TMEM lane) and 8 ranges x 8 isometries
+//                 (128 columns), tests each range's 8-isometry |max| against the range's
+//                 threshold and appends the rare columns above it to the survivor list
+__global__ void __launch_bounds__(kScanThreads, 1)
+scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
+            const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
+            const float* __restrict__ thr, SurvEntry* __restrict__ list_all,
+            unsigned long long* __restrict__ counts, unsigned long long cap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const ScanSmem L = scan_smem_layout(g.K);
+  const int K = g.K;
+  unsigned char* sR = smem + L.r_off;
+  unsigned char* sP = smem + L.p_off;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* empty_bar = full_bar + kScanMaxStages;
+  uint64_t* tfull_bar = empty_bar + kScanMaxStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* rfull_bar = tempty_bar + 2;
+  uint64_t* rempty_bar = rfull_bar + 2;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(rempty_bar + 2);
+  unsigned long long* count = reinterpret_cast<unsigned long long*>(smem + L.bar_off + 448);  // CTA survivors
+  SurvEntry* wbuf_all = reinterpret_cast<SurvEntry*>(smem + L.wbuf_off);
+  SurvEntry* list = list_all + (unsigned long long)blockIdx.x * cap;  // this CTA's partition of `cap` entries
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int nseg = seg_count(lv, cta, G);
+  const int stages = (int)L.stages;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], kScanEpiWarps);  // every epilogue warp reads every tile
+      ptx::mbar_init(&rfull_bar[b], 1);    // arrive.expect_tx of the range-operand loader
+      ptx::mbar_init(&rempty_bar[b], 1);   // tcgen05.commit after a segment's last MMA
+    }
+    ptx::fence_mbar_init();
+    *count = 0;
+  }
+  if (warp == 1) ptx::tmem_alloc<kScanTmemCols>(tmem_base_smem);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ================= producer (lane 0) and range-operand loader (lane 1) =================
+    if (lane == 1) {
+      for (int sg = 0; sg < nseg; ++sg) {
+        if (sg >= 2) ptx::mbar_wait(&rempty_bar[sg & 1], ((sg >> 1) - 1) & 1);
+        ptx::mbar_arrive_expect_tx(&rfull_bar[sg & 1], L.r_bytes);
+        ptx::bulk_g2s(sR + (sg & 1) * L.r_bytes, ropnd + (long long)seg_at(lv, cta, G, sg).m * L.r_bytes, L.r_bytes,
+                      &rfull_bar[sg & 1]);
+      }
+    }
+    if (lane == 0) {
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(upool);
+      int i = 0;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const Segment S = seg_at(lv, cta, G, sg);
+        for (int j = S.j0; j < S.j1; ++j, ++i) {
+          const int s = i % stages;
+          ptx::mbar_wait(&empty_bar[s], ((i / stages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_bar[s], L.p_bytes);
+          ptx::bulk_g2s(sP + s * L.p_bytes, src + (long long)j * lv.stride * L.p_bytes, L.p_bytes, &full_bar[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_f16_f32(128, kScanRows);
+      int i = 0;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const Segment S = seg_at(lv, cta, G, sg);
+        ptx::mbar_wait(&rfull_bar[sg & 1], (sg >> 1) & 1);
+        const uint32_t r_base = ptx::smem_addr(sR + (sg & 1) * L.r_bytes);
+        for (int j = S.j0; j < S.j1; ++j, ++i) {
+          const int s = i % stages;
+          const int buf = i & 1;
+          ptx::mbar_wait(&tempty_bar[buf], ((i >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
+          ptx::tc_fence_after();
+          const uint32_t p_base = ptx::smem_addr(sP + s * L.p_bytes);
+          if (!(g.flags & 16)) {  // debug: flags & 16 skips the MMAs
+#pragma unroll 1
+            for (int kk = 0; kk < K / 16; ++kk) {
+              const uint64_t ad = ptx::smem_desc(p_base + kk * 256, 128, K * 16);
+              const uint64_t bd = ptx::smem_desc(r_base + kk * 256, 128, K * 16);
+              ptx::mma_f16_ss(tmem_base + buf * kScanRows, ad, bd, idesc, kk > 0 ? 1u : 0u);
+            }
+          }
+          ptx::tc_commit(&empty_bar[s]);
+          ptx::tc_commit(&tfull_bar[buf]);
+        }
+        ptx::tc_commit(&rempty_bar[sg & 1]);
+      }
+    }
+  } else {
+    // ================= epilogue =================
+    const int e = warp - 2;
+    const int cq = e >> 2;          // column quarter: ranges cq*8 .. cq*8+7 of the m-tile
+    const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
+    SurvEntry* wb = wbuf_all + e * kWarpBuf;
+    int fill = 0;
+    const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + cq * 64;
+    float T[8];
+    int i = 0;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const Segment S = seg_at(lv, cta, G, sg);
+      const int r0 = S.m * kScanRanges + cq * 8;  // this thread's 8 ranges
+      const float4 t0 = __ldg(reinterpret_cast<const float4*>(thr + r0));
+      const float4 t1 = __ldg(reinterpret_cast<const float4*>(thr + r0) + 1);
+      T[0] = t0.x; T[1] = t0.y; T[2] = t0.z; T[3] = t0.w;
+      T[4] = t1.x; T[5] = t1.y; T[6] = t1.z; T[7] = t1.w;
+      const uint32_t rowbase = (uint32_t)r0 * 8u;
+      for (int j = S.j0; j < S.j1; ++j, ++i) {
+        const int buf = i & 1;
+        const uint32_t d = (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
+        ptx::mbar_wait(&tfull_bar[buf], (i >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t ta = tcol + buf * kScanRows;
+        uint32_t va[32], vb[32];
+        __syncwarp();
+        ptx::tmem_ld_32x32b_x32(ta, va);
+        ptx::tmem_ld_32x32b_x32(ta + 32, vb);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all 64 columns read: release the buffer
+        if (!(g.flags & 8)) {
+          test_chunk(va, T, rowbase, d, wb, fill, list, count, cap);
+          test_chunk(vb, T + 4, rowbase + 32u, d, wb, fill, list, count, cap);
+        }
+      }
+    }
+    // flush the staging buffer
+    __syncwarp();
+    if (fill > 0) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(count, (unsigned long long)fill);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (lane < fill && base + lane < cap) list[base + lane] = wb[lane];
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = *count;
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<kScanTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ survivor evaluation
+// The scan's list is partitioned per scan CTA: partition c holds counts[c] entries (those
+// beyond the partition size `part` were dropped and are detected by the host).
+__device__ __forceinline__ bool list_slot(unsigned long long i, unsigned long long part,
+                                          const unsigned long long* __restrict__ counts) {
+  const unsigned long long c = i / part, j = i - c * part;
+  return j < counts[c];
+}
+
+// One thread per list entry: exact correlation from the q8 row and the range pixels, then
+// the reference's fp64 arithmetic (eval_exact) against the range's current bar; an achieved
+// residual lowers the bar.  res[i] = residual (+inf when pruned or flat).
+template <int NN>
+__global__ void __launch_bounds__(256)
+eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
+            const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
+            const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
+            unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab) {
+  const unsigned long long total = (unsigned long long)parts * part;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const bool screens = !(g.flags & 2);
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if (!list_slot(i, part, counts)) continue;
+    const SurvEntry en = list[i];
+    const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)en.y;
+    double R = inf;
+    const DomainMetaI mi = meta_i[d];
+    if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
+      const RangeMeta rm = rmeta[r];
+      int x0, y0;
+      range_origin(g, r, x0, y0);
+      uint32_t qw[NN / 2], bpk[NN / 4];
+      load_q8_row<NN>(qpool, d, s, qw);
+      load_range_words<NN>(img, g, x0, y0, bpk);
+      unsigned qs, qo;
+      R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, load_bar(gbest, r), screens,
+                        false, tab, qpool, img, d, s, x0, y0, qs, qo);
+      if (R < inf) publish_best(gbest, r, R);
+    }
+    res[i] = R;
+  }
+}
+
+// Among the final level's entries whose residual equals the range's final bar, the
+// smallest (domain, isometry): the reference's first strict minimum (encoder.cpp:281).
+__global__ void winner_kernel(const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts,
+                              int parts, unsigned long long part, const double* __restrict__ res,
+                              const unsigned long long* __restrict__ gbest, unsigned* __restrict__ win) {
+  const unsigned long long total = (unsigned long long)parts * part;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if (!list_slot(i, part, counts)) continue;
+    const SurvEntry en = list[i];
+    const int r = (int)(en.x >> 3);
+    const double R = res[i];
+    if (R < __longlong_as_double(0x7ff0000000000000ll) && (unsigned long long)__double_as_longlong(R) == gbest[r])
+      atomicMin(win + r, en.y * 8u + (en.x & 7u));
+  }
+}
+
+// RangeMapping records: the winner re-evaluated without screens (its quantised codes and
+// residual), or flat_mapping for shadow ranges / ranges without any non-flat candidate
+// (encoder.cpp:176-181, 291-308).  A winner whose residual differs from the bar it was
+// selected by would be an internal error; it is counted in `selfcheck`.
+template <int NN>
+__global__ void __launch_bounds__(128)
+record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
+              const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
+              const unsigned* __restrict__ win, const unsigned long long* __restrict__ gbest,
+              fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= g.R) return;
+  const RangeMeta m = rmeta[r];
+  int x0, y0;
+  range_origin(g, r, x0, y0);
+  uint32_t bpk[NN / 4];
+  load_range_words<NN>(img, g, x0, y0, bpk);
+  fic_mapping o;
+  o.reserved = 0;
+  const unsigned w = m.shadow ? 0xFFFFFFFFu : win[r];
+  if (w != 0xFFFFFFFFu) {
+    const int d = (int)(w >> 3), s = (int)(w & 7);
+    const DomainMetaI mi = meta_i[d];
+    uint32_t qw[NN / 2];
+    load_q8_row<NN>(qpool, d, s, qw);
+    unsigned qs = 0, qo = 0;
+    const double R = eval_exact<NN>(g, qw, bpk, m.sb, (double)m.var / (double)NN, mi.sq, mi.den,
+                                    __longlong_as_double(0x7ff0000000000000ll), false, qs, qo);
+    if ((unsigned long long)__double_as_longlong(R) != gbest[r]) atomicAdd(selfcheck, 1ull);
+    domain_origin(g, d, o.x, o.y);
+    o.sym = s;
+    o.qs = qs;
+    o.qo = qo;
+    o.residual = R;
+  } else {
+    // flat_mapping (encoder.cpp:298-308)
+    const double count_d = (double)NN;
+    const double ov = (double)m.sb / count_d;
+    const unsigned qo = quantize(ov, 255.0, g.o_bits);
+    const double o_deq = dequantize(qo, 255.0, g.o_bits);
+    double rv = 0.0;
+#pragma unroll
+    for (int i = 0; i < NN; ++i) {
+      const double dd = __dsub_rn(o_deq, (double)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu));
+      rv = __dadd_rn(rv, __dmul_rn(dd, dd));
+    }
+    o.x = 0;
+    o.y = 0;
+    o.sym = 0;
+    o.qs = 0;
+    o.qo = qo;
+    o.residual = rv;
+  }
+  out[r] = o;
+}
+
+__global__ void fill_u64_kernel(unsigned long long* p, long long n, unsigned long long v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// ------------------------------------------------------------------ host launchers
+bool scan_supported(const Geometry& g) { return g.N == 4 || g.N == 16 || g.N == 64; }
+
+int scan_tiles(const Geometry& g) { return (g.D + kScanTileDom - 1) / kScanTileDom; }
+
+// Padded domain count of the pools (a multiple of the pool-builder block).
+long long scan_pool_domains(const Geometry& g) { return (long long)((g.D + kPoolBlock - 1) / kPoolBlock) * kPoolBlock; }
+
+int scan_rows_per_cta() { return kScanRanges; }
+
+void launch_pool_v3(const unsigned char* img, const Geometry& g, __half* upool, unsigned short* qpool,
+                    DomainMetaI* meta_i, unsigned long long* flat_count, cudaStream_t st) {
+  const int blocks = (int)(scan_pool_domains(g) / kPoolBlock);
+  pool_v3_kernel<<<blocks, kPoolBlock, kPoolBlock * g.N * sizeof(unsigned short), st>>>(img, g, upool, qpool,
+                                                                                           meta_i, flat_count);
+}
+
+void launch_fill_u64(unsigned long long* p, long long n, unsigned long long v, cudaStream_t st) {
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4096);
+  fill_u64_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(p, n, v);
+}
+
+size_t deq_table_entries(const Geometry& g) { return (size_t)(1 << g.s_bits) + (size_t)(1 << g.o_bits); }
+
+void launch_deq_tables(const Geometry& g, double* deq, cudaStream_t st) {
+  deq_tables_kernel<<<64, 256, 0, st>>>(g, deq, deq + (1 << g.s_bits));
+}
+
+void launch_seed_v3(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
+                    const DomainMetaI* meta_i, const RangeMeta* rmeta, unsigned long long* gbest, const double* deq,
+                    cudaStream_t st) {
+  const long long threads = (long long)g.R * kSeedPerRange;
+  const int blocks = (int)((threads + 127) / 128);
+  const DeqTables tab{deq, deq + (1 << g.s_bits)};
+  if (g.N == 4) seed_v3_kernel<4><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
+  else if (g.N == 16) seed_v3_kernel<16><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
+  else seed_v3_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
+}
+
+// Scan CTAs (= list partitions) of a level: one per SM.
+int scan_grid(const Geometry& g, int stride, int sms) {
+  (void)g;
+  (void)stride;
+  return sms;
+}
+
+static ScanLevel make_level(const Geometry& g, int stride, int G) {
+  ScanLevel lv;
+  const int n_tiles = scan_tiles(g);
+  lv.stride = stride;
+  lv.n_lvl = (n_tiles + stride - 1) / stride;
+  lv.m_tiles = (g.R + kScanRanges - 1) / kScanRanges;
+  lv.rounds = lv.m_tiles / G;
+  lv.rem = lv.m_tiles % G;
+  lv.k = 1;
+  if (lv.rem) {  // chunks per leftover m-tile: minimise ceil(rem * k / G) / k, prefer small k
+    double best = 1e30;
+    for (int k = 1; k <= 16 && k <= lv.n_lvl; ++k) {
+      const double t = (double)((lv.rem * k + G - 1) / G) / k;
+      if (t < best - 1e-9) {
+        best = t;
+        lv.k = k;
+      }
+    }
+  }
+  return lv;
+}
+
+// counts[c] = survivors of scan CTA c; its entries are list[c * part, c * part + min(counts[c], part)).
+cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride, int sms, const __half* upool,
+                        const RangeMeta* rmeta, const unsigned char* ropnd, const float* thr, SurvEntry* list,
+                        unsigned long long* counts, unsigned long long part, cudaStream_t st) {
+  const int grid = scan_grid(g, stride, sms);
+  const ScanLevel lv = make_level(g, stride, grid);
+  const ScanSmem L = scan_smem_layout(g.K);
+  cudaError_t e = cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return e;
+  scan_kernel<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, list, counts, part);
+  return cudaGetLastError();
+}
+
+int scan_padded_ranges(const Geometry& g) { return ((g.R + kScanRanges - 1) / kScanRanges) * kScanRanges; }
+
+void launch_threshold(const Geometry& g, const RangeMeta* rmeta, const unsigned long long* gbest, float* thr,
+                      cudaStream_t st) {
+  const int padded = scan_padded_ranges(g);
+  threshold_kernel<<<(padded + 255) / 256, 256, 0, st>>>(g, rmeta, gbest, thr, padded);
+}
+
+size_t range_op_bytes(const Geometry& g) {
+  return (size_t)((g.R + kScanRanges - 1) / kScanRanges) * kScanRows * g.K * 2;
+}
+
+void launch_range_op(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta, unsigned char* ropnd,
+                     cudaStream_t st) {
+  range_op_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(img, g, rmeta, ropnd);
+}
+
+void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
+                 const RangeMeta* rmeta, const SurvEntry* list, const unsigned long long* counts, int parts,
+                 unsigned long long part, double* res, unsigned long long* gbest, const double* deq, int sms,
+                 cudaStream_t st) {
+  const int blocks = sms * 8;
+  const DeqTables tab{deq, deq + (1 << g.s_bits)};
+  if (g.N == 4)
+    eval_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab);
+  else if (g.N == 16)
+    eval_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab);
+  else
+    eval_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab);
+}
+
+void launch_winner(const SurvEntry* list, const unsigned long long* counts, int parts, unsigned long long part,
+                   const double* res, const unsigned long long* gbest, unsigned* win, int sms, cudaStream_t st) {
+  winner_kernel<<<sms * 4, 256, 0, st>>>(list, counts, parts, part, res, gbest, win);
+}
+
+void launch_record(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
+                   const DomainMetaI* meta_i, const RangeMeta* rmeta, const unsigned* win,
+                   const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck, cudaStream_t st) {
+  const int blocks = (g.R + 127) / 128;
+  if (g.N == 4) record_kernel<4><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
+  else if (g.N == 16) record_kernel<16><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
+  else record_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
+}
+
+}  // namespace ficb

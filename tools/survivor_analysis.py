@@ -118,7 +118,7 @@ def strategies(cfg="cfg2", sample=None, ks=(1, 2, 4, 8, 16, 32, 64)):
     res = {k: [] for k in ks}
     full = []
     prepass = {32: [], 512: []}
-    ch = 128
+    ch = int(os.environ.get("CH", "128"))
     for i0 in range(0, len(ridx), ch):
         b = B[i0:i0 + ch]
         sb = Sb[i0:i0 + ch, None]
