@@ -60,10 +60,11 @@ cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const _
 int scan_padded_ranges(const Geometry&);
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
 size_t range_op_bytes(const Geometry&);
-void launch_range_op(const unsigned char*, const Geometry&, const RangeMeta*, unsigned char*, cudaStream_t);
+void launch_range_op(const unsigned char*, const Geometry&, const RangeMeta*, const float*, unsigned char*,
+                     cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
-                 const double*, int, cudaStream_t);
+                 const double*, uint2*, unsigned long long*, int, cudaStream_t);
 void launch_winner(const uint2*, const unsigned long long*, int, unsigned long long, const double*,
                    const unsigned long long*, unsigned*, int, cudaStream_t);
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
@@ -205,7 +206,7 @@ struct Workspace {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag, scratch, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq;
+      diag, scratch, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
   unsigned long long list_cap = 0;  // survivor-list capacity (entries), grown on overflow
   std::mutex mu;
@@ -259,8 +260,9 @@ int matcher_mode(const Geometry& g) {
 
 constexpr int kMaxLevels = 6;
 constexpr int kPartSlots = 256;      // per-level survivor counters, one per scan CTA (<= SMs)
-constexpr int kScanCountSlots = kMaxLevels * kPartSlots + 1;  // + record self-check failures
+constexpr int kScanCountSlots = kMaxLevels * kPartSlots + 2;  // + record self-check failures, pending count
 constexpr int kSelfcheckSlot = kMaxLevels * kPartSlots;
+constexpr int kPendSlot = kSelfcheckSlot + 1;
 
 // Scan levels: sparse passes over every 8^k-th 128-domain tile (k >= 1, at least one tile)
 // seed the pruning bar, then the full scan.  Each level prunes with the bar the previous
@@ -313,12 +315,15 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
                    unsigned long long* cnt, cudaStream_t st) {
   auto* list = static_cast<uint2*>(ws.list.get((size_t)ws.list_cap * sizeof(uint2)));
   auto* res = static_cast<double*>(ws.res.get((size_t)ws.list_cap * sizeof(double)));
+  auto* pend = static_cast<uint2*>(ws.pend.get((size_t)ws.list_cap * sizeof(uint2)));
   const int parts = scan_grid(g, stride, ws.sms);
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
   launch_threshold(g, b.rm, b.gbest, b.thr, st);
+  launch_range_op(d_img, g, b.rm, b.thr, b.ropnd, st);
   CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, st));
-  launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, ws.sms, st);
-  g_launches += 3;
+  launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
+              b.cnt + kPendSlot, ws.sms, st);
+  g_launches += 5;
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a
@@ -350,8 +355,7 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
   launch_deq_tables(g, b.deq, st);
   launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
-  launch_range_op(d_img, g, b.rm, b.ropnd, st);
-  g_launches += 6;
+  g_launches += 5;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
   const std::vector<int> lv = scan_levels(g);
   for (size_t l = 0; l + 1 < lv.size(); ++l) enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st);

@@ -39,7 +39,7 @@ constexpr int kScanRanges = kScanRows / kSyms;  // 32
 constexpr int kPoolBlock = 128;                 // domains per pool-builder CTA (pool padding)
 constexpr int kScanTileDom = 128;               // domains per pool tile (MMA M = TMEM lanes)
 constexpr int kScanMaxStages = 16;
-constexpr int kScanEpiWarps = 16;
+constexpr int kScanEpiWarps = 8;
 constexpr int kScanThreads = (2 + kScanEpiWarps) * 32;
 constexpr uint32_t kScanTmemCols = 512;
 constexpr int kWarpBuf = 64;                    // survivor staging entries per epilogue warp
@@ -183,6 +183,19 @@ __device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, i
 // not depend on the isometry.
 __device__ __forceinline__ int q_at(const uint32_t* qw, int i) { return (int)((qw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu); }
 
+// sum_i q_i b_i for q packed two u16 per word and b four u8 per word: two DP2A per four
+// pixels (exact: every partial sum < 2^24).
+template <int NN>
+__device__ __forceinline__ int dot_q_b(const uint32_t* qw, const uint32_t* bpk) {
+  unsigned acc = 0;
+#pragma unroll
+  for (int w = 0; w < NN / 4; ++w) {
+    acc = __dp2a_lo(qw[2 * w], bpk[w], acc);
+    acc = __dp2a_hi(qw[2 * w + 1], bpk[w], acc);
+  }
+  return (int)acc;
+}
+
 template <int NN>
 __device__ __forceinline__ double eval_exact(const Geometry& g, const uint32_t* qw, const uint32_t* bpk, int sb,
                                              double ssb, long long sqv, long long denv, double thr, bool screens,
@@ -324,11 +337,9 @@ __device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* q
                                             double ssb, long long sqv, long long denv, double thr, bool screens,
                                             bool upper_only, const DeqTables& tab, const unsigned short* qpool,
                                             const unsigned char* img, int d, int s, int x0, int y0,
-                                            unsigned& qs_out, unsigned& qo_out) {
+                                            unsigned& qs_out, unsigned& qo_out, bool* pending = nullptr) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  int acc = 0;
-#pragma unroll
-  for (int i = 0; i < NN; ++i) acc += q_at(qw, i) * (int)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+  const int acc = dot_q_b<NN>(qw, bpk);
   const long long num_q = (long long)NN * acc - sqv * (long long)sb;
   const double num_d = (double)num_q, den_d = (double)denv, sb_d = (double)sb;
   const double smax = g.s_max;
@@ -368,6 +379,10 @@ __device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* q
     if (screens && screen >= thr + (1e-3 - 1e-9)) return inf;
     qs_out = qs;
     qo_out = qo;
+    if (pending) {  // the caller computes the residual in a separate, convergent pass
+      *pending = true;
+      return inf;
+    }
     return residual_reload<NN>(g, qpool, img, d, s, x0, y0, s_deq, o_deq);
   }
 exact:
@@ -411,7 +426,7 @@ __device__ __forceinline__ double load_bar(const unsigned long long* gbest, int 
 // Exact evaluation of the 8 isometries of the (2h+1)^2 grid domains around each range's own
 // 2x-scaled neighbourhood (self-similar candidates that usually fit well) to give the
 // first scan level a bar.  One thread per (range, local domain, isometry).
-constexpr int kSeedHalf = 2;
+constexpr int kSeedHalf = 1;
 constexpr int kSeedSide = 2 * kSeedHalf + 1;
 constexpr int kSeedPerRange = kSeedSide * kSeedSide * kSyms;
 
@@ -459,12 +474,12 @@ __host__ __device__ inline ScanSmem scan_smem_layout(int K) {
   L.p_bytes = kScanTileDom * K * 2;
   L.r_off = 0;
   L.p_off = 2 * L.r_bytes;
-  const uint32_t fixed = L.p_off + 512 + kScanEpiWarps * kWarpBuf * 8;
+  const uint32_t fixed = L.p_off + 512 + kScanEpiWarps * kWarpBuf * (uint32_t)sizeof(SurvEntry);
   uint32_t st = (kSmemBudget - fixed) / L.p_bytes;
   L.stages = st > kScanMaxStages ? kScanMaxStages : st;
   L.bar_off = L.p_off + L.stages * L.p_bytes;
   L.wbuf_off = L.bar_off + 512;
-  L.total = L.wbuf_off + kScanEpiWarps * kWarpBuf * 8;
+  L.total = L.wbuf_off + kScanEpiWarps * kWarpBuf * (uint32_t)sizeof(SurvEntry);
   return L;
 }
 
@@ -510,11 +525,19 @@ __host__ __device__ inline Segment seg_at(const ScanLevel& lv, int c, int G, int
   return sg;
 }
 
+// Operand scale of a range with scan threshold T: rows are divided by T so every column's
+// test is |X~/T| > 1.  Thresholds below 1e-3 (no usable bar, exhaustive mode) and shadow or
+// padding ranges get scale 0; the former are flagged to the epilogue (all columns pass).
+// (1 + 1e-6) / T >= 1/T even after rounding, so |X~ * scale| <= 1 implies |X~| <= T.
+__device__ __forceinline__ float range_scale(float T) { return T > 1e-3f && T < 1e29f ? (1.0f + 1e-6f) / T : 0.f; }
+__device__ __forceinline__ bool range_allpass(float T) { return !(T > 1e-3f); }
+
 // Range operand of m-tile `mt` into `sR` (threads [tid, tid + nthreads)): row
-// rl * 8 + s holds the centred range rl permuted by isometry s's inverse,
-// R[row][j] = b[i] - Sb/N with perm_s(i) = j, so sum_j u_j R[row][j] = sum_i u[perm_s(i)] (b_i - Sb/N).
+// rl * 8 + s holds the centred range rl permuted by isometry s's inverse and scaled,
+// R[row][j] = (b[i] - Sb/N) / T_r with perm_s(i) = j, so sum_j u_j R[row][j] = X / T_r.
 __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict__ img, const Geometry& g,
-                             const RangeMeta* __restrict__ rmeta, int mt, int tid, int nthreads) {
+                             const RangeMeta* __restrict__ rmeta, const float* __restrict__ thr, int mt, int tid,
+                             int nthreads) {
   const int K = g.K, N = g.N, n = g.n;
   const int chunks = kScanRows * (K / 8);
   for (int c = tid; c < chunks; c += nthreads) {
@@ -527,13 +550,14 @@ __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict_
       int x0, y0;
       range_origin(g, r, x0, y0);
       const float mean = (float)rmeta[r].sb / (float)N;  // exact: N is a power of two
+      const float scale = range_scale(thr[r]);
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
         const int j = kc * 8 + h;
         if (j < N) {
           int ir, ic;
           symmetry_source(sinv, j / n, j % n, n, ir, ic);  // i with perm_s(i) = j
-          const float v = (float)img[(long long)(y0 + ir) * g.W + x0 + ic] - mean;
+          const float v = ((float)img[(long long)(y0 + ir) * g.W + x0 + ic] - mean) * scale;
           w[h >> 1] |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * (h & 1));
         }
       }
@@ -558,20 +582,20 @@ __global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta
   thr[r] = t;
 }
 
-// Range operands of every m-tile, built once per encode into global memory (one CTA per
-// m-tile, r_bytes each) so the scan loads them with one bulk copy per segment.
+// Range operands of every m-tile, built per level into global memory (one CTA per m-tile,
+// r_bytes each) so the scan loads them with one bulk copy per segment.
 __global__ void __launch_bounds__(256)
 range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
-                unsigned char* __restrict__ ropnd) {
-  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, blockIdx.x, threadIdx.x, 256);
+                const float* __restrict__ thr, unsigned char* __restrict__ ropnd) {
+  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, thr, blockIdx.x, threadIdx.x, 256);
 }
 
 // Warp-cooperative append: lane's entries (rowbase + bit, d) for the set bits of `mask`
 // go to the warp's staging buffer; full batches of 32 go to the CTA's list partition,
 // reserved with one shared-memory atomic (entries past the partition are counted, dropped).
-__device__ __forceinline__ void append_bits(uint32_t mask, uint32_t rowbase, uint32_t d, SurvEntry* wb, int& fill,
-                                            SurvEntry* __restrict__ list, unsigned long long* count,
-                                            unsigned long long cap) {
+__device__ __noinline__ int append_bits(uint32_t mask, uint32_t rowbase, uint32_t d, SurvEntry* wb, int fill,
+                                        SurvEntry* __restrict__ list, unsigned long long* count,
+                                        unsigned long long cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   while (true) {
@@ -598,6 +622,7 @@ __device__ __forceinline__ void append_bits(uint32_t mask, uint32_t rowbase, uin
     }
     __syncwarp();
   }
+  return fill;
 }
 
 __device__ __forceinline__ float absmax8(const uint32_t* v) {
@@ -607,37 +632,29 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
                fmaxf(fabsf(f[6]), fabsf(f[7])));
 }
 
-// Tests one 32-column TMEM chunk (4 ranges x 8 isometries) of this lane's domain against
-// the 4 ranges' thresholds and appends the columns above them.
-__device__ __forceinline__ void test_chunk(const uint32_t* v, const float* T, uint32_t rowbase, uint32_t d,
-                                           SurvEntry* wb, int& fill, SurvEntry* __restrict__ list,
-                                           unsigned long long* count, unsigned long long cap) {
-  float gm[4];
+// Appends the columns of one range group (8 isometries, scaled accumulators in v) whose
+// |value| exceeds 1, or all 8 when the range has no usable threshold.
+__device__ __forceinline__ int group_hits(const uint32_t* v, bool allpass, uint32_t rowbase, uint32_t d,
+                                          SurvEntry* wb, int fill, SurvEntry* __restrict__ list,
+                                          unsigned long long* count, unsigned long long cap) {
+  uint32_t bits = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) gm[k] = absmax8(v + 8 * k);
-  const bool hit = (gm[0] > T[0]) | (gm[1] > T[1]) | (gm[2] > T[2]) | (gm[3] > T[3]);
-  if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t bits = 0;
-      if (gm[k] > T[k]) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > T[k]) << c;
-      }
-      if (__any_sync(0xffffffffu, bits != 0)) append_bits(bits, rowbase + 8u * k, d, wb, fill, list, count, cap);
-    }
-  }
+  for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[c])) > 1.0f) << c;
+  if (allpass) bits = 0xFFu;
+  if (__any_sync(0xffffffffu, bits != 0)) fill = append_bits(bits, rowbase, d, wb, fill, list, count, cap);
+  return fill;
 }
 
-// Persistent scan over the segments of ScanLevel (see there); 18 warps:
+// Persistent scan over the segments of ScanLevel (see there); 10 warps:
 //   warp 0        lane 0: bulk-copy producer, 128-domain pool tiles (contiguous 128*K*2 bytes) ->
 //                 smem ring; lane 1: range-operand loader, the segment's 256 x K operand (built
 //                 once per encode by range_op_kernel) -> one of two smem buffers
 //   warp 1        TMEM allocation; lane 0: MMA issuer, K/16 x tcgen05.mma M=128 (domains) x
 //                 N=256 (32 ranges x 8 isometries) x K=16 per tile into one of two 256-column
 //                 TMEM accumulators
-//   warps 2-17    epilogue: 16 warps (lane quarter x column quarter); for every tile a thread
-//                 owns one domain (TMEM lane) and 8 ranges x 8 isometries
+//   warps 2-9     epilogue: 8 warps (lane quarter x column half); for every tile a thread owns
+//                 one domain (TMEM lane) and 16 ranges x 8 isometries (128 columns, scaled so
+//                 the pruning test is |X~/T_r| > 1 for every column)
 //                 (128 columns), tests each range's 8-isometry |max| against the range's
 //                 threshold and appends the rare columns above it to the survivor list
 __global__ void __launch_bounds__(kScanThreads, 1)
@@ -742,38 +759,59 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   } else {
     // ================= epilogue =================
     const int e = warp - 2;
-    const int cq = e >> 2;          // column quarter: ranges cq*8 .. cq*8+7 of the m-tile
+    const int half = e >> 2;        // column half: ranges half*16 .. half*16+15 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
     SurvEntry* wb = wbuf_all + e * kWarpBuf;
     int fill = 0;
-    const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + cq * 64;
-    float T[8];
+    const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + half * 128;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const Segment S = seg_at(lv, cta, G, sg);
-      const int r0 = S.m * kScanRanges + cq * 8;  // this thread's 8 ranges
-      const float4 t0 = __ldg(reinterpret_cast<const float4*>(thr + r0));
-      const float4 t1 = __ldg(reinterpret_cast<const float4*>(thr + r0) + 1);
-      T[0] = t0.x; T[1] = t0.y; T[2] = t0.z; T[3] = t0.w;
-      T[4] = t1.x; T[5] = t1.y; T[6] = t1.z; T[7] = t1.w;
+      const int r0 = S.m * kScanRanges + half * 16;  // this thread's 16 ranges
+      uint32_t allpass = 0;                          // ranges without a usable threshold
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(thr + r0 + k));
+        allpass |= (uint32_t)range_allpass(t.x) << k | (uint32_t)range_allpass(t.y) << (k + 1) |
+                   (uint32_t)range_allpass(t.z) << (k + 2) | (uint32_t)range_allpass(t.w) << (k + 3);
+      }
       const uint32_t rowbase = (uint32_t)r0 * 8u;
       for (int j = S.j0; j < S.j1; ++j, ++i) {
         const int buf = i & 1;
         const uint32_t d = (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
         ptx::mbar_wait(&tfull_bar[buf], (i >> 1) & 1);
         ptx::tc_fence_after();
+        if (g.flags & 128) {  // debug: no TMEM reads at all (MMA + producer throughput)
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
+          continue;
+        }
         const uint32_t ta = tcol + buf * kScanRows;
-        uint32_t va[32], vb[32];
+        uint32_t v[128];
         __syncwarp();
-        ptx::tmem_ld_32x32b_x32(ta, va);
-        ptx::tmem_ld_32x32b_x32(ta + 32, vb);
+        ptx::tmem_ld_32x32b_x32(ta, v);
+        ptx::tmem_ld_32x32b_x32(ta + 32, v + 32);
+        ptx::tmem_ld_32x32b_x32(ta + 64, v + 64);
+        ptx::tmem_ld_32x32b_x32(ta + 96, v + 96);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all 64 columns read: release the buffer
-        if (!(g.flags & 8)) {
-          test_chunk(va, T, rowbase, d, wb, fill, list, count, cap);
-          test_chunk(vb, T + 4, rowbase + 32u, d, wb, fill, list, count, cap);
+        if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all 128 columns read: release the buffer
+        if (g.flags & 8) continue;                          // debug: skip the test
+        // |max| over the 128 scaled accumulators, four independent FMNMX3 chains
+        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
+          m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[32 + c])), fabsf(__uint_as_float(v[33 + c]))));
+          m2 = fmaxf(m2, fmaxf(fabsf(__uint_as_float(v[64 + c])), fabsf(__uint_as_float(v[65 + c]))));
+          m3 = fmaxf(m3, fmaxf(fabsf(__uint_as_float(v[96 + c])), fabsf(__uint_as_float(v[97 + c]))));
+        }
+        const bool hit = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > 1.0f || allpass != 0;
+        if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            fill = group_hits(v + 8 * k, (allpass >> k) & 1u, rowbase + 8u * k, d, wb, fill, list, count, cap);
         }
       }
     }
@@ -813,30 +851,80 @@ __global__ void __launch_bounds__(256)
 eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
             const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
             const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
-            unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab) {
-  const unsigned long long total = (unsigned long long)parts * part;
+            unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab,
+            uint2* __restrict__ pend, unsigned long long* __restrict__ pend_count) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const bool screens = !(g.flags & 2);
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    if (!list_slot(i, part, counts)) continue;
-    const SurvEntry en = list[i];
-    const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)en.y;
-    double R = inf;
-    const DomainMetaI mi = meta_i[d];
-    if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
-      const RangeMeta rm = rmeta[r];
-      int x0, y0;
-      range_origin(g, r, x0, y0);
-      uint32_t qw[NN / 2], bpk[NN / 4];
-      load_q8_row<NN>(qpool, d, s, qw);
-      load_range_words<NN>(img, g, x0, y0, bpk);
-      unsigned qs, qo;
-      R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, load_bar(gbest, r), screens,
-                        false, tab, qpool, img, d, s, x0, y0, qs, qo);
-      if (R < inf) publish_best(gbest, r, R);
+  const int lane = threadIdx.x & 31;
+  const int per = gridDim.x / parts;  // blocks per partition (launch: a multiple of parts)
+  const int c = blockIdx.x / per, sub = blockIdx.x % per;
+  const unsigned long long n = min(counts[c], part);
+  const unsigned long long base = (unsigned long long)c * part;
+  // warp-uniform trip count so the pending pushes below can use warp collectives
+  for (unsigned long long j0 = (unsigned long long)sub * blockDim.x + (threadIdx.x & ~31u); j0 < n;
+       j0 += (unsigned long long)per * blockDim.x) {
+    const unsigned long long j = j0 + lane, i = base + j;
+    bool pending = false;
+    unsigned qs = 0, qo = 0;
+    if (j < n) {
+      const SurvEntry en = list[i];
+      const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)en.y;
+      double R = inf;
+      const DomainMetaI mi = meta_i[d];
+      if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
+        const RangeMeta rm = rmeta[r];
+        int x0, y0;
+        range_origin(g, r, x0, y0);
+        uint32_t qw[NN / 2], bpk[NN / 4];
+        load_q8_row<NN>(qpool, d, s, qw);
+        load_range_words<NN>(img, g, x0, y0, bpk);
+        R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, load_bar(gbest, r),
+                          screens, false, tab, qpool, img, d, s, x0, y0, qs, qo, &pending);
+        if (R < inf) publish_best(gbest, r, R);
+      }
+      res[i] = R;
     }
-    res[i] = R;
+    // candidates that passed every screen: (entry, codes) to the residual pass
+    const unsigned bal = __ballot_sync(0xffffffffu, pending);
+    if (bal) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(pend_count, (unsigned long long)__popc(bal));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (pending) pend[b + __popc(bal & ((1u << lane) - 1u))] = make_uint2((uint32_t)i, qs | (qo << 16));
+    }
+  }
+}
+
+// Exact residuals (encoder.cpp:274-280, pixel order, each operation rounded) of the
+// candidates eval_kernel left pending, with their dequantised codes from the tables.
+template <int NN>
+__global__ void __launch_bounds__(256)
+residual_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
+                const SurvEntry* __restrict__ list, const uint2* __restrict__ pend,
+                const unsigned long long* __restrict__ pend_count, double* __restrict__ res,
+                unsigned long long* __restrict__ gbest, DeqTables tab) {
+  const unsigned long long n = *pend_count;
+  for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint2 p = pend[k];
+    const SurvEntry en = list[p.x];
+    const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)en.y;
+    int x0, y0;
+    range_origin(g, r, x0, y0);
+    uint32_t qw[NN / 2], bpk[NN / 4];
+    load_q8_row<NN>(qpool, d, s, qw);
+    load_range_words<NN>(img, g, x0, y0, bpk);
+    const double s_deq = tab.s[p.y & 0xFFFFu], o_deq = tab.o[p.y >> 16];
+    double r_val = 0.0;
+#pragma unroll
+    for (int i = 0; i < NN; ++i) {
+      const double ai = __dmul_rn((double)q_at(qw, i), 0.25);
+      const double bi = (double)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+      const double dd = __dsub_rn(__dadd_rn(__dmul_rn(s_deq, ai), o_deq), bi);
+      r_val = __dadd_rn(r_val, __dmul_rn(dd, dd));
+    }
+    publish_best(gbest, r, r_val);
+    res[p.x] = r_val;
   }
 }
 
@@ -845,10 +933,12 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
 __global__ void winner_kernel(const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts,
                               int parts, unsigned long long part, const double* __restrict__ res,
                               const unsigned long long* __restrict__ gbest, unsigned* __restrict__ win) {
-  const unsigned long long total = (unsigned long long)parts * part;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    if (!list_slot(i, part, counts)) continue;
+  const int per = gridDim.x / parts;
+  const int c = blockIdx.x / per, sub = blockIdx.x % per;
+  const unsigned long long n = min(counts[c], part);
+  for (unsigned long long j = (unsigned long long)sub * blockDim.x + threadIdx.x; j < n;
+       j += (unsigned long long)per * blockDim.x) {
+    const unsigned long long i = (unsigned long long)c * part + j;
     const SurvEntry en = list[i];
     const int r = (int)(en.x >> 3);
     const double R = res[i];
@@ -1011,28 +1101,36 @@ size_t range_op_bytes(const Geometry& g) {
   return (size_t)((g.R + kScanRanges - 1) / kScanRanges) * kScanRows * g.K * 2;
 }
 
-void launch_range_op(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta, unsigned char* ropnd,
-                     cudaStream_t st) {
-  range_op_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(img, g, rmeta, ropnd);
+void launch_range_op(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta, const float* thr,
+                     unsigned char* ropnd, cudaStream_t st) {
+  range_op_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(img, g, rmeta, thr, ropnd);
 }
 
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
                  const RangeMeta* rmeta, const SurvEntry* list, const unsigned long long* counts, int parts,
-                 unsigned long long part, double* res, unsigned long long* gbest, const double* deq, int sms,
-                 cudaStream_t st) {
-  const int blocks = sms * 8;
+                 unsigned long long part, double* res, unsigned long long* gbest, const double* deq, uint2* pend,
+                 unsigned long long* pend_count, int sms, cudaStream_t st) {
+  const int blocks = parts * 8;
   const DeqTables tab{deq, deq + (1 << g.s_bits)};
-  if (g.N == 4)
-    eval_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab);
-  else if (g.N == 16)
-    eval_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab);
-  else
-    eval_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab);
+  cudaMemsetAsync(pend_count, 0, sizeof(unsigned long long), st);
+  if (g.N == 4) {
+    eval_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
+                                           pend, pend_count);
+    residual_kernel<4><<<sms * 4, 256, 0, st>>>(img, g, qpool, list, pend, pend_count, res, gbest, tab);
+  } else if (g.N == 16) {
+    eval_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
+                                            pend, pend_count);
+    residual_kernel<16><<<sms * 4, 256, 0, st>>>(img, g, qpool, list, pend, pend_count, res, gbest, tab);
+  } else {
+    eval_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
+                                            pend, pend_count);
+    residual_kernel<64><<<sms * 4, 256, 0, st>>>(img, g, qpool, list, pend, pend_count, res, gbest, tab);
+  }
 }
 
 void launch_winner(const SurvEntry* list, const unsigned long long* counts, int parts, unsigned long long part,
                    const double* res, const unsigned long long* gbest, unsigned* win, int sms, cudaStream_t st) {
-  winner_kernel<<<sms * 4, 256, 0, st>>>(list, counts, parts, part, res, gbest, win);
+  winner_kernel<<<parts * 4, 256, 0, st>>>(list, counts, parts, part, res, gbest, win);
 }
 
 void launch_record(const unsigned char* img, const Geometry& g, const unsigned short* qpool,

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:eval_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/eval4_cfg2 -f python tools/encode_once.py cfg2 > gpurun_out/ncu_a.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:seed_v3 --launch-count 1 -o gpurun_out/seed4_cfg2 -f python tools/encode_once.py cfg2 > gpurun_out/ncu_b.log 2>&1
+echo done
