@@ -157,8 +157,14 @@ uint64_t fic_kernel_launch_count(void);
 /* Average device time (ms, CUDA events on the launching stream) of the matcher kernel
  * over the calls since the last reset, and the number of timed launches. */
 int32_t fic_matcher_timing(double* avg_ms, uint64_t* launches, int32_t reset);
-/* Enable/disable per-launch matcher timing (adds two events per encode). */
+/* Enable/disable per-launch matcher timing (adds four events per encode). */
 void fic_set_matcher_timing(int32_t enabled);
+/* Average device time (ms) of the full-level tcgen05 scan kernel alone (the dominant kernel:
+ * every range x domain x isometry correlation of the encode) and the number of timed launches. */
+int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset);
+/* Survivors (candidates passing the tensor-core bound) per scan level of the calling
+ * process's last tcgen05-path encode; returns the number of levels (0 for the CUDA-core path). */
+int32_t fic_last_survivors(uint64_t* counts, int32_t max_levels);
 
 #ifdef __cplusplus
 }

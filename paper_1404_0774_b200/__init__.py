@@ -20,9 +20,11 @@ from .codec import (
     encode_rows,
     encode_with_stats,
     kernel_launch_count,
+    last_survivors,
     matcher_timing,
     psnr,
     rmse,
+    scan_timing,
     set_device,
     set_matcher_timing,
     validate_geometry,
@@ -51,7 +53,9 @@ __all__ = [
     "encode_rows",
     "encode_with_stats",
     "kernel_launch_count",
+    "last_survivors",
     "matcher_timing",
+    "scan_timing",
     "set_device",
     "set_matcher_timing",
 ]

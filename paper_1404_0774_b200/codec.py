@@ -302,3 +302,18 @@ def matcher_timing(reset=False):
 
 def set_matcher_timing(enabled):
     lib().fic_set_matcher_timing(int(bool(enabled)))
+
+
+def scan_timing(reset=False):
+    """(extension) (average ms of the full-level tcgen05 scan kernel, timed launches)."""
+    ms = ctypes.c_double()
+    n = ctypes.c_uint64()
+    lib().fic_scan_timing(ctypes.byref(ms), ctypes.byref(n), int(reset))
+    return ms.value, n.value
+
+
+def last_survivors():
+    """(extension) survivors per scan level of this process's last tcgen05-path encode."""
+    buf = (ctypes.c_uint64 * 8)()
+    n = lib().fic_last_survivors(buf, 8)
+    return [int(buf[i]) for i in range(min(n, 8))]

@@ -88,6 +88,10 @@ std::atomic<int> g_timing{0};
 std::mutex g_timing_mu;
 double g_timing_ms = 0.0;
 unsigned long long g_timing_n = 0;
+double g_scan_ms = 0.0;            // the full-level scan kernel alone
+unsigned long long g_scan_n = 0;
+std::mutex g_surv_mu;
+std::vector<unsigned long long> g_last_surv;  // survivors per level of the last encode (tcgen05 path)
 
 int32_t fail(int32_t code, const std::string& detail) {
   g_err = detail;
@@ -204,7 +208,8 @@ struct Workspace {
   int device = -1;
   int sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  bool scan_timed = false;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
       diag, scratch, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
@@ -227,6 +232,8 @@ Workspace& workspace() {
     CK(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&w->ev0));
     CK(cudaEventCreate(&w->ev1));
+    CK(cudaEventCreate(&w->ev2));
+    CK(cudaEventCreate(&w->ev3));
     g_ws[dev] = w;
   }
   return *g_ws[dev];
@@ -320,7 +327,13 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
   launch_threshold(g, b.rm, b.gbest, b.thr, st);
   launch_range_op(d_img, g, b.rm, b.thr, b.ropnd, st);
+  const bool time_scan = stride == 1 && g_timing.load() != 0;
+  if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, st));
+  if (time_scan) {
+    CK(cudaEventRecord(ws.ev3, st));
+    ws.scan_timed = true;
+  }
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
               b.cnt + kPendSlot, ws.sms, st);
   g_launches += 5;
@@ -440,6 +453,15 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fi
       }
       std::fprintf(stderr, " part %llu selfcheck %llu\n", ws.list_cap / fparts, hc[kSelfcheckSlot]);
     }
+    {
+      std::vector<unsigned long long> surv(nl, 0);
+      for (size_t l = 0; l < nl; ++l) {
+        const int parts = scan_grid(g, lv[l], ws.sms);
+        for (int c = 0; c < parts; ++c) surv[l] += hc[l * kPartSlots + c];
+      }
+      std::lock_guard<std::mutex> lock(g_surv_mu);
+      g_last_surv = surv;
+    }
     if (need <= ws.list_cap / (unsigned long long)fparts) {
       if (hc[kSelfcheckSlot] != 0) throw InternalFail{"scan self-check: a winner's residual differs from its bar"};
       return;
@@ -460,6 +482,12 @@ void collect_timing(Workspace& ws) {
     g_timing_ms += ms;
     g_timing_n += 1;
   }
+  if (ws.scan_timed && cudaEventElapsedTime(&ms, ws.ev2, ws.ev3) == cudaSuccess) {
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    g_scan_ms += ms;
+    g_scan_n += 1;
+  }
+  ws.scan_timed = false;
 }
 
 void fill_stats(fic_stats* stats, const Geometry& g, unsigned long long flat, unsigned long long shadow) {
@@ -830,5 +858,24 @@ int32_t fic_matcher_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
 }
 
 void fic_set_matcher_timing(int32_t enabled) { g_timing.store(enabled ? 1 : 0); }
+
+int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
+  std::lock_guard<std::mutex> lock(g_timing_mu);
+  if (avg_ms) *avg_ms = g_scan_n ? g_scan_ms / (double)g_scan_n : 0.0;
+  if (launches) *launches = g_scan_n;
+  if (reset) {
+    g_scan_ms = 0.0;
+    g_scan_n = 0;
+  }
+  return FIC_OK;
+}
+
+int32_t fic_last_survivors(uint64_t* counts, int32_t max_levels) {
+  std::lock_guard<std::mutex> lock(g_surv_mu);
+  const int32_t n = (int32_t)g_last_surv.size();
+  for (int32_t l = 0; l < n && l < max_levels; ++l)
+    if (counts) counts[l] = g_last_surv[l];
+  return n;
+}
 
 }  // extern "C"

@@ -426,7 +426,7 @@ __device__ __forceinline__ double load_bar(const unsigned long long* gbest, int 
 // Exact evaluation of the 8 isometries of the (2h+1)^2 grid domains around each range's own
 // 2x-scaled neighbourhood (self-similar candidates that usually fit well) to give the
 // first scan level a bar.  One thread per (range, local domain, isometry).
-constexpr int kSeedHalf = 1;
+constexpr int kSeedHalf = 2;
 constexpr int kSeedSide = 2 * kSeedHalf + 1;
 constexpr int kSeedPerRange = kSeedSide * kSeedSide * kSyms;
 
@@ -632,19 +632,6 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
                fmaxf(fabsf(f[6]), fabsf(f[7])));
 }
 
-// Appends the columns of one range group (8 isometries, scaled accumulators in v) whose
-// |value| exceeds 1, or all 8 when the range has no usable threshold.
-__device__ __forceinline__ int group_hits(const uint32_t* v, bool allpass, uint32_t rowbase, uint32_t d,
-                                          SurvEntry* wb, int fill, SurvEntry* __restrict__ list,
-                                          unsigned long long* count, unsigned long long cap) {
-  uint32_t bits = 0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[c])) > 1.0f) << c;
-  if (allpass) bits = 0xFFu;
-  if (__any_sync(0xffffffffu, bits != 0)) fill = append_bits(bits, rowbase, d, wb, fill, list, count, cap);
-  return fill;
-}
-
 // Persistent scan over the segments of ScanLevel (see there); 10 warps:
 //   warp 0        lane 0: bulk-copy producer, 128-domain pool tiles (contiguous 128*K*2 bytes) ->
 //                 smem ring; lane 1: range-operand loader, the segment's 256 x K operand (built
@@ -798,20 +785,36 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all 128 columns read: release the buffer
         if (g.flags & 8) continue;                          // debug: skip the test
-        // |max| over the 128 scaled accumulators, four independent FMNMX3 chains
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+        // |max| of each range's 8 isometry columns (4 FMNMX3 each); mask of ranges above 1
+        uint32_t gmask = allpass;
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
-          m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[32 + c])), fabsf(__uint_as_float(v[33 + c]))));
-          m2 = fmaxf(m2, fmaxf(fabsf(__uint_as_float(v[64 + c])), fabsf(__uint_as_float(v[65 + c]))));
-          m3 = fmaxf(m3, fmaxf(fabsf(__uint_as_float(v[96 + c])), fabsf(__uint_as_float(v[97 + c]))));
+        for (int k = 0; k < 16; ++k) {
+          const float* f = reinterpret_cast<const float*>(v + 8 * k);
+          const float gm = fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
+                                       fmaxf(fabsf(f[4]), fabsf(f[5]))),
+                                 fmaxf(fabsf(f[6]), fabsf(f[7])));
+          gmask |= (uint32_t)(gm > 1.0f) << k;
         }
-        const bool hit = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > 1.0f || allpass != 0;
-        if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k)
-            fill = group_hits(v + 8 * k, (allpass >> k) & 1u, rowbase + 8u * k, d, wb, fill, list, count, cap);
+        uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+        while (groups) {  // ranges with a hit in some lane of the warp
+          const int k = __ffs(groups) - 1;
+          groups &= groups - 1;
+          uint32_t bits = 0;
+          switch (k) {  // static register indices per case
+#define FIC_GROUP_BITS(K)                                                                       \
+  case K:                                                                                       \
+    _Pragma("unroll") for (int c = 0; c < 8; ++c) bits |=                                       \
+        (uint32_t)(fabsf(__uint_as_float(v[8 * K + c])) > 1.0f) << c;                           \
+    break;
+            FIC_GROUP_BITS(0) FIC_GROUP_BITS(1) FIC_GROUP_BITS(2) FIC_GROUP_BITS(3)
+            FIC_GROUP_BITS(4) FIC_GROUP_BITS(5) FIC_GROUP_BITS(6) FIC_GROUP_BITS(7)
+            FIC_GROUP_BITS(8) FIC_GROUP_BITS(9) FIC_GROUP_BITS(10) FIC_GROUP_BITS(11)
+            FIC_GROUP_BITS(12) FIC_GROUP_BITS(13) FIC_GROUP_BITS(14) FIC_GROUP_BITS(15)
+#undef FIC_GROUP_BITS
+            default: break;
+          }
+          if ((allpass >> k) & 1u) bits = 0xFFu;
+          fill = append_bits(bits, rowbase + 8u * (uint32_t)k, d, wb, fill, list, count, cap);
         }
       }
     }

@@ -100,7 +100,7 @@ def run(cfg, sample=None, tile=128, lag=1, prepass=0, seed9=True, chunks=1):
           f"{per.mean():.1f} p50 {np.median(per):.0f} p99 {np.quantile(per, .99):.0f} max {per.max():.0f}")
 
 
-def static_levels(cfg, sample=None, tile=128, schemes=((64, 8), (32,), (256, 16), (128, 8), (16,))):
+def static_levels(cfg, sample=None, tile=128, schemes=((64, 8), (32,), (256, 16), (128, 8), (16,)), seed_h=1):
     """Static multi-level scheme: seed (9 local domains) -> level strides (sparse tile subsets,
     each scanned against the bar of the previous levels, all survivors evaluated) -> full scan."""
     gen, n, step = images.CONFIGS[cfg]
@@ -150,8 +150,8 @@ def static_levels(cfg, sample=None, tile=128, schemes=((64, 8), (32,), (256, 16)
         seed = np.full(len(b), np.inf)
         xi0 = np.clip((xs[i0:i0 + ch] - n // 2) // step, 0, None)
         yi0 = np.clip((ys[i0:i0 + ch] - n // 2) // step, 0, None)
-        for dx in (-1, 0, 1):
-            for dy in (-1, 0, 1):
+        for dx in range(-seed_h, seed_h + 1):
+            for dy in range(-seed_h, seed_h + 1):
                 xi, yi = xi0 + dx, yi0 + dy
                 okk = (xi >= 0) & (yi >= 0) & (xi < PY) & (yi < PY)
                 d = np.where(okk, xi * PY + yi, 0)
