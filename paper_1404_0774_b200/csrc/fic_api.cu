@@ -58,6 +58,7 @@ cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const _
                         const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long,
                         cudaStream_t);
 int scan_padded_ranges(const Geometry&);
+bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
 size_t range_op_bytes(const Geometry&);
 void launch_range_op(const unsigned char*, const Geometry&, const RangeMeta*, const float*, unsigned char*,
@@ -320,13 +321,14 @@ ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
 // their exact evaluation.  cnt: the level's kPartSlots counters.
 void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, int stride,
                    unsigned long long* cnt, cudaStream_t st) {
+  const int first_stride = scan_levels(g).front();  // pair mode builds the (unscaled) range operands once
   auto* list = static_cast<uint2*>(ws.list.get((size_t)ws.list_cap * sizeof(uint2)));
   auto* res = static_cast<double*>(ws.res.get((size_t)ws.list_cap * sizeof(double)));
   auto* pend = static_cast<uint2*>(ws.pend.get((size_t)ws.list_cap * sizeof(uint2)));
   const int parts = scan_grid(g, stride, ws.sms);
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
   launch_threshold(g, b.rm, b.gbest, b.thr, st);
-  launch_range_op(d_img, g, b.rm, b.thr, b.ropnd, st);
+  if (!scan_pair_mode() || stride == first_stride) launch_range_op(d_img, g, b.rm, b.thr, b.ropnd, st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, st));
@@ -360,7 +362,7 @@ void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g,
 // tcgen05 path: K1 normalised pool, range pass, seed, sparse levels, final level.
 void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b,
                          fic_mapping* d_out, unsigned long long* d_counters, cudaStream_t st) {
-  if (ws.list_cap == 0) ws.list_cap = std::max<unsigned long long>(1ull << 20, (unsigned long long)g.R * 8 * 64);
+  if (ws.list_cap == 0) ws.list_cap = std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128);
   CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(b.cnt, 0, kScanCountSlots * sizeof(unsigned long long), st));
   launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);

@@ -28,9 +28,12 @@
 //    is in the full level's list; winner_kernel takes the smallest (domain, isometry)
 //    among them and record_kernel re-evaluates it into the RangeMapping record.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "tc2_ptx.cuh"
 
 namespace ficb {
 
@@ -474,12 +477,12 @@ __host__ __device__ inline ScanSmem scan_smem_layout(int K) {
   L.p_bytes = kScanTileDom * K * 2;
   L.r_off = 0;
   L.p_off = 2 * L.r_bytes;
-  const uint32_t fixed = L.p_off + 512 + kScanEpiWarps * kWarpBuf * (uint32_t)sizeof(SurvEntry);
+  const uint32_t fixed = L.p_off + 512;
   uint32_t st = (kSmemBudget - fixed) / L.p_bytes;
   L.stages = st > kScanMaxStages ? kScanMaxStages : st;
   L.bar_off = L.p_off + L.stages * L.p_bytes;
   L.wbuf_off = L.bar_off + 512;
-  L.total = L.wbuf_off + kScanEpiWarps * kWarpBuf * (uint32_t)sizeof(SurvEntry);
+  L.total = L.wbuf_off;
   return L;
 }
 
@@ -590,40 +593,78 @@ range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMe
   build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, thr, blockIdx.x, threadIdx.x, 256);
 }
 
-// Warp-cooperative append: lane's entries (rowbase + bit, d) for the set bits of `mask`
-// go to the warp's staging buffer; full batches of 32 go to the CTA's list partition,
-// reserved with one shared-memory atomic (entries past the partition are counted, dropped).
-__device__ __noinline__ int append_bits(uint32_t mask, uint32_t rowbase, uint32_t d, SurvEntry* wb, int fill,
-                                        SurvEntry* __restrict__ list, unsigned long long* count,
-                                        unsigned long long cap) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
-  while (true) {
-    const bool has = mask != 0;
-    const uint32_t bal = __ballot_sync(0xffffffffu, has);
-    if (!bal) break;
-    if (has) {
-      const int b = __ffs(mask) - 1;
-      mask &= mask - 1;
-      wb[fill + __popc(bal & lt)] = make_uint2(rowbase + (uint32_t)b, d);
-    }
-    fill += __popc(bal);
-    if (fill >= 32) {
-      __syncwarp();
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(count, 32ull);  // shared-memory counter
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base + lane < cap) list[base + lane] = wb[lane];
-      SurvEntry tail = make_uint2(0, 0);
-      if (lane < fill - 32) tail = wb[32 + lane];
-      __syncwarp();
-      if (lane < fill - 32) wb[lane] = tail;
-      fill -= 32;
-    }
-    __syncwarp();
+// Survivor appender of one warp: entries go straight to the CTA's list partition, into
+// 64-entry chunks the warp reserves with one 32-bit shared-memory atomic.  Slots a warp
+// leaves unused at a chunk switch or at exit hold kSentinel (skipped by the consumers);
+// entries past the partition size are dropped (the reserved count still reports them).
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+constexpr uint32_t kChunk = 64;
+
+struct WarpAppender {
+  SurvEntry* list;
+  unsigned* count;   // CTA's reserved slots (shared memory)
+  uint32_t cap;      // partition size
+  uint32_t base;     // next slot of the warp's chunk
+  uint32_t left;     // slots left in it
+
+  __device__ __forceinline__ void put(SurvEntry e, uint32_t pos) {
+    if (pos < cap) list[pos] = e;
   }
-  return fill;
-}
+  // Pad the current chunk with sentinels (lanes of the warp cooperatively).
+  __device__ __forceinline__ void close() {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t k = lane; k < left; k += 32) put(make_uint2(kSentinel, kSentinel), base + k);
+    left = 0;
+  }
+  // Appends (rowbase + b, d) for every set bit b of this lane's mask.
+  __device__ __forceinline__ void bits(uint32_t mask, uint32_t rowbase, uint32_t d) {
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    while (true) {
+      const bool has = mask != 0;
+      const uint32_t bal = __ballot_sync(0xffffffffu, has);
+      if (!bal) break;
+      const uint32_t n = __popc(bal);
+      if (n > left) {
+        close();
+        uint32_t nb = 0;
+        if (lane == 0) nb = atomicAdd(count, kChunk);
+        base = __shfl_sync(0xffffffffu, nb, 0);
+        left = kChunk;
+      }
+      if (has) {
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        put(make_uint2(rowbase + (uint32_t)b, d), base + __popc(bal & lt));
+      }
+      base += n;
+      left -= n;
+    }
+  }
+  // Appends (rowid, d0 + b) for every set bit b of this lane's column mask.
+  __device__ __forceinline__ void cols(uint32_t mask, uint32_t rowid, uint32_t d0) {
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    while (true) {
+      const bool has = mask != 0;
+      const uint32_t bal = __ballot_sync(0xffffffffu, has);
+      if (!bal) break;
+      const uint32_t n = __popc(bal);
+      if (n > left) {
+        close();
+        uint32_t nb = 0;
+        if (lane == 0) nb = atomicAdd(count, kChunk);
+        base = __shfl_sync(0xffffffffu, nb, 0);
+        left = kChunk;
+      }
+      if (has) {
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        put(make_uint2(rowid, d0 + (uint32_t)b), base + __popc(bal & lt));
+      }
+      base += n;
+      left -= n;
+    }
+  }
+};
 
 __device__ __forceinline__ float absmax8(const uint32_t* v) {
   const float* f = reinterpret_cast<const float*>(v);
@@ -661,8 +702,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   uint64_t* rfull_bar = tempty_bar + 2;
   uint64_t* rempty_bar = rfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(rempty_bar + 2);
-  unsigned long long* count = reinterpret_cast<unsigned long long*>(smem + L.bar_off + 448);  // CTA survivors
-  SurvEntry* wbuf_all = reinterpret_cast<SurvEntry*>(smem + L.wbuf_off);
+  unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 448);  // CTA's reserved survivor slots
   SurvEntry* list = list_all + (unsigned long long)blockIdx.x * cap;  // this CTA's partition of `cap` entries
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -748,8 +788,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     const int e = warp - 2;
     const int half = e >> 2;        // column half: ranges half*16 .. half*16+15 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
-    SurvEntry* wb = wbuf_all + e * kWarpBuf;
-    int fill = 0;
+    WarpAppender app{list, count, (uint32_t)cap, 0u, 0u};
     const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + half * 128;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
@@ -814,18 +853,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             default: break;
           }
           if ((allpass >> k) & 1u) bits = 0xFFu;
-          fill = append_bits(bits, rowbase + 8u * (uint32_t)k, d, wb, fill, list, count, cap);
+          app.bits(bits, rowbase + 8u * (uint32_t)k, d);
         }
       }
     }
-    // flush the staging buffer
-    __syncwarp();
-    if (fill > 0) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(count, (unsigned long long)fill);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (lane < fill && base + lane < cap) list[base + lane] = wb[lane];
-    }
+    app.close();
   }
 
   ptx::tc_fence_before();
@@ -871,9 +903,9 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
     unsigned qs = 0, qo = 0;
     if (j < n) {
       const SurvEntry en = list[i];
-      const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)en.y;
+      const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)(en.y & 0x7FFFFFFFu);
       double R = inf;
-      const DomainMetaI mi = meta_i[d];
+      const DomainMetaI mi = en.x == kSentinel ? DomainMetaI{0, -1} : meta_i[d];
       if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
         const RangeMeta rm = rmeta[r];
         int x0, y0;
@@ -943,6 +975,7 @@ __global__ void winner_kernel(const SurvEntry* __restrict__ list, const unsigned
        j += (unsigned long long)per * blockDim.x) {
     const unsigned long long i = (unsigned long long)c * part + j;
     const SurvEntry en = list[i];
+    if (en.x == kSentinel) continue;
     const int r = (int)(en.x >> 3);
     const double R = res[i];
     if (R < __longlong_as_double(0x7ff0000000000000ll) && (unsigned long long)__double_as_longlong(R) == gbest[r])
@@ -1011,13 +1044,309 @@ __global__ void fill_u64_kernel(unsigned long long* p, long long n, unsigned lon
     p[i] = v;
 }
 
+// ================================================================== CTA-pair scan
+// The same contraction with the roles the hardware favours for this shape: the ranges are
+// the resident operand A, kept in TMEM (no shared-memory reads per MMA), the pool tiles the
+// streamed operand B, split across the two CTAs of a cluster (each SM streams and holds 112
+// of the 224 domains of a tile).  tcgen05.mma.cta_group::2 M=256 (each CTA's 128 (range,
+// isometry) rows) x N=224 x K=16, accumulators in two 224-column TMEM buffers per CTA.
+// Per SM and tile: 14 KB of pool streamed and read once by the tensor core, 28672 results,
+// 448 cycles of MMA at K=64.  Each epilogue thread owns one (range, isometry) row, so its
+// threshold is a register and the test is |x| > T over 112 columns.
+constexpr int kP2Dom = 224;                     // domains per pair tile (MMA N)
+constexpr int kP2Half = kP2Dom / 2;             // domains per CTA
+constexpr int kP2Bufs = 2;                      // TMEM accumulator buffers
+constexpr int kP2Epi = 8;                       // epilogue warps per CTA
+constexpr int kP2Threads = (2 + kP2Epi) * 32;
+constexpr uint32_t kP2AccCols = kP2Dom;         // per TMEM accumulator buffer
+constexpr uint32_t kP2ACol = kP2Bufs * kP2AccCols;  // A (ranges) buffers start here: 2 x K/2 columns
+
+struct Scan2Smem {
+  uint32_t p_bytes, stages, p_off, bar_off, wbuf_off, total;
+};
+
+__host__ __device__ inline Scan2Smem scan2_smem_layout(int K) {
+  Scan2Smem L;
+  L.p_bytes = kP2Half * K * 2;
+  L.p_off = 0;
+  const uint32_t fixed = 1024;
+  uint32_t st = (kSmemBudget - fixed) / L.p_bytes;
+  L.stages = st > kScanMaxStages ? kScanMaxStages : st;
+  L.bar_off = L.p_off + L.stages * L.p_bytes;
+  L.wbuf_off = L.bar_off + 1024;
+  L.total = L.wbuf_off;
+  return L;
+}
+
+// Plain row-major range operand of every m-tile (256 rows x K fp16, unscaled): row
+// rl * 8 + s holds the centred range rl permuted by isometry s's inverse (as build_ranges).
+__global__ void __launch_bounds__(256)
+range_op2_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
+                 unsigned short* __restrict__ ropnd) {
+  const int K = g.K, N = g.N, n = g.n;
+  const int mt = blockIdx.x;
+  for (int c = threadIdx.x; c < kScanRows * K; c += blockDim.x) {
+    const int row = c / K, j = c % K;
+    const int rl = row >> 3, s = row & 7;
+    const int r = mt * kScanRanges + rl;
+    const int sinv = s == 1 ? 3 : (s == 3 ? 1 : s);
+    unsigned short h = 0;
+    if (r < g.R && j < N) {
+      int x0, y0;
+      range_origin(g, r, x0, y0);
+      const float mean = (float)rmeta[r].sb / (float)N;
+      int ir, ic;
+      symmetry_source(sinv, j / n, j % n, n, ir, ic);  // i with perm_s(i) = j
+      h = __half_as_ushort(__float2half_rn((float)img[(long long)(y0 + ir) * g.W + x0 + ic] - mean));
+    }
+    ropnd[((long long)mt * kScanRows + row) * K + j] = h;
+  }
+}
+
+// 112-column |max| test of one epilogue thread's row against its threshold, appending the
+// columns above it (entries (rowid, d0 + column)).
+template <int W>
+__device__ __forceinline__ uint32_t mask_above(const uint32_t* v, float T) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int c = 0; c < W; ++c) m |= (uint32_t)(fabsf(__uint_as_float(v[c])) > T) << c;
+  return m;
+}
+
+// Cluster of 2 CTAs per pair; 10 warps per CTA:
+//   warp 0        lane 0: producer of this CTA's half (112 domains) of every pool tile
+//   warp 1        TMEM allocation (cta_group::2); lane 0: MMA issuer in the even CTA, relay of
+//                 the odd CTA's "tile landed" to the even CTA's barrier in the odd one
+//   warps 2-9     epilogue: lane quarter x column half (112 columns); the four warps of column
+//                 half 0 also write the segment's range rows into TMEM (A)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
+scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const unsigned short* __restrict__ ropnd,
+             const float* __restrict__ thr, SurvEntry* __restrict__ list_all,
+             unsigned long long* __restrict__ counts, unsigned long long cap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const Scan2Smem L = scan2_smem_layout(g.K);
+  const int K = g.K;
+  unsigned char* sP = smem + L.p_off;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* empty_bar = full_bar + kScanMaxStages;
+  uint64_t* pfull_bar = empty_bar + kScanMaxStages;   // even CTA: the odd CTA's half has landed
+  uint64_t* tfull_bar = pfull_bar + kScanMaxStages;
+  uint64_t* tempty_bar = tfull_bar + kP2Bufs;
+  uint64_t* afull_bar = tempty_bar + kP2Bufs;
+  uint64_t* aempty_bar = afull_bar + 2;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(aempty_bar + 2);
+  unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 960);
+  SurvEntry* list = list_all + (unsigned long long)blockIdx.x * cap;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int G = gridDim.x >> 1, pair = blockIdx.x >> 1;
+  const int nseg = seg_count(lv, pair, G);
+  const int stages = (int)L.stages;
+  const uint32_t a_cols = (uint32_t)K / 2;  // TMEM columns of one A buffer
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+      ptx::mbar_init(&pfull_bar[s], 1);
+    }
+    for (int b = 0; b < kP2Bufs; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 2 * kP2Epi);  // every epilogue warp of both CTAs
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&afull_bar[b], 8);            // the 4 A-writer warps of both CTAs
+      ptx::mbar_init(&aempty_bar[b], 1);
+    }
+    ptx::fence_mbar_init();
+    *count = 0;
+  }
+  if (warp == 1) ptx::tmem_alloc_2sm<512>(tmem_base_smem);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tb = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ================= producer: this CTA's half of every tile =================
+    if (lane == 0) {
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) + (size_t)rank * L.p_bytes;
+      int i = 0;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const Segment S = seg_at(lv, pair, G, sg);
+        for (int j = S.j0; j < S.j1; ++j, ++i) {
+          const int s = i % stages;
+          ptx::mbar_wait(&empty_bar[s], ((i / stages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&full_bar[s], L.p_bytes);
+          ptx::bulk_g2s(sP + s * L.p_bytes, src + (size_t)j * lv.stride * 2 * L.p_bytes, L.p_bytes, &full_bar[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ================= MMA issuer (even CTA) =================
+      const uint32_t idesc = ptx::idesc_f16_f32(256, kP2Dom);
+      int i = 0;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const Segment S = seg_at(lv, pair, G, sg);
+        ptx::mbar_wait_cluster(&afull_bar[sg & 1], (sg >> 1) & 1);
+        const uint32_t a_base = tb + kP2ACol + (uint32_t)(sg & 1) * a_cols;
+        for (int j = S.j0; j < S.j1; ++j, ++i) {
+          const int s = i % stages;
+          const int buf = i % kP2Bufs;
+          ptx::mbar_wait_cluster(&tempty_bar[buf], ((i / kP2Bufs) & 1) ^ 1);
+          ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
+          ptx::mbar_wait_cluster(&pfull_bar[s], (i / stages) & 1);
+          ptx::tc_fence_after();
+          const uint32_t b_base = ptx::smem_addr(sP + s * L.p_bytes);
+          if (!(g.flags & 16)) {
+#pragma unroll 1
+            for (int kk = 0; kk < K / 16; ++kk) {
+              const uint64_t bd = ptx::smem_desc(b_base + kk * 256, 128, K * 16);
+              ptx::mma_f16_ts_2sm(tb + buf * kP2AccCols, a_base + kk * 8, bd, idesc, kk > 0 ? 1u : 0u);
+            }
+          }
+          ptx::tc_commit_2sm_mc(&empty_bar[s], 0x3);
+          ptx::tc_commit_2sm_mc(&tfull_bar[buf], 0x3);
+        }
+        ptx::tc_commit_2sm_mc(&aempty_bar[sg & 1], 0x3);
+      }
+    } else if (lane == 0) {
+      // ================= relay (odd CTA): my half landed -> even CTA's pfull =================
+      const uint32_t remote = ptx::leader_addr(ptx::smem_addr(pfull_bar));
+      int i = 0;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const Segment S = seg_at(lv, pair, G, sg);
+        for (int j = S.j0; j < S.j1; ++j, ++i) {
+          const int s = i % stages;
+          ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
+          ptx::mbar_arrive_cluster(remote + s * 8);
+        }
+      }
+    }
+  } else {
+    // ================= epilogue =================
+    const int e = warp - 2;
+    const int half = e >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;                 // TMEM lane = this CTA's (range, isometry) row
+    WarpAppender app{list, count, (uint32_t)cap, 0u, 0u};
+    const uint32_t tlane = tb + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t tempty_remote = ptx::leader_addr(ptx::smem_addr(tempty_bar));
+    const uint32_t afull_remote = ptx::leader_addr(ptx::smem_addr(afull_bar));
+    // A (range rows) of segment sg into TMEM buffer sg & 1 (column-half-0 warps)
+    auto write_a = [&](int sg) {
+      const Segment S = seg_at(lv, pair, G, sg);
+      if (sg >= 2) ptx::mbar_wait(&aempty_bar[sg & 1], ((sg >> 1) - 1) & 1);
+      const uint4* src = reinterpret_cast<const uint4*>(ropnd + ((long long)S.m * kScanRows + rank * 128 + row) * K);
+      const uint32_t ta = tlane + kP2ACol + (uint32_t)(sg & 1) * a_cols;
+      if (K == 64) {
+        uint32_t v[32];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const uint4 q = __ldg(src + w);
+          v[4 * w] = q.x; v[4 * w + 1] = q.y; v[4 * w + 2] = q.z; v[4 * w + 3] = q.w;
+        }
+        ptx::tmem_st_32x32b_x32(ta, v);
+      } else {  // K == 16
+        uint32_t v[8];
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const uint4 q = __ldg(src + w);
+          v[4 * w] = q.x; v[4 * w + 1] = q.y; v[4 * w + 2] = q.z; v[4 * w + 3] = q.w;
+        }
+        ptx::tmem_st_32x32b_x8(ta, v);
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(afull_remote + (sg & 1) * 8);
+    };
+    if (half == 0 && nseg > 0) write_a(0);
+    int i = 0;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const Segment S = seg_at(lv, pair, G, sg);
+      if (half == 0 && sg + 1 < nseg) write_a(sg + 1);
+      const int r = S.m * kScanRanges + (int)rank * 16 + (row >> 3);
+      const float T = r < g.R ? __ldg(thr + r) : 1e30f;  // shadow / padding: 1e30 (never), no bar: -1 (all)
+      const uint32_t rowid = (uint32_t)r * 8u + (uint32_t)(row & 7);
+      for (int j = S.j0; j < S.j1; ++j, ++i) {
+        const int buf = i % kP2Bufs;
+        ptx::mbar_wait(&tfull_bar[buf], (i / kP2Bufs) & 1);
+        ptx::tc_fence_after();
+        const uint32_t ta = tlane + buf * kP2AccCols + half * kP2Half;
+        uint32_t v[kP2Half];
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c + 32 <= kP2Half; c += 32) ptx::tmem_ld_32x32b_x32(ta + c, v + c);
+        if constexpr (kP2Half % 32 == 16) ptx::tmem_ld_32x32b_x16(ta + kP2Half - 16, v + kP2Half - 16);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_remote + buf * 8);
+        if (g.flags & 8) continue;
+        constexpr int Q = kP2Half / 4;  // four independent FMNMX3 chains
+        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+#pragma unroll
+        for (int c = 0; c < Q; c += 2) {
+          m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
+          m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[Q + c])), fabsf(__uint_as_float(v[Q + 1 + c]))));
+          m2 = fmaxf(m2, fmaxf(fabsf(__uint_as_float(v[2 * Q + c])), fabsf(__uint_as_float(v[2 * Q + 1 + c]))));
+          m3 = fmaxf(m3, fmaxf(fabsf(__uint_as_float(v[3 * Q + c])), fabsf(__uint_as_float(v[3 * Q + 1 + c]))));
+        }
+        const bool hit = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > T;
+        if (__any_sync(0xffffffffu, hit)) {
+          const uint32_t d0 = (uint32_t)(j * lv.stride * kP2Dom + half * kP2Half);
+          constexpr int NQ = (kP2Half + 31) / 32;
+          uint32_t mk[NQ];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) mk[q] = 0;
+          if (hit) {
+#pragma unroll
+            for (int q = 0; q < kP2Half / 32; ++q) mk[q] = mask_above<32>(v + 32 * q, T);
+            if constexpr (kP2Half % 32 == 16) mk[NQ - 1] = mask_above<16>(v + kP2Half - 16, T);
+          }
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            if (__any_sync(0xffffffffu, mk[q] != 0))
+              app.cols(mk[q], rowid, d0 + 32u * q);
+        }
+      }
+    }
+    app.close();
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();
+  if (threadIdx.x == 0) counts[blockIdx.x] = *count;
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<512>(tb);
+  }
+}
+
 // ------------------------------------------------------------------ host launchers
 bool scan_supported(const Geometry& g) { return g.N == 4 || g.N == 16 || g.N == 64; }
 
-int scan_tiles(const Geometry& g) { return (g.D + kScanTileDom - 1) / kScanTileDom; }
+// Single-CTA scan (default) or the CTA-pair scan (FIC_SCAN=pair).
+bool scan_pair_mode() {
+  const char* e = std::getenv("FIC_SCAN");
+  return e && std::strcmp(e, "pair") == 0;
+}
+
+int scan_tiles(const Geometry& g) {
+  const int t = scan_pair_mode() ? kP2Dom : kScanTileDom;
+  return (g.D + t - 1) / t;
+}
 
 // Padded domain count of the pools (a multiple of the pool-builder block).
-long long scan_pool_domains(const Geometry& g) { return (long long)((g.D + kPoolBlock - 1) / kPoolBlock) * kPoolBlock; }
+long long scan_pool_domains(const Geometry& g) {
+  const long long q = 896;  // multiple of the pool-builder block (128) and the pair tile (224)
+  return (g.D + q - 1) / q * q;
+}
 
 int scan_rows_per_cta() { return kScanRanges; }
 
@@ -1050,11 +1379,11 @@ void launch_seed_v3(const unsigned char* img, const Geometry& g, const unsigned 
   else seed_v3_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
 }
 
-// Scan CTAs (= list partitions) of a level: one per SM.
+// Scan CTAs (= list partitions) of a level: one per SM (an even number in pair mode).
 int scan_grid(const Geometry& g, int stride, int sms) {
   (void)g;
   (void)stride;
-  return sms;
+  return scan_pair_mode() ? sms & ~1 : sms;
 }
 
 static ScanLevel make_level(const Geometry& g, int stride, int G) {
@@ -1084,6 +1413,15 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
                         const RangeMeta* rmeta, const unsigned char* ropnd, const float* thr, SurvEntry* list,
                         unsigned long long* counts, unsigned long long part, cudaStream_t st) {
   const int grid = scan_grid(g, stride, sms);
+  if (scan_pair_mode()) {
+    const ScanLevel lv = make_level(g, stride, grid / 2);
+    const Scan2Smem L2 = scan2_smem_layout(g.K);
+    cudaError_t e = cudaFuncSetAttribute(scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L2.total);
+    if (e != cudaSuccess) return e;
+    scan2_kernel<<<grid, kP2Threads, L2.total, st>>>(g, lv, upool, reinterpret_cast<const unsigned short*>(ropnd),
+                                                     thr, list, counts, part);
+    return cudaGetLastError();
+  }
   const ScanLevel lv = make_level(g, stride, grid);
   const ScanSmem L = scan_smem_layout(g.K);
   cudaError_t e = cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
@@ -1106,7 +1444,11 @@ size_t range_op_bytes(const Geometry& g) {
 
 void launch_range_op(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta, const float* thr,
                      unsigned char* ropnd, cudaStream_t st) {
-  range_op_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(img, g, rmeta, thr, ropnd);
+  if (scan_pair_mode())  // unscaled plain rows (the pair scan compares with per-row thresholds)
+    range_op2_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(
+        img, g, rmeta, reinterpret_cast<unsigned short*>(ropnd));
+  else
+    range_op_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(img, g, rmeta, thr, ropnd);
 }
 
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
