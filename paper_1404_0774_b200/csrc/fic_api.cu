@@ -281,9 +281,20 @@ std::vector<int> scan_levels(const Geometry& g) {
   const int tiles = scan_tiles(g);
   const char* pp = std::getenv("FIC_PREPASS");
   const bool prepass = !(pp && std::strcmp(pp, "0") == 0);
-  if (prepass)
-    for (int s = 4096; s >= 8; s /= 8)
+  // ratio 8 between levels (measured: a final ratio-4 level costs cfg4 more scan work than it
+  // saves in survivors; cfg2 is indifferent)
+  const char* sched = std::getenv("FIC_LEVELS");  // optional override, e.g. "64,8"
+  if (sched) {
+    for (const char* p = sched; *p;) {
+      const int v = std::atoi(p);
+      if (v > 1 && tiles > v) lv.push_back(v);
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+  } else if (prepass) {
+    for (int s : {4096, 512, 64, 8})
       if (tiles > s) lv.push_back(s);
+  }
   lv.push_back(1);
   return lv;
 }
@@ -468,10 +479,18 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fi
       if (hc[kSelfcheckSlot] != 0) throw InternalFail{"scan self-check: a winner's residual differs from its bar"};
       return;
     }
-    // a partition of the full level's list was truncated: grow the list and re-run that
-    // level (the bar it achieved so far only lowers the survivor count)
-    if (attempt >= 4) throw InternalFail{"survivor list keeps overflowing"};
-    ws.list_cap = (need + need / 4 + 1024) * (unsigned long long)ws.sms;
+    // a partition of the full level's list was truncated: re-run that level with a larger
+    // list.  The entries evaluated so far already lowered the bar, so every attempt has
+    // fewer survivors; the list grows toward the need within a quarter of free device memory.
+    if (attempt >= 12) throw InternalFail{"survivor list keeps overflowing"};
+    {
+      const unsigned long long want = (need + need / 4 + 1024) * (unsigned long long)fparts;
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      const unsigned long long per_entry = sizeof(uint2) * 2 + sizeof(double);  // list + pending + residual
+      const unsigned long long limit = (ws.list.cap + ws.res.cap + ws.pend.cap + free_b / 4) / per_entry;
+      ws.list_cap = std::max(ws.list_cap, std::min(want, limit));
+    }
     enqueue_final(ws, d_img, g, b, nl - 1, d_out, st);
   }
 }

@@ -57,7 +57,9 @@ typedef uint2 SurvEntry;
 // exactly; flat iff (double)den <= 16*shadow_eps (encoder.cpp:223).  Phase 2: all threads
 // write the tile's fp16 operand (UMMA K-major no-swizzle core matrices, 16-byte coalesced
 // chunks: [domain/8][k/8][domain%8][8 halves]) and the exact u16 q rows.
-__global__ void __launch_bounds__(kPoolBlock)
+constexpr int kPoolThreads = 512;
+
+__global__ void __launch_bounds__(kPoolThreads)
 pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __restrict__ upool,
                unsigned short* __restrict__ qpool, DomainMetaI* __restrict__ meta_i,
                unsigned long long* __restrict__ flat_count) {
@@ -70,14 +72,14 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   const int N = g.N, n = g.n, K = g.K;
   const long long dbase = (long long)blockIdx.x * kPoolBlock;
   if (t == 0) s_flat = 0;
-  for (int k = t; k < kSyms * N; k += kPoolBlock) {  // perm_s(i) (transforms.cpp:13-26)
+  for (int k = t; k < kSyms * N; k += kPoolThreads) {  // perm_s(i) (transforms.cpp:13-26)
     const int s = k / N, i = k % N;
     int sr, sc;
     symmetry_source(s, i / n, i % n, n, sr, sc);
     s_perm[k] = (unsigned char)(sr * n + sc);
   }
   // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step
-  for (int idx = t; idx < kPoolBlock * N; idx += kPoolBlock) {
+  for (int idx = t; idx < kPoolBlock * N; idx += kPoolThreads) {
     const int dl = idx / N, j = idx % N;
     const long long d = dbase + dl;
     int v = 0;
@@ -92,7 +94,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   }
   __syncthreads();
   // moments of domain t: Sq, Sqq, den = N*Sqq - Sq^2 (exact), flat iff (double)den <= 16*shadow_eps (encoder.cpp:223)
-  {
+  if (t < kPoolBlock) {
     const long long d = dbase + t;
     long long s = 0, ss = 0;
     for (int j = 0; j < N; ++j) {
@@ -118,7 +120,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   // core matrices, chunk c = ((dl/8) * (K/8) + k/8) * 8 + dl%8 (16-byte coalesced stores)
   uint4* out = reinterpret_cast<uint4*>(upool + dbase * K);
   const int kc_n = K / 8;
-  for (int c = t; c < kPoolBlock * kc_n; c += kPoolBlock) {
+  for (int c = t; c < kPoolBlock * kc_n; c += kPoolThreads) {
     const int d8 = c & 7, kc = (c >> 3) % kc_n, dg = (c >> 3) / kc_n;
     const int dl = dg * 8 + d8;
     const double inv = s_inv[dl];
@@ -143,7 +145,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   if (N >= 8) {
     const int wpr = N / 8;  // 16-byte words per row
     uint4* qdst = reinterpret_cast<uint4*>(qpool + dbase * kSyms * N);
-    for (int c = t; c < kPoolBlock * kSyms * wpr; c += kPoolBlock) {
+    for (int c = t; c < kPoolBlock * kSyms * wpr; c += kPoolThreads) {
       const int w = c % wpr, row = c / wpr, sym = row & 7, dl = row >> 3;
       const unsigned char* pr = s_perm + sym * N + w * 8;
       const unsigned short* qs = sq_tile + dl * N;
@@ -154,7 +156,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     }
   } else {  // N == 4: one 8-byte row per (domain, isometry)
     uint2* qdst = reinterpret_cast<uint2*>(qpool + dbase * kSyms * N);
-    for (int row = t; row < kPoolBlock * kSyms; row += kPoolBlock) {
+    for (int row = t; row < kPoolBlock * kSyms; row += kPoolThreads) {
       const int sym = row & 7, dl = row >> 3;
       const unsigned char* pr = s_perm + sym * N;
       const unsigned short* qs = sq_tile + dl * N;
@@ -429,7 +431,7 @@ __device__ __forceinline__ double load_bar(const unsigned long long* gbest, int 
 // Exact evaluation of the 8 isometries of the (2h+1)^2 grid domains around each range's own
 // 2x-scaled neighbourhood (self-similar candidates that usually fit well) to give the
 // first scan level a bar.  One thread per (range, local domain, isometry).
-constexpr int kSeedHalf = 2;
+constexpr int kSeedHalf = 1;
 constexpr int kSeedSide = 2 * kSeedHalf + 1;
 constexpr int kSeedPerRange = kSeedSide * kSeedSide * kSyms;
 
@@ -540,9 +542,8 @@ __device__ __forceinline__ bool range_allpass(float T) { return !(T > 1e-3f); }
 // R[row][j] = (b[i] - Sb/N) / T_r with perm_s(i) = j, so sum_j u_j R[row][j] = X / T_r.
 __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict__ img, const Geometry& g,
                              const RangeMeta* __restrict__ rmeta, const float* __restrict__ thr, int mt, int tid,
-                             int nthreads) {
+                             int nthreads, int chunks) {
   const int K = g.K, N = g.N, n = g.n;
-  const int chunks = kScanRows * (K / 8);
   for (int c = tid; c < chunks; c += nthreads) {
     const int row = c / (K / 8), kc = c % (K / 8);
     const int rl = row >> 3, s = row & 7;
@@ -590,7 +591,10 @@ __global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta
 __global__ void __launch_bounds__(256)
 range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
                 const float* __restrict__ thr, unsigned char* __restrict__ ropnd) {
-  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, thr, blockIdx.x, threadIdx.x, 256);
+  // blockIdx.y splits the m-tile's 256 x K/8 chunks over several CTAs
+  const int per = kScanRows * (g.K / 8) / gridDim.y;
+  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, thr, blockIdx.x,
+               blockIdx.y * per + threadIdx.x, blockDim.x, blockIdx.y * per + per);
 }
 
 // Survivor appender of one warp: entries go straight to the CTA's list partition, into
@@ -1085,7 +1089,7 @@ range_op2_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeM
                  unsigned short* __restrict__ ropnd) {
   const int K = g.K, N = g.N, n = g.n;
   const int mt = blockIdx.x;
-  for (int c = threadIdx.x; c < kScanRows * K; c += blockDim.x) {
+  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < kScanRows * K; c += blockDim.x * gridDim.y) {
     const int row = c / K, j = c % K;
     const int rl = row >> 3, s = row & 7;
     const int r = mt * kScanRanges + rl;
@@ -1353,7 +1357,7 @@ int scan_rows_per_cta() { return kScanRanges; }
 void launch_pool_v3(const unsigned char* img, const Geometry& g, __half* upool, unsigned short* qpool,
                     DomainMetaI* meta_i, unsigned long long* flat_count, cudaStream_t st) {
   const int blocks = (int)(scan_pool_domains(g) / kPoolBlock);
-  pool_v3_kernel<<<blocks, kPoolBlock, kPoolBlock * g.N * sizeof(unsigned short), st>>>(img, g, upool, qpool,
+  pool_v3_kernel<<<blocks, kPoolThreads, kPoolBlock * g.N * sizeof(unsigned short), st>>>(img, g, upool, qpool,
                                                                                            meta_i, flat_count);
 }
 
@@ -1445,10 +1449,10 @@ size_t range_op_bytes(const Geometry& g) {
 void launch_range_op(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta, const float* thr,
                      unsigned char* ropnd, cudaStream_t st) {
   if (scan_pair_mode())  // unscaled plain rows (the pair scan compares with per-row thresholds)
-    range_op2_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(
+    range_op2_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, 4), 256, 0, st>>>(
         img, g, rmeta, reinterpret_cast<unsigned short*>(ropnd));
   else
-    range_op_kernel<<<(g.R + kScanRanges - 1) / kScanRanges, 256, 0, st>>>(img, g, rmeta, thr, ropnd);
+    range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(img, g, rmeta, thr, ropnd);
 }
 
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
