@@ -214,7 +214,8 @@ struct Workspace {
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
       diag, scratch, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
-  unsigned long long list_cap = 0;  // survivor-list capacity (entries), grown on overflow
+  unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
+  unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
   std::mutex mu;
 };
 
@@ -373,7 +374,10 @@ void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g,
 // tcgen05 path: K1 normalised pool, range pass, seed, sparse levels, final level.
 void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b,
                          fic_mapping* d_out, unsigned long long* d_counters, cudaStream_t st) {
-  if (ws.list_cap == 0) ws.list_cap = std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128);
+  // list capacity: the geometry's default, or what an earlier overflow grew it to
+  ws.list_cap_grown = std::max(ws.list_cap_grown, std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128));
+  ws.list_cap = ws.list_cap_grown;
+  if (const char* lc = std::getenv("FIC_LIST_CAP")) ws.list_cap = std::strtoull(lc, nullptr, 10);  // tests: force overflow
   CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(b.cnt, 0, kScanCountSlots * sizeof(unsigned long long), st));
   launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);
@@ -490,6 +494,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fi
       const unsigned long long per_entry = sizeof(uint2) * 2 + sizeof(double);  // list + pending + residual
       const unsigned long long limit = (ws.list.cap + ws.res.cap + ws.pend.cap + free_b / 4) / per_entry;
       ws.list_cap = std::max(ws.list_cap, std::min(want, limit));
+      if (!std::getenv("FIC_LIST_CAP")) ws.list_cap_grown = ws.list_cap;
     }
     enqueue_final(ws, d_img, g, b, nl - 1, d_out, st);
   }

@@ -32,15 +32,36 @@ def assert_same(got, want, ctx=""):
     assert len(bad) == 0, f"{ctx}: residual bits differ at {bad[:10]}: {got['residual'][bad[:3]]} vs {want['residual'][bad[:3]]}"
 
 
-@pytest.fixture(params=["tc", "simt"])
+class env:
+    """Temporarily set environment variables (the library reads them on every call)."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.old[k] = os.environ.get(k)
+            os.environ[k] = str(v)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+# "tc": the single-CTA tcgen05 scan (default), "pair": the CTA-pair scan (cta_group::2),
+# "simt": the CUDA-core matcher (parity anchor, n >= 16 path)
+MATCHERS = {"tc": dict(FIC_MATCHER="tc", FIC_SCAN="1cta"), "pair": dict(FIC_MATCHER="tc", FIC_SCAN="pair"),
+            "simt": dict(FIC_MATCHER="simt", FIC_SCAN="1cta")}
+
+
+@pytest.fixture(params=list(MATCHERS))
 def matcher(request):
-    old = os.environ.get("FIC_MATCHER")
-    os.environ["FIC_MATCHER"] = request.param
-    yield request.param
-    if old is None:
-        os.environ.pop("FIC_MATCHER", None)
-    else:
-        os.environ["FIC_MATCHER"] = old
+    with env(**MATCHERS[request.param]):
+        yield request.param
 
 
 VARIANTS = [dict(), dict(step=2, s_max=0.75), dict(o_bits=6, s_bits=4)]
@@ -173,3 +194,35 @@ def test_batch(oracle):
         assert_same(encs[i].mappings, want, f"slice {i}")
         total += s["candidates_tested"]
     assert st["candidates_tested"] == total
+
+
+@pytest.mark.parametrize("mode", ["exhaustive", "no_prepass", "tiny_list", "pair_tiny_list"])
+def test_pruning_is_output_neutral(oracle, mode):
+    """The scan's bound, the sparse levels and the survivor-list overflow path never change the
+    result: exhaustive evaluation (every candidate through the exact path), a single full level,
+    and a list so small that every level overflows and the full level is re-run all give the
+    reference's records."""
+    settings = {"exhaustive": dict(FIC_DEBUG=1), "no_prepass": dict(FIC_PREPASS=0),
+                "tiny_list": dict(FIC_LIST_CAP=4096), "pair_tiny_list": dict(FIC_LIST_CAP=4096, FIC_SCAN="pair")}
+    img = oracle.noise_image(64, 911)
+    img[:16, :16] = 90  # some shadow ranges and flat domains
+    for pv in (dict(n=4, step=1), dict(n=8, step=2), dict(n=2, step=3)):
+        want, st = oracle.encode(img, pv)
+        with env(**settings[mode]):
+            enc = fic.encode(img, fic.CodecParams(**pv))
+        assert_same(enc.mappings, want, f"{mode} {pv}")
+        assert enc.stats == st
+
+
+def test_scan_modes_cfg4_sample(oracle):
+    """cfg4 (2048x2048, n=8, step 2): both tcgen05 scans agree with the reference on sampled rows."""
+    img = images.xray(2048, 1404004)
+    pv = dict(n=8, step=2)
+    rows = [0, 101, 255]
+    want, _ = oracle.encode_threaded(img, pv, rows=rows)
+    R = 2048 // 8
+    for scan in ("1cta", "pair"):
+        with env(FIC_SCAN=scan):
+            enc = fic.encode(img, fic.CodecParams(**pv))
+        got = np.concatenate([enc.mappings[r * R:(r + 1) * R] for r in rows])
+        assert_same(got, want, f"cfg4 rows {scan}")
