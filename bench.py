@@ -273,6 +273,17 @@ def run_ours(args):
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = comps * world * e2e_steps / float(e2e_s.item())
 
+    # ---- decoder (K3): 10 iterations at magnification 8 (4096^2 fp64 rasters for cfg2,
+    # 128 MiB each: above L2), HBM-bound; device time of the iterations via events ----
+    dec_scale = max(1, 4096 // side)
+    fic.set_matcher_timing(True)
+    fic.decode(enc, scale=dec_scale, iterations=2)
+    fic.decode_timing(reset=True)
+    for _ in range(3):
+        fic.decode(enc, scale=dec_scale, iterations=10)
+    dec_ms, dec_bytes, _ = fic.decode_timing(reset=True)
+    fic.set_matcher_timing(False)
+
     line = None
     if rank == 0:
         bf16, hbm, src = peaks()
@@ -307,6 +318,12 @@ def run_ours(args):
                          "matcher_ms": matcher_ms, "matcher_tflops": matcher_tflops,
                          "matcher_note": "all scan levels + survivor evaluation, per encode"},
             "survivors_per_level": survivors,
+            "decoder": {"kernel": "decode_step_kernel (+ fused step-RMSE partials)", "bound": "hbm",
+                        "scale": dec_scale, "iterations": 10, "output": f"{side * dec_scale}^2 fp64",
+                        "ms": dec_ms, "achieved": dec_bytes / (dec_ms / 1e3) / 1e9 if dec_ms > 0 else None,
+                        "peak": hbm, "unit": "GB/s",
+                        "frac": dec_bytes / (dec_ms / 1e3) / 1e9 / hbm if dec_ms > 0 else None,
+                        "bytes_per_pixel_iteration": 16},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

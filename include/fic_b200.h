@@ -162,6 +162,11 @@ void fic_set_matcher_timing(int32_t enabled);
 /* Average device time (ms) of the full-level tcgen05 scan kernel alone (the dominant kernel:
  * every range x domain x isometry correlation of the encode) and the number of timed launches. */
 int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset);
+/* Device time (ms) of the decode iterations of fic_decode calls without a convergence test
+ * (decode_step kernels with the fused step-RMSE partials), their algorithmic bytes
+ * (16 B per output pixel and iteration: the next raster written, the current one read) and
+ * the number of timed calls; timing is enabled with fic_set_matcher_timing. */
+int32_t fic_decode_timing(double* avg_ms, double* avg_bytes, uint64_t* calls, int32_t reset);
 /* Survivors (candidates passing the tensor-core bound) per scan level of the calling
  * process's last tcgen05-path encode; returns the number of levels (0 for the CUDA-core path). */
 int32_t fic_last_survivors(uint64_t* counts, int32_t max_levels);

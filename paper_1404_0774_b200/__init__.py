@@ -12,6 +12,7 @@ from .codec import (
     decode,
     decode_step,
     decode_traced,
+    decode_timing,
     decoded_error_bound,
     encode,
     encode_batch,
@@ -46,6 +47,7 @@ __all__ = [
     "write_pgm",
     # extensions
     "decode_step",
+    "decode_timing",
     "decode_traced",
     "encode_batch",
     "encode_device",

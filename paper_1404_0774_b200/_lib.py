@@ -42,13 +42,14 @@ def _declare(L):
     L.fic_set_matcher_timing.argtypes = [i32]
     L.fic_scan_timing.argtypes = [vp, vp, i32]
     L.fic_last_survivors.argtypes = [vp, i32]
+    L.fic_decode_timing.argtypes = [vp, vp, vp, i32]
     L.fic_set_device.argtypes = [i32]
     L.fic_device_count.argtypes = [vp]
     for name in ["fic_normalize_params", "fic_validate_geometry", "fic_encode", "fic_encode_parallel",
                  "fic_encode_range", "fic_encode_rows", "fic_encode_batch", "fic_encode_device",
                  "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
-                 "fic_last_survivors"]:
+                 "fic_last_survivors", "fic_decode_timing"]:
         getattr(L, name).restype = i32
     return L
 
@@ -73,5 +74,5 @@ EXPORTS = [
     "fic_encode", "fic_encode_parallel", "fic_encode_range", "fic_encode_rows", "fic_encode_batch",
     "fic_encode_device", "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
-    "fic_device_count", "fic_scan_timing", "fic_last_survivors",
+    "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing",
 ]

@@ -312,6 +312,15 @@ def scan_timing(reset=False):
     return ms.value, n.value
 
 
+def decode_timing(reset=False):
+    """(extension) (average ms, average algorithmic bytes, timed calls) of the decode iterations."""
+    ms = ctypes.c_double()
+    by = ctypes.c_double()
+    n = ctypes.c_uint64()
+    lib().fic_decode_timing(ctypes.byref(ms), ctypes.byref(by), ctypes.byref(n), int(reset))
+    return ms.value, by.value, n.value
+
+
 def last_survivors():
     """(extension) survivors per scan level of this process's last tcgen05-path encode."""
     buf = (ctypes.c_uint64 * 8)()

@@ -52,8 +52,10 @@ decode_step_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
     symmetry_source(t.sym, r, c, kn, sr, sc);
     const double* row0 = cur + (long long)(t.dy + 2 * sr) * out_w + t.dx + 2 * sc;
     const double* row1 = row0 + out_w;
-    // ((p00 + p01) + p10 + p11) / 4.0 then s*z + o, each op rounded (decoder.cpp:71-75)
-    const double z = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(row0[0], row0[1]), row1[0]), row1[1]), 4.0);
+    // ((p00 + p01) + p10 + p11) / 4.0 then s*z + o, each op rounded (decoder.cpp:71-75); the
+    // division by 4 is an exact power-of-two scaling, identical to the multiplication by 0.25
+    const double z = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(__ldg(row0), __ldg(row0 + 1)), __ldg(row1)), __ldg(row1 + 1)),
+                               0.25);
     const double v = __dadd_rn(__dmul_rn(t.s, z), t.o);
     nxt[idx] = v;
     const double dlt = __dsub_rn(cur[idx], v);
@@ -102,6 +104,12 @@ __global__ void quantize_raster_kernel(const double* __restrict__ r, long long c
 }
 
 int decode_blocks(long long count) { return (int)((count + kDecodeThreads - 1) / kDecodeThreads); }
+
+// Partials one decode step writes.
+int decode_partials(int out_w, int kn) {
+  (void)kn;
+  return decode_blocks((long long)out_w * out_w);
+}
 
 void launch_xform(const fic_mapping* maps, int count, int scale, const Geometry& g, RangeXform* xf, cudaStream_t st) {
   xform_kernel<<<(count + 255) / 256, 256, 0, st>>>(maps, count, scale, g.s_bits, g.s_max, g.o_bits, xf);

@@ -37,6 +37,7 @@ struct RangeXform {
   int pad;
 };
 int decode_blocks(long long);
+int decode_partials(int, int);
 void launch_xform(const fic_mapping*, int, int, const Geometry&, RangeXform*, cudaStream_t);
 void launch_decode_step(const double*, double*, const RangeXform*, int, int, int, double*, cudaStream_t);
 void launch_rmse_finish(const double*, int, long long, double*, cudaStream_t);
@@ -91,6 +92,9 @@ double g_timing_ms = 0.0;
 unsigned long long g_timing_n = 0;
 double g_scan_ms = 0.0;            // the full-level scan kernel alone
 unsigned long long g_scan_n = 0;
+double g_decode_ms = 0.0;          // decode iterations (decode_step + RMSE partials), device time
+unsigned long long g_decode_n = 0;
+double g_decode_bytes = 0.0;       // their algorithmic bytes
 std::mutex g_surv_mu;
 std::vector<unsigned long long> g_last_surv;  // survivors per level of the last encode (tcgen05 path)
 
@@ -786,10 +790,12 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
     launch_raster_init(a, cnt, initial_kind, d_sup, ws.stream);
     launch_xform(d_maps, g.R, scale, g, xf, ws.stream);
     g_launches += 2;
+    const bool timed = g_timing.load() != 0 && !has_eps;
+    if (timed) CK(cudaEventRecord(ws.ev0, ws.stream));
     int runs = 0;
     for (int it = 0; it < iterations; ++it) {
       launch_decode_step(a, b, xf, out_w, p.n * scale, g.RX, part, ws.stream);
-      launch_rmse_finish(part, blocks, cnt, d_rmse + it, ws.stream);
+      launch_rmse_finish(part, decode_partials(out_w, p.n * scale), cnt, d_rmse + it, ws.stream);
       g_launches += 2;
       std::swap(a, b);
       ++runs;
@@ -799,12 +805,24 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
         if (h_rmse[it] < convergence_eps) break;
       }
     }
+    if (timed) CK(cudaEventRecord(ws.ev1, ws.stream));
     launch_quantize_raster(a, cnt, d_u8, ws.stream);
     g_launches += 1;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h_rmse, d_rmse, (size_t)runs * 8, cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaMemcpyAsync(out, d_u8, (size_t)cnt, cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
+    if (timed) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ws.ev0, ws.ev1) == cudaSuccess) {
+        std::lock_guard<std::mutex> lock(g_timing_mu);
+        g_decode_ms += ms;
+        g_decode_n += 1;
+        // per iteration and output pixel: 8 B written + 8 B of the current raster read (the
+        // minimum; the 2x2 gathers and the step-RMSE re-read hit the same raster)
+        g_decode_bytes += (double)runs * 16.0 * (double)cnt;
+      }
+    }
     if (step_rmse) std::memcpy(step_rmse, h_rmse, (size_t)runs * 8);
     if (iterations_run) *iterations_run = runs;
     return FIC_OK;
@@ -839,7 +857,7 @@ int32_t fic_collage_error(const uint8_t* image, int32_t img_width, int32_t img_h
     launch_raster_init(a, cnt, FIC_INITIAL_SUPPLIED, d_u8, ws.stream);
     launch_xform(d_maps, g.R, 1, g, xf, ws.stream);
     launch_decode_step(a, b, xf, width, p.n, g.RX, part, ws.stream);
-    launch_rmse_finish(part, blocks, cnt, d_rmse, ws.stream);
+    launch_rmse_finish(part, decode_partials(width, p.n), cnt, d_rmse, ws.stream);
     g_launches += 4;
     CK(cudaGetLastError());
     double r = 0;
@@ -892,6 +910,18 @@ int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
   if (reset) {
     g_scan_ms = 0.0;
     g_scan_n = 0;
+  }
+  return FIC_OK;
+}
+
+int32_t fic_decode_timing(double* avg_ms, double* avg_bytes, uint64_t* calls, int32_t reset) {
+  std::lock_guard<std::mutex> lock(g_timing_mu);
+  if (avg_ms) *avg_ms = g_decode_n ? g_decode_ms / (double)g_decode_n : 0.0;
+  if (avg_bytes) *avg_bytes = g_decode_n ? g_decode_bytes / (double)g_decode_n : 0.0;
+  if (calls) *calls = g_decode_n;
+  if (reset) {
+    g_decode_ms = g_decode_bytes = 0.0;
+    g_decode_n = 0;
   }
   return FIC_OK;
 }
