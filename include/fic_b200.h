@@ -125,6 +125,15 @@ int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height,
                           const fic_params* params, fic_mapping* d_out, fic_stats* stats,
                           void* stream);
 
+/* Device-resident batch (cfg5 volume): `d_images` holds `count` slices back to back,
+ * `d_out` count * (side/n)^2 records, both device pointers.  Up to 64 slices are stacked
+ * into one encode pass (one pool, one scan over every slice's ranges; each range only
+ * meets its own slice's domains), so a volume costs a handful of launches per 64 slices.
+ * Synchronises `stream` before returning; stats are the sum over slices. */
+int32_t fic_encode_batch_device(const uint8_t* d_images, int32_t count, int32_t width,
+                                int32_t height, const fic_params* params, fic_mapping* d_out,
+                                fic_stats* stats, void* stream);
+
 /* ---- decoder (proj/include/fic/decoder.hpp:45-63) ---- */
 /* decode_step (proj/src/decoder.cpp:39-79) on fp64 rasters of (width*scale)^2 pixels. */
 int32_t fic_decode_step(const double* current, int32_t cur_width, int32_t cur_height,

@@ -17,6 +17,7 @@ from .codec import (
     encode,
     encode_batch,
     encode_device,
+    encode_batch_device,
     encode_range,
     encode_rows,
     encode_with_stats,
@@ -51,6 +52,7 @@ __all__ = [
     "decode_traced",
     "encode_batch",
     "encode_device",
+    "encode_batch_device",
     "encode_range",
     "encode_rows",
     "encode_with_stats",

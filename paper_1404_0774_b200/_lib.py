@@ -33,6 +33,7 @@ def _declare(L):
     L.fic_encode_rows.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp]
     L.fic_encode_batch.argtypes = [vp, i32, i32, i32, vp, vp, vp]
     L.fic_encode_device.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.fic_encode_batch_device.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fic_decode_step.argtypes = [vp, i32, i32, vp, i32, i32, vp, i32, vp]
     L.fic_decode.argtypes = [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, i32, f64, vp, vp, vp]
     L.fic_collage_error.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp]
@@ -49,7 +50,7 @@ def _declare(L):
                  "fic_encode_range", "fic_encode_rows", "fic_encode_batch", "fic_encode_device",
                  "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
-                 "fic_last_survivors", "fic_decode_timing"]:
+                 "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device"]:
         getattr(L, name).restype = i32
     return L
 
@@ -74,5 +75,5 @@ EXPORTS = [
     "fic_encode", "fic_encode_parallel", "fic_encode_range", "fic_encode_rows", "fic_encode_batch",
     "fic_encode_device", "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
-    "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing",
+    "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
 ]

@@ -168,8 +168,9 @@ def encode_rows(image, row_begin, row_end, params=None):
 
 
 def encode_batch(images, params=None):
-    """(extension) encode a (count, side, side) uint8 volume slice by slice; returns a list of
-    EncodedImage and the summed stats."""
+    """(extension) encode a (count, side, side) uint8 volume (up to 64 slices per encode pass;
+    each slice's codes equal its own fic_encode); returns a list of EncodedImage and the
+    summed stats."""
     params = CodecParams() if params is None else params
     vol = np.ascontiguousarray(np.asarray(images), dtype=np.uint8)
     if vol.ndim != 3:
@@ -285,6 +286,18 @@ def encode_device(d_image_ptr, width, height, d_out_ptr, params=None, stream=0, 
                                    ctypes.byref(params.struct), ctypes.c_void_p(d_out_ptr),
                                    ctypes.byref(st) if stats else None, ctypes.c_void_p(stream)))
     return st.as_dict() if stats else None
+
+
+def encode_batch_device(d_images_ptr, count, width, height, d_out_ptr, params=None, stream=0):
+    """(extension) device-resident volume encode: `count` uint8 slices back to back at
+    `d_images_ptr`, count x (width/n)^2 records at `d_out_ptr`; up to 64 slices per encode
+    pass.  Synchronises `stream`; returns the summed stats."""
+    params = CodecParams() if params is None else params
+    st = FicStats()
+    _check(lib().fic_encode_batch_device(ctypes.c_void_p(d_images_ptr), int(count), int(width), int(height),
+                                         ctypes.byref(params.struct), ctypes.c_void_p(d_out_ptr),
+                                         ctypes.byref(st), ctypes.c_void_p(stream)))
+    return st.as_dict()
 
 
 def kernel_launch_count():

@@ -36,6 +36,13 @@ struct Geometry {
   int s_bits, o_bits;
   double s_max;
   double shadow_eps;
+  // batched encodes (volumes): `batch` equal slices stacked vertically (H = H1 * batch); ranges
+  // are numbered across the stack (R = R1 * batch), domains per slice (D), and slice b's pool
+  // entries start at domain b * Dt.  batch == 1 for single images.
+  int batch;
+  int H1;
+  int R1;
+  int Dt;
 };
 
 // Per-domain metadata written by the pool builder.
@@ -78,11 +85,24 @@ __host__ __device__ __forceinline__ void range_origin(const Geometry& g, int r, 
   }
 }
 
-// Pixel origin of canonical domain d: x outer, y inner (proj/src/codebook.cpp:17-18).
+// Slice-local position of canonical domain d: x outer, y inner (proj/src/codebook.cpp:17-18)
+// (d is a pool index; in a batch, slice b's domains are b * Dt + local index).
 __host__ __device__ __forceinline__ void domain_origin(const Geometry& g, int d, int& x, int& y) {
-  x = (d / g.PY) * g.step;
-  y = (d % g.PY) * g.step;
+  const int dl = g.batch > 1 ? d % g.Dt : d;
+  x = (dl / g.PY) * g.step;
+  y = (dl % g.PY) * g.step;
 }
+
+// Pixel origin of pool domain d in the (stacked) image, and its slice.
+__host__ __device__ __forceinline__ int domain_origin_px(const Geometry& g, int d, int& x, int& y) {
+  const int b = g.batch > 1 ? d / g.Dt : 0;
+  domain_origin(g, d, x, y);
+  y += b * g.H1;
+  return b;
+}
+
+// Slice of encoded range r.
+__host__ __device__ __forceinline__ int range_slice(const Geometry& g, int r) { return g.batch > 1 ? r / g.R1 : 0; }
 
 // ------------------------------------------------------------------ quantiser
 // UniformQuantizer::quantize / dequantize (proj/include/fic/format.hpp:26-40).

@@ -172,6 +172,10 @@ Geometry make_geometry(int w, int h, const fic_params& p) {
   g.o_bits = p.o_bits;
   g.s_max = p.s_max;
   g.shadow_eps = p.shadow_eps;
+  g.batch = 1;
+  g.H1 = h;
+  g.R1 = g.R;
+  g.Dt = 0;
   return g;
 }
 
@@ -318,7 +322,7 @@ struct ScanBufs {
 };
 
 ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
-  const long long Dt = scan_pool_domains(g);
+  const long long Dt = (long long)g.Dt * g.batch;  // every slice's pool
   ScanBufs b;
   b.upool = static_cast<__half*>(ws.upool.get((size_t)Dt * g.K * 2));
   b.qpool = static_cast<unsigned short*>(ws.qpool.get((size_t)Dt * 8 * g.N * 2));  // q8: [domain][isometry][N]
@@ -382,10 +386,10 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   ws.list_cap_grown = std::max(ws.list_cap_grown, std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128));
   ws.list_cap = ws.list_cap_grown;
   if (const char* lc = std::getenv("FIC_LIST_CAP")) ws.list_cap = std::strtoull(lc, nullptr, 10);  // tests: force overflow
-  CK(cudaMemsetAsync(d_counters, 0, 2 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(d_counters, 0, 2 * g.batch * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(b.cnt, 0, kScanCountSlots * sizeof(unsigned long long), st));
-  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);
-  launch_range_pass(d_img, g, b.rm, d_counters + 1, st);
+  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);  // flat domains per slice
+  launch_range_pass(d_img, g, b.rm, d_counters + g.batch, st);       // shadow ranges per slice
   launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
   launch_deq_tables(g, b.deq, st);
   launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
@@ -438,10 +442,14 @@ void enqueue_encode_simt(Workspace& ws, const unsigned char* d_img, const Geomet
 
 // Enqueue the whole encode of the region described by g and wait for it; a survivor list
 // that overflowed is grown to the count the scan reported and the encode is re-run.
-// counters[0] = flat domains, counters[1] = shadow ranges (copied to h_counters).
-void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fic_mapping* d_out,
+// counters[b] = flat domains and counters[batch + b] = shadow ranges of slice b (copied to
+// h_counters; batch == 1 for a single image).
+void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in, fic_mapping* d_out,
                 unsigned long long* d_counters, unsigned long long* h_counters, cudaStream_t st) {
+  Geometry g = g_in;
+  if (g.Dt == 0) g.Dt = (int)scan_pool_domains(g);  // per-slice pool stride (a multiple of 896)
   if (matcher_mode(g) == 0) {
+    if (g.batch != 1) throw InternalFail{"batched encode needs the tcgen05 scan path"};
     enqueue_encode_simt(ws, d_img, g, d_out, d_counters, st);
     if (h_counters)
       CK(cudaMemcpyAsync(h_counters, d_counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -455,7 +463,8 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g, fi
   for (int attempt = 0;; ++attempt) {
     CK(cudaMemcpyAsync(hc, b.cnt, kScanCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (h_counters)
-      CK(cudaMemcpyAsync(h_counters, d_counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_counters, d_counters, 2 * g.batch * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                         st));
     CK(cudaStreamSynchronize(st));
     const std::vector<int> lv = scan_levels(g);
     const int fparts = scan_grid(g, 1, ws.sms);
@@ -520,6 +529,40 @@ void collect_timing(Workspace& ws) {
   ws.scan_timed = false;
 }
 
+// EncodeStats summed over the slices of a batch (flat[b] = h[b], shadow[b] = h[batch + b]).
+void fill_stats_batch(fic_stats* stats, const Geometry& g, const unsigned long long* h) {
+  if (!stats) return;
+  fic_stats t{0, 0, 0};
+  for (int b = 0; b < g.batch; ++b) {
+    const unsigned long long flat = h[b], shadow = h[g.batch + b];
+    const unsigned long long active = (unsigned long long)g.R1 - shadow;
+    t.candidates_tested += 8ull * active * ((unsigned long long)g.D - flat);
+    t.shadow_ranges += shadow;
+    t.shadow_codeblocks += 8ull * active * flat;
+  }
+  *stats = t;
+}
+
+// Slices stacked into one encode pass: up to 64 when the tcgen05 scan applies and a slice
+// holds whole 32-range scan tiles (so no tile straddles two slices' domain pools), else 1.
+int batch_chunk(const Geometry& g) {
+  if (matcher_mode(g) != 1 || g.R % 32 != 0) return 1;
+  if (const char* e = std::getenv("FIC_BATCH_CHUNK")) return std::max(1, std::atoi(e));
+  return 64;
+}
+
+Geometry batch_geometry(const Geometry& g1, int slices) {
+  Geometry g = g1;
+  if (slices <= 1) return g;
+  g.batch = slices;
+  g.H1 = g1.H;
+  g.R1 = g1.R;
+  g.H = g1.H * slices;
+  g.R = g1.R * slices;
+  g.Dt = (int)scan_pool_domains(g1);
+  return g;
+}
+
 void fill_stats(fic_stats* stats, const Geometry& g, unsigned long long flat, unsigned long long shadow) {
   if (!stats) return;
   const unsigned long long active = (unsigned long long)g.R - shadow;
@@ -551,16 +594,19 @@ int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, f
     std::memcpy(h_img, image, img_bytes);
     auto* d_img = static_cast<unsigned char*>(ws.img.get(img_bytes));
     auto* d_out = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
-    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
+    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * g.batch * sizeof(unsigned long long)));
     auto* h_out = static_cast<fic_mapping*>(ws.h_out.get((size_t)g.R * sizeof(fic_mapping)));
-    auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * sizeof(unsigned long long)));
+    auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * g.batch * sizeof(unsigned long long)));
     CK(cudaMemcpyAsync(d_img, h_img, img_bytes, cudaMemcpyHostToDevice, ws.stream));
     run_encode(ws, d_img, g, d_out, d_cnt, h_cnt, ws.stream);
     CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
     collect_timing(ws);
     std::memcpy(out, h_out, (size_t)g.R * sizeof(fic_mapping));
-    fill_stats(stats, g, h_cnt[0], h_cnt[1]);
+    if (g.batch > 1)
+      fill_stats_batch(stats, g, h_cnt);
+    else
+      fill_stats(stats, g, h_cnt[0], h_cnt[1]);
     return FIC_OK;
   });
 }
@@ -679,11 +725,14 @@ int32_t fic_encode_batch(const uint8_t* images, int32_t count, int32_t width, in
   if (e) return e;
   if ((e = geometry_check(width, height, p))) return e;
   if (count < 0) return fail(FIC_ERR_BAD_PARAMS, "negative batch size");
+  if (count > 0 && (!images || !out)) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
   const Geometry g = make_geometry(width, height, p);
   fic_stats total{0, 0, 0};
-  for (int i = 0; i < count; ++i) {
+  const int chunk = batch_chunk(g);
+  for (int i = 0; i < count; i += chunk) {
+    const int k = std::min(chunk, count - i);
     fic_stats s{0, 0, 0};
-    e = encode_host(images + (size_t)i * width * height, g, out + (size_t)i * g.R, &s);
+    e = encode_host(images + (size_t)i * width * height, batch_geometry(g, k), out + (size_t)i * g.R, &s);
     if (e) return e;
     total.candidates_tested += s.candidates_tested;
     total.shadow_ranges += s.shadow_ranges;
@@ -691,6 +740,43 @@ int32_t fic_encode_batch(const uint8_t* images, int32_t count, int32_t width, in
   }
   if (stats) *stats = total;
   return FIC_OK;
+}
+
+// Encode `count` slices already resident on the device (d_images: count x height x width,
+// d_out: count x ranges per slice), stacked `batch_chunk` slices per pass.
+int32_t fic_encode_batch_device(const uint8_t* d_images, int32_t count, int32_t width, int32_t height,
+                                const fic_params* params, fic_mapping* d_out, fic_stats* stats, void* stream) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  if (count < 0) return fail(FIC_ERR_BAD_PARAMS, "negative batch size");
+  if (count > 0 && (!d_images || !d_out)) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  const Geometry g1 = make_geometry(width, height, p);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    fic_stats total{0, 0, 0};
+    const int chunk = batch_chunk(g1);
+    for (int i = 0; i < count; i += chunk) {
+      const Geometry g = batch_geometry(g1, std::min(chunk, count - i));
+      auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * g.batch * sizeof(unsigned long long)));
+      auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * g.batch * sizeof(unsigned long long)));
+      run_encode(ws, d_images + (size_t)i * width * height, g, d_out + (size_t)i * g1.R, d_cnt, h_cnt, st);
+      fic_stats s{0, 0, 0};
+      if (g.batch > 1)
+        fill_stats_batch(&s, g, h_cnt);
+      else
+        fill_stats(&s, g, h_cnt[0], h_cnt[1]);
+      total.candidates_tested += s.candidates_tested;
+      total.shadow_ranges += s.shadow_ranges;
+      total.shadow_codeblocks += s.shadow_codeblocks;
+      collect_timing(ws);
+    }
+    if (stats) *stats = total;
+    return FIC_OK;
+  });
 }
 
 int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height, const fic_params* params,

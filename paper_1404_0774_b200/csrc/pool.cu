@@ -109,7 +109,7 @@ __global__ void range_pass_kernel(const unsigned char* __restrict__ img, Geometr
   const long long var = (long long)g.N * sbb - sb * sb;
   const int shadow = (double)var <= g.shadow_eps;
   meta[r] = RangeMeta{(int)sb, shadow, var};
-  if (shadow) atomicAdd(shadow_count, 1ull);
+  if (shadow) atomicAdd(shadow_count + range_slice(g, r), 1ull);  // per slice of a batch
 }
 
 void launch_pool_build(const unsigned char* img, const Geometry& g, unsigned char* pool, DomainMetaF* meta_f,

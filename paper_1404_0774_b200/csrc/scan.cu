@@ -78,14 +78,17 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     symmetry_source(s, i / n, i % n, n, sr, sc);
     s_perm[k] = (unsigned char)(sr * n + sc);
   }
+  // a block never straddles slices of a batch (Dt is a multiple of the block)
+  const int slice = g.batch > 1 ? (int)(dbase / g.Dt) : 0;
+  const long long lbase = dbase - (long long)slice * (g.batch > 1 ? g.Dt : 0);  // slice-local index
   // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step
   for (int idx = t; idx < kPoolBlock * N; idx += kPoolThreads) {
     const int dl = idx / N, j = idx % N;
     const long long d = dbase + dl;
     int v = 0;
-    if (d < g.D) {
+    if (lbase + dl < g.D) {
       int x, y;
-      domain_origin(g, (int)d, x, y);
+      domain_origin_px(g, (int)d, x, y);
       const unsigned char* row0 = img + (long long)(y + 2 * (j / n)) * g.W + x + 2 * (j % n);
       const unsigned char* row1 = row0 + g.W;
       v = row0[0] + row0[1] + row1[0] + row1[1];
@@ -102,7 +105,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
       s += v;
       ss += (long long)v * v;
     }
-    if (d < g.D) {
+    if (lbase + t < g.D) {
       const long long den = (long long)N * ss - s * s;
       const bool flat = (double)den <= 16.0 * g.shadow_eps;
       meta_i[d] = DomainMetaI{s, flat ? -1 : den};
@@ -115,7 +118,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     s_sum[t] = s;
   }
   __syncthreads();
-  if (t == 0 && s_flat) atomicAdd(flat_count, (unsigned long long)s_flat);
+  if (t == 0 && s_flat) atomicAdd(flat_count + slice, (unsigned long long)s_flat);  // per slice
   // phase 2a: fp16 normalised operand u = (N q - Sq) / sqrt(den), UMMA K-major no-swizzle
   // core matrices, chunk c = ((dl/8) * (K/8) + k/8) * 8 + dl%8 (16-byte coalesced stores)
   uint4* out = reinterpret_cast<uint4*>(upool + dbase * K);
@@ -448,11 +451,12 @@ seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned
   if (m.shadow || g.D == 0) return;
   int x0, y0;
   range_origin(g, r, x0, y0);
-  const int cx = x0 - g.n / 2, cy = y0 - g.n / 2;
+  const int b = range_slice(g, r);
+  const int cx = x0 - g.n / 2, cy = y0 - b * g.H1 - g.n / 2;  // slice-local
   const int xi0 = min(max(cx / g.step, 0), g.PX - 1), yi0 = min(max(cy / g.step, 0), g.PY - 1);
   const int xi = xi0 + w / kSeedSide - kSeedHalf, yi = yi0 + w % kSeedSide - kSeedHalf;
   if (xi < 0 || yi < 0 || xi >= g.PX || yi >= g.PY) return;
-  const int d = xi * g.PY + yi;
+  const int d = b * g.Dt + xi * g.PY + yi;
   const DomainMetaI mi = meta_i[d];
   if (mi.den < 0) return;
   uint32_t qw[NN / 2], bpk[NN / 4];
@@ -745,10 +749,12 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       }
     }
     if (lane == 0) {
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(upool);
       int i = 0;
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, cta, G, sg);
+        // the segment's slice pool (batched encodes: slice b's domains start at b * Dt)
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) +
+                                   (long long)range_slice(g, S.m * kScanRanges) * g.Dt * K * 2;
         for (int j = S.j0; j < S.j1; ++j, ++i) {
           const int s = i % stages;
           ptx::mbar_wait(&empty_bar[s], ((i / stages) & 1) ^ 1);
@@ -798,6 +804,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     for (int sg = 0; sg < nseg; ++sg) {
       const Segment S = seg_at(lv, cta, G, sg);
       const int r0 = S.m * kScanRanges + half * 16;  // this thread's 16 ranges
+      const uint32_t dslice = (uint32_t)(range_slice(g, r0) * g.Dt);  // pool index of the slice's domain 0
       uint32_t allpass = 0;                          // ranges without a usable threshold
 #pragma unroll
       for (int k = 0; k < 16; k += 4) {
@@ -808,7 +815,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       const uint32_t rowbase = (uint32_t)r0 * 8u;
       for (int j = S.j0; j < S.j1; ++j, ++i) {
         const int buf = i & 1;
-        const uint32_t d = (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
+        const uint32_t d = dslice + (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
         ptx::mbar_wait(&tfull_bar[buf], (i >> 1) & 1);
         ptx::tc_fence_after();
         if (g.flags & 128) {  // debug: no TMEM reads at all (MMA + producer throughput)
@@ -1176,10 +1183,11 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
   if (warp == 0) {
     // ================= producer: this CTA's half of every tile =================
     if (lane == 0) {
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) + (size_t)rank * L.p_bytes;
       int i = 0;
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, pair, G, sg);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) + (size_t)rank * L.p_bytes +
+                                   (long long)range_slice(g, S.m * kScanRanges) * g.Dt * K * 2;
         for (int j = S.j0; j < S.j1; ++j, ++i) {
           const int s = i % stages;
           ptx::mbar_wait(&empty_bar[s], ((i / stages) & 1) ^ 1);
@@ -1302,7 +1310,8 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
         }
         const bool hit = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > T;
         if (__any_sync(0xffffffffu, hit)) {
-          const uint32_t d0 = (uint32_t)(j * lv.stride * kP2Dom + half * kP2Half);
+          const uint32_t d0 =
+              (uint32_t)(range_slice(g, r) * g.Dt) + (uint32_t)(j * lv.stride * kP2Dom + half * kP2Half);
           constexpr int NQ = (kP2Half + 31) / 32;
           uint32_t mk[NQ];
 #pragma unroll
@@ -1356,7 +1365,7 @@ int scan_rows_per_cta() { return kScanRanges; }
 
 void launch_pool_v3(const unsigned char* img, const Geometry& g, __half* upool, unsigned short* qpool,
                     DomainMetaI* meta_i, unsigned long long* flat_count, cudaStream_t st) {
-  const int blocks = (int)(scan_pool_domains(g) / kPoolBlock);
+  const int blocks = (int)((long long)g.Dt * g.batch / kPoolBlock);
   pool_v3_kernel<<<blocks, kPoolThreads, kPoolBlock * g.N * sizeof(unsigned short), st>>>(img, g, upool, qpool,
                                                                                            meta_i, flat_count);
 }

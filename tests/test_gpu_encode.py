@@ -196,6 +196,55 @@ def test_batch(oracle):
     assert st["candidates_tested"] == total
 
 
+@pytest.mark.parametrize("scan", ["tc", "pair"])
+@pytest.mark.parametrize("pv,chunk", [(dict(n=4, step=2), "64"), (dict(n=8, step=3), "2"), (dict(n=2, step=1), "3")])
+def test_batch_stacked(oracle, scan, pv, chunk):
+    """Slices stacked into one encode pass (slice-offset pools, one scan over every slice's
+    ranges): each slice's records and the summed stats equal the oracle's per-slice encode.
+    Slices differ in content (noise, smooth, a constant slice, a half-flat slice) so flat
+    domains and shadow ranges are counted per slice; chunk 2 and 3 leave a ragged last pass."""
+    side = 64
+    vol = np.stack([oracle.noise_image(side, 500 + i) for i in range(5)])
+    vol[1] = oracle.smooth_image(side, 77)
+    vol[2] = 123
+    vol[3, :, : side // 2] = 40
+    total = {"candidates_tested": 0, "shadow_ranges": 0, "shadow_codeblocks": 0}
+    wants = []
+    for i in range(len(vol)):
+        want, st = oracle.encode(vol[i], pv)
+        wants.append(want)
+        for k in total:
+            total[k] += st[k]
+    with env(FIC_BATCH_CHUNK=chunk, **MATCHERS[scan]):
+        encs, st = fic.encode_batch(vol, fic.CodecParams(**pv))
+    for i, want in enumerate(wants):
+        assert_same(encs[i].mappings, want, f"slice {i} {pv} chunk {chunk}")
+    assert st == total
+
+
+def test_batch_device_cfg5_shape(oracle):
+    """fic_encode_batch_device on cfg5 slices (512x512 CT slices, n=8, step 4), three slices in
+    one pass: every slice against fic_encode of that slice (itself oracle-checked by the cfg2
+    test), and slice 2's first two range rows against the oracle directly."""
+    import torch
+    from paper_1404_0774_b200.abi import MAPPING_DTYPE
+    vol = images.volume(count=3, side=512)
+    p = fic.CodecParams(n=8, step=4)
+    per = (512 // 8) ** 2
+    d_img = torch.from_numpy(vol).cuda()
+    d_out = torch.zeros(3 * per * MAPPING_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    st = fic.encode_batch_device(d_img.data_ptr(), 3, 512, 512, d_out.data_ptr(), p)
+    got = d_out.cpu().numpy().view(MAPPING_DTYPE)
+    total = 0
+    for i in range(3):
+        enc = fic.encode(vol[i], p)
+        assert_same(got[i * per:(i + 1) * per], enc.mappings, f"slice {i}")
+        total += enc.stats["candidates_tested"]
+    assert st["candidates_tested"] == total
+    rows, _ = oracle.encode_threaded(vol[2], {"n": 8, "step": 4}, rows=[0, 1])
+    assert_same(got[2 * per:2 * per + len(rows)], rows, "slice 2 oracle rows")
+
+
 @pytest.mark.parametrize("mode", ["exhaustive", "no_prepass", "tiny_list", "pair_tiny_list"])
 def test_pruning_is_output_neutral(oracle, mode):
     """The scan's bound, the sparse levels and the survivor-list overflow path never change the
