@@ -36,6 +36,8 @@ CONFIG_TEXT = {
     "cfg2": "512x512 CT-slice-shaped synthetic image, 8x8 ranges, domain stride 4, 8 isometries, full search",
     "cfg3": "512x512 synthetic image, 4x4 ranges, 8x8 domains stride 2, 8 isometries, full search",
     "cfg4": "2048x2048 X-ray-shaped synthetic image, 8x8 ranges, domain stride 2, 8 isometries, full search",
+    "cfg5": "volume of 512x512 CT-shaped synthetic slices, 8x8 ranges, domain stride 4, 8 isometries, full search, "
+            "slices sharded over the ranks, up to 64 slices stacked per encode pass",
 }
 
 
@@ -46,8 +48,13 @@ def _env_int(name, default):
         return default
 
 
-def make_image(cfg, rank=0):
+def make_image(cfg, rank=0, world=1, slices=512):
+    """The step's input: one image, or (cfg5) this rank's shard of the slice volume."""
     from paper_1404_0774_b200 import images
+    if cfg == "cfg5":
+        per = (slices + world - 1) // world
+        z = range(rank * per, min(slices, (rank + 1) * per))
+        return np.stack([images.ct_slice(512, 1404005 + k, k / max(slices, 1)) for k in z]), 8, 4
     gen, n, step = images.CONFIGS[cfg]
     if rank == 0 or cfg not in ("cfg2", "cfg3"):
         img = gen()
@@ -160,7 +167,9 @@ def run_reference(args):
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
-    img, n, step = make_image(args.config)
+    img, n, step = make_image(args.config, slices=1)
+    if img.ndim == 3:  # cfg5: the per-slice encode is the unit the reference runs
+        img = img[0]
     threads = os.cpu_count() or 1
     target = args.ref_ranges
     vals = []
@@ -202,21 +211,30 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    img, n, step = make_image(args.config, rank)
-    side = img.shape[0]
+    img, n, step = make_image(args.config, rank, world, args.slices)
+    volume = img.ndim == 3
+    count = img.shape[0] if volume else 1  # images per rank and step
+    side = img.shape[-1]
     R = (side // n) ** 2
     params = fic.CodecParams(n=n, step=step)
     stream = torch.cuda.current_stream()
     d_img = torch.from_numpy(img).cuda()
-    d_out = torch.empty(R * 32, dtype=torch.uint8, device="cuda")
-    gather = torch.empty(world * R * 32, dtype=torch.uint8, device="cuda") if world > 1 else None
+    d_out = torch.empty(count * R * 32, dtype=torch.uint8, device="cuda")
+    gather = torch.empty(world * count * R * 32, dtype=torch.uint8, device="cuda") if world > 1 else None
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    stats = fic.encode_device(d_img.data_ptr(), side, side, d_out.data_ptr(), params, stream.cuda_stream, stats=True)
-    comps = stats["candidates_tested"]
+    def encode_step(stats=False):
+        if volume:
+            return fic.encode_batch_device(d_img.data_ptr(), count, side, side, d_out.data_ptr(), params,
+                                           stream.cuda_stream)
+        return fic.encode_device(d_img.data_ptr(), side, side, d_out.data_ptr(), params, stream.cuda_stream,
+                                 stats=stats)
+
+    stats = encode_step(stats=True)
+    comps = stats["candidates_tested"]  # per rank and step
 
     def step_fn():
-        fic.encode_device(d_img.data_ptr(), side, side, d_out.data_ptr(), params, stream.cuda_stream)
+        encode_step()
         if world > 1:
             dist.all_gather_into_tensor(gather, d_out)
 
@@ -258,15 +276,20 @@ def run_ours(args):
 
     # ---- end-to-end through the public API (host image in, host records out) ----
     e2e_steps = max(args.steps, 5)
+    def public_encode():
+        if volume:
+            return fic.encode_batch(img, params)[0][0]
+        return fic.encode(img, params)
+
     for _ in range(2):
-        fic.encode(img, params)
+        public_encode()
     e2e_times = []
     for i in range(e2e_steps):
         flush.fill_(i & 0xFF)
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        enc = fic.encode(img, params)
+        enc = public_encode()
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -288,9 +311,11 @@ def run_ours(args):
     if rank == 0:
         bf16, hbm, src = peaks()
         D = ((side - 2 * n) // step + 1) ** 2
-        nominal = R * D * 8  # every (range, domain, isometry) correlation the full-level scan computes
-        flops = 2.0 * n * n * nominal  # algorithmic ops per full-level scan launch: 2 n^2 per comparison
-        achieved = flops / (scan_ms / 1e3) / 1e12 if scan_ms > 0 else None
+        nominal = R * D * 8 * count  # every (range, domain, isometry) correlation of the step's full-level scans
+        flops = 2.0 * n * n * nominal  # algorithmic ops per step: 2 n^2 per comparison
+        scan_launches_per_step = scan_n / args.steps if scan_n else 1
+        scan_ms_step = scan_ms * scan_launches_per_step  # full-level scan time per step
+        achieved = flops / (scan_ms_step / 1e3) / 1e12 if scan_ms > 0 else None
         matcher_tflops = 2.0 * n * n * comps / (matcher_ms / 1e3) / 1e12 if matcher_ms > 0 else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -299,20 +324,25 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "cfg": args.config, "image": f"{side}x{side}", "n": n,
                        "step": step, "ranges": R, "domains": ((side - 2 * n) // step + 1) ** 2,
-                       "comparisons_per_image": comps, "l2": "flushed between timed steps (256 MB write)",
-                       "parallelism": f"weak: {world} rank(s) x 1 image, codes all-gathered over NCCL"
+                       "images_per_rank_step": count, "comparisons_per_rank_step": comps,
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "parallelism": (f"{world} rank(s) x {count} slice(s) of a {args.slices}-slice volume, "
+                                       "codes all-gathered over NCCL" if volume else
+                                       f"weak: {world} rank(s) x 1 image, codes all-gathered over NCCL")
                        if world > 1 else "1 GPU"},
-            "encode_ms_per_image": ms_per_step,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": side * side,
-                    "d2h_bytes_per_step": R * 32 + 16,
-                    "encode_ms_per_image": float(e2e_s.item()) / e2e_steps * 1e3,
-                    "api": "paper_1404_0774_b200.encode (C-ABI fic_encode)"},
+            "encode_ms_per_image": ms_per_step / count,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": count * side * side,
+                    "d2h_bytes_per_step": count * R * 32 + 16,
+                    "encode_ms_per_image": float(e2e_s.item()) / e2e_steps * 1e3 / count,
+                    "api": "paper_1404_0774_b200.encode_batch (C-ABI fic_encode_batch)" if volume else
+                           "paper_1404_0774_b200.encode (C-ABI fic_encode)"},
             "roofline": {"bound": "tensor", "kernel": "scan_kernel (full level: all R x D x 8 correlations)",
                          "achieved": achieved, "peak": bf16,
                          "unit": "TFLOP/s", "frac": (achieved / bf16) if achieved else None,
                          "peak_source": f"{src} dense bf16 burst (the scan issues kind::f16 MMAs at the bf16 rate)",
                          "frac_of_int8_peak": (achieved / (2 * bf16)) if achieved else None,
                          "kernel_ms": scan_ms, "kernel_launches_timed": scan_n,
+                         "kernel_launches_per_step": scan_launches_per_step,
                          "ops_per_comparison": 2 * n * n, "comparisons_per_launch": nominal,
                          "traffic": traffic_for(args.config),
                          "matcher_ms": matcher_ms, "matcher_tflops": matcher_tflops,
@@ -329,7 +359,8 @@ def run_ours(args):
         }
         if args.cpu_baseline:
             threads = os.cpu_count() or 1
-            c_comps, c_dt, used, RR = cpu_reference_sample(img, n, step, args.ref_ranges, threads)
+            c_comps, c_dt, used, RR = cpu_reference_sample(img[0] if volume else img, n, step, args.ref_ranges,
+                                                           threads)
             line["cpu_baseline"] = {
                 "value": c_comps / c_dt, "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": f"{used} of {RR} ranges (evenly strided) via the reference encode_range, {threads} threads",
@@ -349,6 +380,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIG_TEXT))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-ranges", type=int, default=1024, help="ranges per CPU-reference sample")
+    ap.add_argument("--slices", type=int, default=512, help="cfg5: slices in the volume (sharded over ranks)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":

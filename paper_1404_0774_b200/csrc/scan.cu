@@ -42,7 +42,10 @@ constexpr int kScanRanges = kScanRows / kSyms;  // 32
 constexpr int kPoolBlock = 128;                 // domains per pool-builder CTA (pool padding)
 constexpr int kScanTileDom = 128;               // domains per pool tile (MMA M = TMEM lanes)
 constexpr int kScanMaxStages = 16;
-constexpr int kScanEpiWarps = 8;
+constexpr int kScanEpiWarps = 16;                       // 4 lane quarters x kEpiParts column parts
+constexpr int kEpiParts = kScanEpiWarps / 4;
+constexpr int kEpiRanges = kScanRanges / kEpiParts;    // ranges per epilogue thread
+constexpr int kEpiCols = kEpiRanges * kSyms;           // TMEM columns per epilogue thread
 constexpr int kScanThreads = (2 + kScanEpiWarps) * 32;
 constexpr uint32_t kScanTmemCols = 512;
 constexpr int kWarpBuf = 64;                    // survivor staging entries per epilogue warp
@@ -688,11 +691,11 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 //   warp 1        TMEM allocation; lane 0: MMA issuer, K/16 x tcgen05.mma M=128 (domains) x
 //                 N=256 (32 ranges x 8 isometries) x K=16 per tile into one of two 256-column
 //                 TMEM accumulators
-//   warps 2-9     epilogue: 8 warps (lane quarter x column half); for every tile a thread owns
-//                 one domain (TMEM lane) and 16 ranges x 8 isometries (128 columns, scaled so
-//                 the pruning test is |X~/T_r| > 1 for every column)
-//                 (128 columns), tests each range's 8-isometry |max| against the range's
-//                 threshold and appends the rare columns above it to the survivor list
+//   warps 2-17    epilogue: 16 warps (lane quarter x column part); for every tile a thread owns
+//                 one domain (TMEM lane) and kEpiRanges ranges x 8 isometries (kEpiCols columns,
+//                 scaled so the pruning test is |X~/T_r| > 1 for every column), tests each
+//                 range's 8-isometry |max| against 1 and appends the rare columns above it to
+//                 the survivor list
 __global__ void __launch_bounds__(kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
             const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
@@ -796,18 +799,18 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   } else {
     // ================= epilogue =================
     const int e = warp - 2;
-    const int half = e >> 2;        // column half: ranges half*16 .. half*16+15 of the m-tile
+    const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
     WarpAppender app{list, count, (uint32_t)cap, 0u, 0u};
-    const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + half * 128;
+    const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + part * kEpiCols;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const Segment S = seg_at(lv, cta, G, sg);
-      const int r0 = S.m * kScanRanges + half * 16;  // this thread's 16 ranges
+      const int r0 = S.m * kScanRanges + part * kEpiRanges;  // this thread's ranges
       const uint32_t dslice = (uint32_t)(range_slice(g, r0) * g.Dt);  // pool index of the slice's domain 0
       uint32_t allpass = 0;                          // ranges without a usable threshold
 #pragma unroll
-      for (int k = 0; k < 16; k += 4) {
+      for (int k = 0; k < kEpiRanges; k += 4) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(thr + r0 + k));
         allpass |= (uint32_t)range_allpass(t.x) << k | (uint32_t)range_allpass(t.y) << (k + 1) |
                    (uint32_t)range_allpass(t.z) << (k + 2) | (uint32_t)range_allpass(t.w) << (k + 3);
@@ -824,21 +827,19 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           continue;
         }
         const uint32_t ta = tcol + buf * kScanRows;
-        uint32_t v[128];
+        uint32_t v[kEpiCols];
         __syncwarp();
-        ptx::tmem_ld_32x32b_x32(ta, v);
-        ptx::tmem_ld_32x32b_x32(ta + 32, v + 32);
-        ptx::tmem_ld_32x32b_x32(ta + 64, v + 64);
-        ptx::tmem_ld_32x32b_x32(ta + 96, v + 96);
+#pragma unroll
+        for (int c = 0; c < kEpiCols; c += 32) ptx::tmem_ld_32x32b_x32(ta + c, v + c);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all 128 columns read: release the buffer
+        if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
         if (g.flags & 8) continue;                          // debug: skip the test
         // |max| of each range's 8 isometry columns (4 FMNMX3 each); mask of ranges above 1
         uint32_t gmask = allpass;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < kEpiRanges; ++k) {
           const float* f = reinterpret_cast<const float*>(v + 8 * k);
           const float gm = fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
                                        fmaxf(fabsf(f[4]), fabsf(f[5]))),
@@ -854,7 +855,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
 #define FIC_GROUP_BITS(K)                                                                       \
   case K:                                                                                       \
     _Pragma("unroll") for (int c = 0; c < 8; ++c) bits |=                                       \
-        (uint32_t)(fabsf(__uint_as_float(v[8 * K + c])) > 1.0f) << c;                           \
+        (uint32_t)(fabsf(__uint_as_float(v[(8 * K + c) % kEpiCols])) > 1.0f) << c;             \
     break;
             FIC_GROUP_BITS(0) FIC_GROUP_BITS(1) FIC_GROUP_BITS(2) FIC_GROUP_BITS(3)
             FIC_GROUP_BITS(4) FIC_GROUP_BITS(5) FIC_GROUP_BITS(6) FIC_GROUP_BITS(7)
