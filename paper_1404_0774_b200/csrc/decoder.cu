@@ -8,6 +8,8 @@
 // sums the partials in a fixed order (deterministic run to run; the reference's
 // sequential sum order is not reproduced, so step_rmse agrees to ~1e-15 relative,
 // while every raster value is bit-exact).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ficb {
@@ -74,6 +76,121 @@ decode_step_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
   }
 }
 
+// Tiled variant of decode_step_kernel for the common geometries (kn a multiple of 32, or a
+// divisor of 32 with the raster a whole number of 32 x 32 tiles).  One CTA per 32 x 32 output
+// tile, i.e. (32/T)^2 blocks of T x T output pixels (T = min(kn, 32)), each block the whole
+// range (kn <= 32) or a sub-square of one (kn > 32).  An isometry maps an aligned T x T
+// sub-square of the range onto an aligned T x T sub-square of its source, so phase 1 loads
+// the 2T x 2T source windows of the tile's blocks row by row (coalesced for every isometry)
+// and forms their 2x2 means z in shared memory; phase 2 writes the tile's outputs
+// row-coalesced, reading z through the isometry (the transposing isometries, half of them,
+// no longer turn every warp's gather into 32 separate raster rows).  Same per-pixel
+// arithmetic as decode_step_kernel, so the rasters are bit-identical.
+constexpr int kTile = 32;
+constexpr int kTileThreads = 256;
+
+bool decode_tiled(int out_w, int kn) {
+  if (out_w % kTile != 0) return false;
+  return kn >= kTile ? kn % kTile == 0 : (kTile % kn == 0 && kn >= 2);
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+decode_tile_kernel(const double* __restrict__ cur, double* __restrict__ nxt, const RangeXform* __restrict__ xf,
+                   int out_w, int kn, int ranges_x, double* __restrict__ partial) {
+  __shared__ double zs[kTile][kTile + 1];
+  struct Blk {
+    double s, o;
+    int row0, col0;  // raster origin of the block's source window (2T x 2T)
+    int sym, sr0, sc0;
+  };
+  __shared__ Blk blk[(kTile / 2) * (kTile / 2)];
+  const int T = kn < kTile ? kn : kTile;
+  const int bpr = kTile / T;  // blocks per tile row
+  const int tiles_x = out_w / kTile;
+  const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
+  const int Y0 = ty * kTile, X0 = tx * kTile;
+  for (int b = threadIdx.x; b < bpr * bpr; b += kTileThreads) {
+    const int bi = b / bpr, bj = b % bpr;
+    const int Yb = Y0 + bi * T, Xb = X0 + bj * T;  // the block's first output pixel
+    const int ry = Yb / kn, rx = Xb / kn;
+    const int a = Yb - ry * kn, c = Xb - rx * kn;  // its offset inside the range
+    const RangeXform t = xf[ry * ranges_x + rx];
+    int r0, c0, r1, c1;
+    symmetry_source(t.sym, a, c, kn, r0, c0);
+    symmetry_source(t.sym, a + T - 1, c + T - 1, kn, r1, c1);
+    Blk B;
+    B.s = t.s;
+    B.o = t.o;
+    B.sym = t.sym;
+    B.sr0 = min(r0, r1);
+    B.sc0 = min(c0, c1);
+    B.row0 = t.dy + 2 * B.sr0;
+    B.col0 = t.dx + 2 * B.sc0;
+    blk[b] = B;
+  }
+  __syncthreads();
+  // phase 1: z of every block's source sub-square, stored at the block's place in the tile
+  // (all 16 loads of a thread issued before the first use)
+  constexpr int kPer = kTile * kTile / kTileThreads;
+  double p[kPer][4];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTileThreads;
+    const int zr = e / kTile, zc = e % kTile;
+    const Blk& B = blk[(zr / T) * bpr + zc / T];
+    const double* row0 = cur + (long long)(B.row0 + 2 * (zr % T)) * out_w + B.col0 + 2 * (zc % T);
+    p[k][0] = __ldg(row0);
+    p[k][1] = __ldg(row0 + 1);
+    p[k][2] = __ldg(row0 + out_w);
+    p[k][3] = __ldg(row0 + out_w + 1);
+  }
+  double cv[kPer];  // the tile's own current values, for the step RMSE
+  if (partial) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = threadIdx.x + k * kTileThreads;
+      cv[k] = __ldg(cur + (long long)(Y0 + e / kTile) * out_w + X0 + e % kTile);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTileThreads;
+    zs[e / kTile][e % kTile] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(p[k][0], p[k][1]), p[k][2]), p[k][3]), 0.25);
+  }
+  __syncthreads();
+  // phase 2: outputs, row-coalesced.  The next raster is written with evict-first stores so
+  // the current one (re-read by the overlapping domain windows) keeps the L2.
+  double sq = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTileThreads;
+    const int orow = e / kTile, ocol = e % kTile;
+    const int bi = orow / T, bj = ocol / T;
+    const Blk& B = blk[bi * bpr + bj];
+    const int Y = Y0 + orow, X = X0 + ocol;
+    int sr, sc;
+    symmetry_source(B.sym, Y % kn, X % kn, kn, sr, sc);
+    const double z = zs[bi * T + sr - B.sr0][bj * T + sc - B.sc0];
+    const double v = __dadd_rn(__dmul_rn(B.s, z), B.o);
+    __stcs(nxt + (long long)Y * out_w + X, v);
+    if (partial) {
+      const double dlt = __dsub_rn(cv[k], v);
+      sq = __dadd_rn(sq, __dmul_rn(dlt, dlt));
+    }
+  }
+  if (partial) {
+    __shared__ double red[kTileThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kTileThreads / 32; ++w) s = __dadd_rn(s, red[w]);
+      partial[blockIdx.x] = s;
+    }
+  }
+}
+
 // Sums the per-block partials in index order and writes rmse = sqrt(sum / count).
 __global__ void rmse_finish_kernel(const double* __restrict__ partial, int blocks, long long count,
                                    double* __restrict__ out) {
@@ -107,7 +224,7 @@ int decode_blocks(long long count) { return (int)((count + kDecodeThreads - 1) /
 
 // Partials one decode step writes.
 int decode_partials(int out_w, int kn) {
-  (void)kn;
+  if (decode_tiled(out_w, kn) && !std::getenv("FIC_DECODE_FLAT")) return (out_w / kTile) * (out_w / kTile);
   return decode_blocks((long long)out_w * out_w);
 }
 
@@ -118,6 +235,11 @@ void launch_xform(const fic_mapping* maps, int count, int scale, const Geometry&
 void launch_decode_step(const double* cur, double* nxt, const RangeXform* xf, int out_w, int kn, int ranges_x,
                         double* partial, cudaStream_t st) {
   const long long count = (long long)out_w * out_w;
+  if (decode_tiled(out_w, kn) && !std::getenv("FIC_DECODE_FLAT")) {
+    decode_tile_kernel<<<(out_w / kTile) * (out_w / kTile), kTileThreads, 0, st>>>(cur, nxt, xf, out_w, kn, ranges_x,
+                                                                                   partial);
+    return;
+  }
   decode_step_kernel<<<decode_blocks(count), kDecodeThreads, 0, st>>>(cur, nxt, xf, out_w, kn, ranges_x, partial);
 }
 

@@ -98,3 +98,37 @@ def test_decode_errors():
         fic.collage_error(np.zeros((32, 32), np.uint8), enc)
     with pytest.raises(fic.CodecError, match="NonContractive"):
         fic.decoded_error_bound(1.0, 1.0)
+
+
+def _random_maps(W, n, step, seed):
+    """Random but valid code records (every isometry, codes across their range)."""
+    from paper_1404_0774_b200.abi import MAPPING_DTYPE
+    rng = np.random.default_rng(seed)
+    R = (W // n) ** 2
+    P = (W - 2 * n) // step + 1
+    m = np.zeros(R, MAPPING_DTYPE)
+    m["x"] = rng.integers(0, P, R) * step
+    m["y"] = rng.integers(0, P, R) * step
+    m["sym"] = np.arange(R) % 8
+    m["qs"] = rng.integers(0, 32, R)
+    m["qo"] = rng.integers(0, 128, R)
+    return m
+
+
+# (image side, n, step, scale): kn = n * scale covers the tiled decoder (kn a multiple of 32,
+# or a divisor of 32) and the per-pixel kernel (kn = 40, 24)
+@pytest.mark.parametrize("W,n,step,scale", [(32, 8, 4, 4), (32, 8, 2, 8), (64, 4, 2, 16), (32, 2, 1, 1),
+                                            (64, 8, 8, 1), (32, 8, 4, 5), (32, 8, 4, 3), (16, 4, 1, 8)])
+def test_decode_step_tiled_geometries(oracle, W, n, step, scale):
+    maps = _random_maps(W, n, step, W * 1000 + n * 10 + scale)
+    pv = dict(n=n, step=step)
+    enc = fic.EncodedImage(W, W, fic.CodecParams(**pv), maps)
+    rng = np.random.default_rng(scale)
+    cur = rng.uniform(-20, 300, size=(W * scale, W * scale))
+    got = fic.decode_step(cur, enc, scale)
+    want = oracle.decode_step(cur, maps, W, pv, scale)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    out, rm, runs = fic.decode_traced(enc, scale=scale, iterations=3, initial="mid-gray")
+    wout, wrm, _ = oracle.decode(maps, W, pv, scale, 3)
+    assert np.array_equal(out, wout)
+    np.testing.assert_allclose(rm, wrm, rtol=1e-12, atol=1e-300)
