@@ -191,6 +191,138 @@ decode_tile_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
   }
 }
 
+// ------------------------------------------------------------------ mean-raster decoder
+// Every 2x2 mean the decoder reads, z = ((p00 + p01) + p10 + p11) / 4 at (dy + 2 sr, dx + 2 sc),
+// lies on the even grid whenever the magnified domain origins (multiples of step * scale) are
+// even.  Then an iteration needs only the half-resolution MEAN raster m(i, j) = z at
+// (2i, 2j) of the current raster (a quarter of its size, L2-resident up to 8192^2 outputs),
+// and each output tile, being 32 x 32 at even coordinates, yields the next iteration's means
+// of its own outputs.  Per iteration the full raster is written once and read once (the
+// step RMSE's current values), instead of gathering four doubles per output pixel.  Same
+// per-value arithmetic in the same order, so every raster value is bit-identical.
+bool decode_mean_ok(int out_w, int kn, int step_scale) { return decode_tiled(out_w, kn) && step_scale % 2 == 0; }
+
+__global__ void mean_raster_kernel(const double* __restrict__ r, double* __restrict__ m, int out_w) {
+  const int hw = out_w / 2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)hw * hw) return;
+  const int y = (int)(i / hw), x = (int)(i % hw);
+  const double* p = r + (long long)(2 * y) * out_w + 2 * x;
+  m[i] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), p[out_w]), p[out_w + 1]), 0.25);
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mcur, double* __restrict__ nxt,
+                   double* __restrict__ mnxt, const RangeXform* __restrict__ xf, int out_w, int kn, int ranges_x,
+                   double* __restrict__ partial) {
+  __shared__ double zs[kTile][kTile + 1];
+  __shared__ double vs[kTile][kTile + 1];
+  struct Blk {
+    double s, o;
+    int mrow0, mcol0;  // mean-raster origin of the block's source sub-square (T x T)
+    int sym, sr0, sc0;
+  };
+  __shared__ Blk blk[(kTile / 2) * (kTile / 2)];
+  const int T = kn < kTile ? kn : kTile;
+  const int bpr = kTile / T;
+  const int tiles_x = out_w / kTile, hw = out_w / 2;
+  const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
+  const int Y0 = ty * kTile, X0 = tx * kTile;
+  constexpr int kPer = kTile * kTile / kTileThreads;
+  double zv[kPer], cv[kPer];
+  // the tile's current values (step RMSE) first: they depend on nothing, so their DRAM reads
+  // overlap the code-record load and the block setup
+  if (partial) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = threadIdx.x + k * kTileThreads;
+      cv[k] = __ldcs(cur + (long long)(Y0 + e / kTile) * out_w + X0 + e % kTile);
+    }
+  }
+  for (int b = threadIdx.x; b < bpr * bpr; b += kTileThreads) {
+    const int bi = b / bpr, bj = b % bpr;
+    const int Yb = Y0 + bi * T, Xb = X0 + bj * T;
+    const int ry = Yb / kn, rx = Xb / kn;
+    const int a = Yb - ry * kn, c = Xb - rx * kn;
+    const RangeXform t = xf[ry * ranges_x + rx];
+    int r0, c0, r1, c1;
+    symmetry_source(t.sym, a, c, kn, r0, c0);
+    symmetry_source(t.sym, a + T - 1, c + T - 1, kn, r1, c1);
+    Blk B;
+    B.s = t.s;
+    B.o = t.o;
+    B.sym = t.sym;
+    B.sr0 = min(r0, r1);
+    B.sc0 = min(c0, c1);
+    B.mrow0 = t.dy / 2 + B.sr0;
+    B.mcol0 = t.dx / 2 + B.sc0;
+    blk[b] = B;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTileThreads;
+    const int zr = e / kTile, zc = e % kTile;
+    const Blk& B = blk[(zr / T) * bpr + zc / T];
+    zv[k] = __ldg(mcur + (long long)(B.mrow0 + zr % T) * hw + B.mcol0 + zc % T);
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTileThreads;
+    zs[e / kTile][e % kTile] = zv[k];
+  }
+  __syncthreads();
+  double sq = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTileThreads;
+    const int orow = e / kTile, ocol = e % kTile;
+    const int bi = orow / T, bj = ocol / T;
+    const Blk& B = blk[bi * bpr + bj];
+    const int Y = Y0 + orow, X = X0 + ocol;
+    int sr, sc;
+    symmetry_source(B.sym, Y % kn, X % kn, kn, sr, sc);
+    const double v = __dadd_rn(__dmul_rn(B.s, zs[bi * T + sr - B.sr0][bj * T + sc - B.sc0]), B.o);
+    __stcs(nxt + (long long)Y * out_w + X, v);
+    vs[orow][ocol] = v;
+    if (partial) {
+      const double dlt = __dsub_rn(cv[k], v);
+      sq = __dadd_rn(sq, __dmul_rn(dlt, dlt));
+    }
+  }
+  __syncthreads();
+  {  // the next iteration's means of this tile's outputs: 16 x 16, one per thread
+    const int i = threadIdx.x / (kTile / 2), j = threadIdx.x % (kTile / 2);
+    const double m = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dadd_rn(vs[2 * i][2 * j], vs[2 * i][2 * j + 1]), vs[2 * i + 1][2 * j]), vs[2 * i + 1][2 * j + 1]),
+        0.25);
+    mnxt[(long long)(Y0 / 2 + i) * hw + X0 / 2 + j] = m;
+  }
+  if (partial) {
+    __shared__ double red[kTileThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kTileThreads / 32; ++w) t = __dadd_rn(t, red[w]);
+      partial[blockIdx.x] = t;
+    }
+  }
+}
+
+void launch_mean_raster(const double* r, double* m, int out_w, cudaStream_t st) {
+  const long long n = (long long)(out_w / 2) * (out_w / 2);
+  mean_raster_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(r, m, out_w);
+}
+
+// One iteration on the mean raster (decode_mean_ok); partials as decode_partials.
+void launch_decode_mean(const double* cur, const double* mcur, double* nxt, double* mnxt, const RangeXform* xf,
+                        int out_w, int kn, int ranges_x, double* partial, cudaStream_t st) {
+  decode_mean_kernel<<<(out_w / kTile) * (out_w / kTile), kTileThreads, 0, st>>>(cur, mcur, nxt, mnxt, xf, out_w, kn,
+                                                                                 ranges_x, partial);
+}
+
 // Sums the per-block partials in index order and writes rmse = sqrt(sum / count).
 __global__ void rmse_finish_kernel(const double* __restrict__ partial, int blocks, long long count,
                                    double* __restrict__ out) {

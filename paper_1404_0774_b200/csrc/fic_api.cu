@@ -41,6 +41,10 @@ int decode_partials(int, int);
 void launch_xform(const fic_mapping*, int, int, const Geometry&, RangeXform*, cudaStream_t);
 void launch_decode_step(const double*, double*, const RangeXform*, int, int, int, double*, cudaStream_t);
 void launch_rmse_finish(const double*, int, long long, double*, cudaStream_t);
+bool decode_mean_ok(int, int, int);
+void launch_mean_raster(const double*, double*, int, cudaStream_t);
+void launch_decode_mean(const double*, const double*, double*, double*, const RangeXform*, int, int, int, double*,
+                        cudaStream_t);
 void launch_raster_init(double*, long long, int, const unsigned char*, cudaStream_t);
 void launch_quantize_raster(const double*, long long, unsigned char*, cudaStream_t);
 // scan.cu (tcgen05 path, n in {2, 4, 8})
@@ -220,7 +224,7 @@ struct Workspace {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   bool scan_timed = false;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag, scratch, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
+      diag, scratch, mra, mrb, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
   unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
   unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
@@ -879,8 +883,24 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
     const bool timed = g_timing.load() != 0 && !has_eps;
     if (timed) CK(cudaEventRecord(ws.ev0, ws.stream));
     int runs = 0;
+    // mean-raster iterations when every 2x2 mean lies on the even grid (decoder.cu)
+    const int kn = p.n * scale;
+    const bool mean = decode_mean_ok(out_w, kn, p.step * scale) && !std::getenv("FIC_DECODE_FLAT") &&
+                      !std::getenv("FIC_DECODE_TILE");
+    double *ma = nullptr, *mb = nullptr;
+    if (mean) {
+      ma = static_cast<double*>(ws.mra.get((size_t)cnt / 4 * 8));
+      mb = static_cast<double*>(ws.mrb.get((size_t)cnt / 4 * 8));
+      launch_mean_raster(a, ma, out_w, ws.stream);
+      g_launches += 1;
+    }
     for (int it = 0; it < iterations; ++it) {
-      launch_decode_step(a, b, xf, out_w, p.n * scale, g.RX, part, ws.stream);
+      if (mean) {
+        launch_decode_mean(a, ma, b, mb, xf, out_w, kn, g.RX, part, ws.stream);
+        std::swap(ma, mb);
+      } else {
+        launch_decode_step(a, b, xf, out_w, kn, g.RX, part, ws.stream);
+      }
       launch_rmse_finish(part, decode_partials(out_w, p.n * scale), cnt, d_rmse + it, ws.stream);
       g_launches += 2;
       std::swap(a, b);

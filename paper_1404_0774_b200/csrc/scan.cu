@@ -819,7 +819,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       for (int j = S.j0; j < S.j1; ++j, ++i) {
         const int buf = i & 1;
         const uint32_t d = dslice + (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
-        ptx::mbar_wait(&tfull_bar[buf], (i >> 1) & 1);
+        ptx::mbar_wait_sleep(&tfull_bar[buf], (i >> 1) & 1);
         ptx::tc_fence_after();
         if (g.flags & 128) {  // debug: no TMEM reads at all (MMA + producer throughput)
           __syncwarp();
@@ -846,26 +846,20 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                                  fmaxf(fabsf(f[6]), fabsf(f[7])));
           gmask |= (uint32_t)(gm > 1.0f) << k;
         }
-        uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
-        while (groups) {  // ranges with a hit in some lane of the warp
-          const int k = __ffs(groups) - 1;
-          groups &= groups - 1;
-          uint32_t bits = 0;
-          switch (k) {  // static register indices per case
-#define FIC_GROUP_BITS(K)                                                                       \
-  case K:                                                                                       \
-    _Pragma("unroll") for (int c = 0; c < 8; ++c) bits |=                                       \
-        (uint32_t)(fabsf(__uint_as_float(v[(8 * K + c) % kEpiCols])) > 1.0f) << c;             \
-    break;
-            FIC_GROUP_BITS(0) FIC_GROUP_BITS(1) FIC_GROUP_BITS(2) FIC_GROUP_BITS(3)
-            FIC_GROUP_BITS(4) FIC_GROUP_BITS(5) FIC_GROUP_BITS(6) FIC_GROUP_BITS(7)
-            FIC_GROUP_BITS(8) FIC_GROUP_BITS(9) FIC_GROUP_BITS(10) FIC_GROUP_BITS(11)
-            FIC_GROUP_BITS(12) FIC_GROUP_BITS(13) FIC_GROUP_BITS(14) FIC_GROUP_BITS(15)
-#undef FIC_GROUP_BITS
-            default: break;
+        const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+        if (groups) {
+          // ranges with a hit in some lane of the warp, one warp-uniform branch per range, so
+          // only the hit ranges' column bits are formed (8 compares each)
+#pragma unroll
+          for (int k = 0; k < kEpiRanges; ++k) {
+            if ((groups >> k) & 1u) {
+              uint32_t bits = 0;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
+              if ((allpass >> k) & 1u) bits = 0xFFu;
+              app.bits(bits, rowbase + 8u * (uint32_t)k, d);
+            }
           }
-          if ((allpass >> k) & 1u) bits = 0xFFu;
-          app.bits(bits, rowbase + 8u * (uint32_t)k, d);
         }
       }
     }

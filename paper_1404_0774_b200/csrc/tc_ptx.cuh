@@ -44,6 +44,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// mbar_wait with a suspend-time hint: a waiting thread is parked until the phase completes
+// (or the hint expires) instead of re-polling, so warps that wait a long time (the scan's
+// epilogue between tiles) stop taking issue slots from the warps that are working.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
 // 1-D bulk copy global -> shared, completion counted on `bar` (UBLKCP in SASS).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

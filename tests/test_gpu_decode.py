@@ -118,7 +118,8 @@ def _random_maps(W, n, step, seed):
 # (image side, n, step, scale): kn = n * scale covers the tiled decoder (kn a multiple of 32,
 # or a divisor of 32) and the per-pixel kernel (kn = 40, 24)
 @pytest.mark.parametrize("W,n,step,scale", [(32, 8, 4, 4), (32, 8, 2, 8), (64, 4, 2, 16), (32, 2, 1, 1),
-                                            (64, 8, 8, 1), (32, 8, 4, 5), (32, 8, 4, 3), (16, 4, 1, 8)])
+                                            (64, 8, 8, 1), (32, 8, 4, 5), (32, 8, 4, 3), (16, 4, 1, 8),
+                                            (64, 4, 3, 1), (32, 4, 1, 2)])
 def test_decode_step_tiled_geometries(oracle, W, n, step, scale):
     maps = _random_maps(W, n, step, W * 1000 + n * 10 + scale)
     pv = dict(n=n, step=step)
