@@ -211,10 +211,16 @@ __global__ void mean_raster_kernel(const double* __restrict__ r, double* __restr
   m[i] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), p[out_w]), p[out_w + 1]), 0.25);
 }
 
+// LT = log2 of the block side T: 5 = the tile lies inside one range (kn a multiple of 32), else
+// T = kn = 2^LT < 32 and the tile holds (32/T)^2 whole ranges.  Index arithmetic is shifts and
+// masks (the kernel is issue-bound otherwise: per-pixel divisions by kn).
+template <int LT>
 __global__ void __launch_bounds__(kTileThreads)
 decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mcur, double* __restrict__ nxt,
                    double* __restrict__ mnxt, const RangeXform* __restrict__ xf, int out_w, int kn, int ranges_x,
                    double* __restrict__ partial) {
+  constexpr bool kWhole = LT == 5;
+  constexpr int T = 1 << LT, bpr = kTile / T, nb = bpr * bpr;
   __shared__ double zs[kTile][kTile + 1];
   __shared__ double vs[kTile][kTile + 1];
   struct Blk {
@@ -222,68 +228,87 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     int mrow0, mcol0;  // mean-raster origin of the block's source sub-square (T x T)
     int sym, sr0, sc0;
   };
-  __shared__ Blk blk[(kTile / 2) * (kTile / 2)];
-  const int T = kn < kTile ? kn : kTile;
-  const int bpr = kTile / T;
+  __shared__ Blk blk[kWhole ? 1 : nb];
   const int tiles_x = out_w / kTile, hw = out_w / 2;
   const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
   const int Y0 = ty * kTile, X0 = tx * kTile;
+  const int lane_c = threadIdx.x & (kTile - 1), row0 = threadIdx.x >> 5;  // element e = threadIdx.x + 256 k
   constexpr int kPer = kTile * kTile / kTileThreads;
+  constexpr int kRowStep = kTileThreads / kTile;
   double zv[kPer], cv[kPer];
   // the tile's current values (step RMSE) first: they depend on nothing, so their DRAM reads
   // overlap the code-record load and the block setup
   if (partial) {
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = threadIdx.x + k * kTileThreads;
-      cv[k] = __ldcs(cur + (long long)(Y0 + e / kTile) * out_w + X0 + e % kTile);
-    }
+    for (int k = 0; k < kPer; ++k)
+      cv[k] = __ldcs(cur + (long long)(Y0 + row0 + k * kRowStep) * out_w + X0 + lane_c);
   }
-  for (int b = threadIdx.x; b < bpr * bpr; b += kTileThreads) {
-    const int bi = b / bpr, bj = b % bpr;
-    const int Yb = Y0 + bi * T, Xb = X0 + bj * T;
-    const int ry = Yb / kn, rx = Xb / kn;
-    const int a = Yb - ry * kn, c = Xb - rx * kn;
+  Blk B;     // kWhole: the tile's one block, computed by every thread (broadcast load, no sync)
+  int a0 = 0, c0 = 0;  // kWhole: the tile's offset inside its range
+  if (kWhole) {
+    const int ry = Y0 / kn, rx = X0 / kn;
+    a0 = Y0 - ry * kn;
+    c0 = X0 - rx * kn;
     const RangeXform t = xf[ry * ranges_x + rx];
-    int r0, c0, r1, c1;
-    symmetry_source(t.sym, a, c, kn, r0, c0);
-    symmetry_source(t.sym, a + T - 1, c + T - 1, kn, r1, c1);
-    Blk B;
+    int r0, cc0, r1, c1;
+    symmetry_source(t.sym, a0, c0, kn, r0, cc0);
+    symmetry_source(t.sym, a0 + T - 1, c0 + T - 1, kn, r1, c1);
     B.s = t.s;
     B.o = t.o;
     B.sym = t.sym;
     B.sr0 = min(r0, r1);
-    B.sc0 = min(c0, c1);
+    B.sc0 = min(cc0, c1);
     B.mrow0 = t.dy / 2 + B.sr0;
     B.mcol0 = t.dx / 2 + B.sc0;
-    blk[b] = B;
-  }
-  __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int e = threadIdx.x + k * kTileThreads;
-    const int zr = e / kTile, zc = e % kTile;
-    const Blk& B = blk[(zr / T) * bpr + zc / T];
-    zv[k] = __ldg(mcur + (long long)(B.mrow0 + zr % T) * hw + B.mcol0 + zc % T);
+    for (int k = 0; k < kPer; ++k)
+      zv[k] = __ldg(mcur + (long long)(B.mrow0 + row0 + k * kRowStep) * hw + B.mcol0 + lane_c);
+  } else {
+    for (int b = threadIdx.x; b < nb; b += kTileThreads) {
+      const int ry = (Y0 >> LT) + b / bpr, rx = (X0 >> LT) + b % bpr;
+      const RangeXform t = xf[ry * ranges_x + rx];
+      Blk Q;
+      Q.s = t.s;
+      Q.o = t.o;
+      Q.sym = t.sym;
+      Q.sr0 = Q.sc0 = 0;
+      Q.mrow0 = t.dy / 2;
+      Q.mcol0 = t.dx / 2;
+      blk[b] = Q;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int zr = row0 + k * kRowStep, zc = lane_c;
+      const Blk& Q = blk[(zr >> LT) * bpr + (zc >> LT)];
+      zv[k] = __ldg(mcur + (long long)(Q.mrow0 + (zr & (T - 1))) * hw + Q.mcol0 + (zc & (T - 1)));
+    }
   }
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int e = threadIdx.x + k * kTileThreads;
-    zs[e / kTile][e % kTile] = zv[k];
-  }
+  for (int k = 0; k < kPer; ++k) zs[row0 + k * kRowStep][lane_c] = zv[k];
   __syncthreads();
   double sq = 0.0;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
-    const int e = threadIdx.x + k * kTileThreads;
-    const int orow = e / kTile, ocol = e % kTile;
-    const int bi = orow / T, bj = ocol / T;
-    const Blk& B = blk[bi * bpr + bj];
-    const int Y = Y0 + orow, X = X0 + ocol;
-    int sr, sc;
-    symmetry_source(B.sym, Y % kn, X % kn, kn, sr, sc);
-    const double v = __dadd_rn(__dmul_rn(B.s, zs[bi * T + sr - B.sr0][bj * T + sc - B.sc0]), B.o);
-    __stcs(nxt + (long long)Y * out_w + X, v);
+    const int orow = row0 + k * kRowStep, ocol = lane_c;
+    double z, s, o;
+    if (kWhole) {
+      int sr, sc;
+      symmetry_source(B.sym, a0 + orow, c0 + ocol, kn, sr, sc);
+      z = zs[sr - B.sr0][sc - B.sc0];
+      s = B.s;
+      o = B.o;
+    } else {
+      const int bi = orow >> LT, bj = ocol >> LT;
+      const Blk& Q = blk[bi * bpr + bj];
+      int sr, sc;
+      symmetry_source(Q.sym, orow & (T - 1), ocol & (T - 1), T, sr, sc);
+      z = zs[(bi << LT) + sr][(bj << LT) + sc];
+      s = Q.s;
+      o = Q.o;
+    }
+    const double v = __dadd_rn(__dmul_rn(s, z), o);
+    __stcs(nxt + (long long)(Y0 + orow) * out_w + X0 + ocol, v);
     vs[orow][ocol] = v;
     if (partial) {
       const double dlt = __dsub_rn(cv[k], v);
@@ -292,7 +317,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
   }
   __syncthreads();
   {  // the next iteration's means of this tile's outputs: 16 x 16, one per thread
-    const int i = threadIdx.x / (kTile / 2), j = threadIdx.x % (kTile / 2);
+    const int i = threadIdx.x >> 4, j = threadIdx.x & 15;
     const double m = __dmul_rn(
         __dadd_rn(__dadd_rn(__dadd_rn(vs[2 * i][2 * j], vs[2 * i][2 * j + 1]), vs[2 * i + 1][2 * j]), vs[2 * i + 1][2 * j + 1]),
         0.25);
@@ -300,7 +325,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
   }
   if (partial) {
     __shared__ double red[kTileThreads / 32];
-    for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+    for (int off = 16; off > 0; off >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -319,8 +344,16 @@ void launch_mean_raster(const double* r, double* m, int out_w, cudaStream_t st) 
 // One iteration on the mean raster (decode_mean_ok); partials as decode_partials.
 void launch_decode_mean(const double* cur, const double* mcur, double* nxt, double* mnxt, const RangeXform* xf,
                         int out_w, int kn, int ranges_x, double* partial, cudaStream_t st) {
-  decode_mean_kernel<<<(out_w / kTile) * (out_w / kTile), kTileThreads, 0, st>>>(cur, mcur, nxt, mnxt, xf, out_w, kn,
-                                                                                 ranges_x, partial);
+  const int grid = (out_w / kTile) * (out_w / kTile);
+#define FIC_MEAN(LT) decode_mean_kernel<LT><<<grid, kTileThreads, 0, st>>>(cur, mcur, nxt, mnxt, xf, out_w, kn, ranges_x, partial)
+  switch (kn >= kTile ? 5 : __builtin_ctz((unsigned)kn)) {
+    case 1: FIC_MEAN(1); break;
+    case 2: FIC_MEAN(2); break;
+    case 3: FIC_MEAN(3); break;
+    case 4: FIC_MEAN(4); break;
+    default: FIC_MEAN(5); break;
+  }
+#undef FIC_MEAN
 }
 
 // Sums the per-block partials in index order and writes rmse = sqrt(sum / count).

@@ -60,8 +60,9 @@ size_t deq_table_entries(const Geometry&);
 void launch_deq_tables(const Geometry&, double*, cudaStream_t);
 int scan_grid(const Geometry&, int, int);
 cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const __half*, const RangeMeta*,
-                        const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long,
-                        cudaStream_t);
+                        const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long, void*,
+                        unsigned long long*, cudaStream_t);
+size_t scan_rec_bytes(unsigned long long, int);
 int scan_padded_ranges(const Geometry&);
 bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
@@ -224,7 +225,7 @@ struct Workspace {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   bool scan_timed = false;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag, scratch, mra, mrb, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
+      diag, scratch, mra, mrb, recs, rcounts, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
   unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
   unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
@@ -355,14 +356,16 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   if (!scan_pair_mode() || stride == first_stride) launch_range_op(d_img, g, b.rm, b.thr, b.ropnd, st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
-  CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, st));
+  void* recs = ws.recs.get(scan_rec_bytes(ws.list_cap, parts));
+  auto* rcnt = static_cast<unsigned long long*>(ws.rcounts.get(kPartSlots * sizeof(unsigned long long)));
+  CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, recs, rcnt, st));
   if (time_scan) {
     CK(cudaEventRecord(ws.ev3, st));
     ws.scan_timed = true;
   }
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
               b.cnt + kPendSlot, ws.sms, st);
-  g_launches += 5;
+  g_launches += scan_pair_mode() ? 5 : 6;
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a
@@ -508,8 +511,9 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
       const unsigned long long want = (need + need / 4 + 1024) * (unsigned long long)fparts;
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
-      const unsigned long long per_entry = sizeof(uint2) * 2 + sizeof(double);  // list + pending + residual
-      const unsigned long long limit = (ws.list.cap + ws.res.cap + ws.pend.cap + free_b / 4) / per_entry;
+      // list + pending + residual, + the scan's mask records (40 B per two entry slots)
+      const unsigned long long per_entry = sizeof(uint2) * 2 + sizeof(double) + 20;
+      const unsigned long long limit = (ws.list.cap + ws.res.cap + ws.pend.cap + ws.recs.cap + free_b / 4) / per_entry;
       ws.list_cap = std::max(ws.list_cap, std::min(want, limit));
       if (!std::getenv("FIC_LIST_CAP")) ws.list_cap_grown = ws.list_cap;
     }

@@ -677,6 +677,50 @@ struct WarpAppender {
   }
 };
 
+// Mask records: the scan epilogue writes one record per (warp, tile, range) with a hit: the
+// range's encoded index r * 8, the pool index of the warp's first domain and, per lane (one
+// domain each), the 8-bit mask of its isometry columns above the threshold.  One 8-byte
+// header store and one coalesced 32-byte store per record instead of a ballot loop per
+// survivor; expand_kernel turns the records into SurvEntry lists for the evaluation.
+struct MaskRec {
+  uint32_t r8;      // r * 8 (kSentinel: unused slot)
+  uint32_t d0;      // pool index of lane 0's domain
+  uint8_t m[32];    // lane l: isometry mask of domain d0 + l
+};
+constexpr uint32_t kRecChunk = 16;
+
+struct WarpRecAppender {
+  MaskRec* recs;
+  unsigned* count;   // CTA's reserved record slots (shared memory)
+  uint32_t cap;      // partition size (records)
+  uint32_t base;
+  uint32_t left;
+
+  // Warp-uniform: every lane passes its mask (0 for none).
+  __device__ __forceinline__ void put(uint32_t bits, uint32_t r8, uint32_t d0) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (left == 0) {
+      uint32_t nb = 0;
+      if (lane == 0) nb = atomicAdd(count, kRecChunk);
+      base = __shfl_sync(0xffffffffu, nb, 0);
+      left = kRecChunk;
+    }
+    if (base < cap) {
+      MaskRec* rc = recs + base;
+      if (lane == 0) *reinterpret_cast<uint2*>(rc) = make_uint2(r8, d0);
+      rc->m[lane] = (uint8_t)bits;
+    }
+    ++base;
+    --left;
+  }
+  __device__ __forceinline__ void close() {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t k = lane; k < left; k += 32)
+      if (base + k < cap) recs[base + k].r8 = kSentinel;
+    left = 0;
+  }
+};
+
 __device__ __forceinline__ float absmax8(const uint32_t* v) {
   const float* f = reinterpret_cast<const float*>(v);
   return fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
@@ -699,8 +743,9 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 __global__ void __launch_bounds__(kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
             const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
-            const float* __restrict__ thr, SurvEntry* __restrict__ list_all,
-            unsigned long long* __restrict__ counts, unsigned long long cap) {
+            const float* __restrict__ thr, MaskRec* __restrict__ recs_all,
+            unsigned long long* __restrict__ rcounts, unsigned long long rcap,
+            unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const ScanSmem L = scan_smem_layout(g.K);
   const int K = g.K;
@@ -713,8 +758,8 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   uint64_t* rfull_bar = tempty_bar + 2;
   uint64_t* rempty_bar = rfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(rempty_bar + 2);
-  unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 448);  // CTA's reserved survivor slots
-  SurvEntry* list = list_all + (unsigned long long)blockIdx.x * cap;  // this CTA's partition of `cap` entries
+  unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 448);  // CTA's reserved record slots
+  MaskRec* recs = recs_all + (unsigned long long)blockIdx.x * rcap;  // this CTA's partition of `rcap` records
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -801,7 +846,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     const int e = warp - 2;
     const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
-    WarpAppender app{list, count, (uint32_t)cap, 0u, 0u};
+    WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u};
     const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + part * kEpiCols;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
@@ -857,7 +902,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
 #pragma unroll
               for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
               if ((allpass >> k) & 1u) bits = 0xFFu;
-              app.bits(bits, rowbase + 8u * (uint32_t)k, d);
+              app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
             }
           }
         }
@@ -868,10 +913,84 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) counts[blockIdx.x] = *count;
+  if (threadIdx.x == 0) {
+    rcounts[blockIdx.x] = *count;
+    counts[blockIdx.x] = 0;  // entries: accumulated by expand_kernel
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kScanTmemCols>(tmem_base);
+  }
+}
+
+// Mask records of partition c -> SurvEntry list partition c (counts[c] entries; entries past
+// the partition size are dropped but counted, as with direct appends).  A record partition
+// that overflowed reports at least twice its record count as the entry count, which makes
+// the host re-run the level with lists large enough for it (records take half an entry
+// partition's slot count).  One thread per record (its 32 mask bytes in registers), one warp
+// prefix sum and one global atomic per 32 records.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, uint32_t lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (uint32_t)o) v += t;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+expand_kernel(const MaskRec* __restrict__ recs_all, const unsigned long long* __restrict__ rcounts,
+              unsigned long long rcap, SurvEntry* __restrict__ list_all, unsigned long long* __restrict__ counts,
+              unsigned long long part, int per) {
+  const int c = blockIdx.x / per, sub = blockIdx.x % per;
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned long long nr = rcounts[c];
+  if (nr > rcap) {
+    if (sub == 0 && threadIdx.x == 0) atomicAdd(counts + c, 2ull * nr);
+    return;
+  }
+  const MaskRec* recs = recs_all + (unsigned long long)c * rcap;
+  SurvEntry* list = list_all + (unsigned long long)c * part;
+  const unsigned long long wpb = blockDim.x / 32;
+  const unsigned long long nw = (unsigned long long)per * wpb;
+  for (unsigned long long i0 = ((unsigned long long)sub * wpb + threadIdx.x / 32) * 32; i0 < nr; i0 += nw * 32) {
+    const unsigned long long i = i0 + lane;
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint2 h = make_uint2(kSentinel, 0);
+    if (i < nr) {
+      const uint2* rp = reinterpret_cast<const uint2*>(recs + i);  // records are 8-byte aligned
+      h = rp[0];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // loaded with the header (no dependent round trip)
+        const uint2 t = rp[1 + q];
+        w[2 * q] = t.x;
+        w[2 * q + 1] = t.y;
+      }
+      if (h.x == kSentinel) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = 0;
+      }
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cnt += __popc(w[q]);
+    const uint32_t incl = warp_incl_scan(cnt, lane);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    unsigned long long b0 = 0;
+    if (lane == 0) b0 = atomicAdd(counts + c, (unsigned long long)total);
+    unsigned long long pos = __shfl_sync(0xffffffffu, b0, 0) + incl - cnt;
+    // byte l of the mask words is domain d0 + l, bit k of a byte isometry k
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t x = w[q];
+      while (x) {
+        const int b = __ffs(x) - 1;
+        x &= x - 1;
+        if (pos < part) list[pos] = make_uint2(h.x + (uint32_t)(b & 7), h.y + (uint32_t)(4 * q + (b >> 3)));
+        ++pos;
+      }
+    }
   }
 }
 
@@ -909,19 +1028,23 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
     unsigned qs = 0, qo = 0;
     if (j < n) {
       const SurvEntry en = list[i];
-      const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)(en.y & 0x7FFFFFFFu);
       double R = inf;
-      const DomainMetaI mi = en.x == kSentinel ? DomainMetaI{0, -1} : meta_i[d];
-      if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
+      if (en.x != kSentinel) {
+        const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)(en.y & 0x7FFFFFFFu);
+        // every operand load depends only on the entry: issued together, one L2 round trip
+        const DomainMetaI mi = meta_i[d];
         const RangeMeta rm = rmeta[r];
+        const double bar = load_bar(gbest, r);
         int x0, y0;
         range_origin(g, r, x0, y0);
         uint32_t qw[NN / 2], bpk[NN / 4];
         load_q8_row<NN>(qpool, d, s, qw);
         load_range_words<NN>(img, g, x0, y0, bpk);
-        R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, load_bar(gbest, r),
-                          screens, false, tab, qpool, img, d, s, x0, y0, qs, qo, &pending);
-        if (R < inf) publish_best(gbest, r, R);
+        if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
+          R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar, screens, false, tab,
+                            qpool, img, d, s, x0, y0, qs, qo, &pending);
+          if (R < inf) publish_best(gbest, r, R);
+        }
       }
       res[i] = R;
     }
@@ -1417,9 +1540,16 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
 }
 
 // counts[c] = survivors of scan CTA c; its entries are list[c * part, c * part + min(counts[c], part)).
+// Record partition size for entry partitions of `part` entries (see expand_kernel).
+unsigned long long scan_rec_part(unsigned long long part) { return (part / 2 + 2) & ~1ull; }  // even: 16-byte aligned partitions
+size_t scan_rec_bytes(unsigned long long list_cap, int parts) {
+  return (size_t)scan_rec_part(list_cap / (unsigned long long)parts) * parts * sizeof(MaskRec);
+}
+
 cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride, int sms, const __half* upool,
                         const RangeMeta* rmeta, const unsigned char* ropnd, const float* thr, SurvEntry* list,
-                        unsigned long long* counts, unsigned long long part, cudaStream_t st) {
+                        unsigned long long* counts, unsigned long long part, void* recs, unsigned long long* rcounts,
+                        cudaStream_t st) {
   const int grid = scan_grid(g, stride, sms);
   if (scan_pair_mode()) {
     const ScanLevel lv = make_level(g, stride, grid / 2);
@@ -1434,7 +1564,12 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   const ScanSmem L = scan_smem_layout(g.K);
   cudaError_t e = cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
-  scan_kernel<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, list, counts, part);
+  const unsigned long long rcap = scan_rec_part(part);
+  MaskRec* R = static_cast<MaskRec*>(recs);
+  scan_kernel<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts, rcap, counts);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,10 @@
+# mask-record appends + lean mean decoder: full GPU tests, bench cfg2/3/4, launch list
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+for c in cfg2 cfg3; do
+timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/bench_$c.json').read().strip().splitlines()[-1]); print('$c', d['ms_per_step'], 'e2e', d['e2e']['encode_ms_per_image'], 'scan', d['roofline']['kernel_ms'], 'matcher', d['roofline']['matcher_ms'], d['survivors_per_level'], 'decoder ms', d['decoder']['ms'], d['decoder']['frac'])"
+done
+timeout 900 python bench.py --config cfg4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg4.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/bench_cfg4.json').read().strip().splitlines()[-1]); print('cfg4', d['ms_per_step'], 'scan', d['roofline']['kernel_ms'], d['roofline']['frac'])"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu rc=$?
