@@ -336,7 +336,9 @@ def run_ours(args):
                     "encode_ms_per_image": float(e2e_s.item()) / e2e_steps * 1e3 / count,
                     "api": "paper_1404_0774_b200.encode_batch (C-ABI fic_encode_batch)" if volume else
                            "paper_1404_0774_b200.encode (C-ABI fic_encode)"},
-            "roofline": {"bound": "tensor", "kernel": "scan_kernel (full level: all R x D x 8 correlations)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "scan_kernel + expand_kernel (full level: all R x D x 8 correlations, "
+                                   "survivor mask records expanded to entries; events around both)",
                          "achieved": achieved, "peak": bf16,
                          "unit": "TFLOP/s", "frac": (achieved / bf16) if achieved else None,
                          "peak_source": f"{src} dense bf16 burst (the scan issues kind::f16 MMAs at the bf16 rate)",
@@ -348,7 +350,7 @@ def run_ours(args):
                          "matcher_ms": matcher_ms, "matcher_tflops": matcher_tflops,
                          "matcher_note": "all scan levels + survivor evaluation, per encode"},
             "survivors_per_level": survivors,
-            "decoder": {"kernel": "decode_step_kernel (+ fused step-RMSE partials)", "bound": "hbm",
+            "decoder": {"kernel": "decode_mean_kernel (+ fused step-RMSE partials and next 2x2 means)", "bound": "hbm",
                         "scale": dec_scale, "iterations": 10, "output": f"{side * dec_scale}^2 fp64",
                         "ms": dec_ms, "achieved": dec_bytes / (dec_ms / 1e3) / 1e9 if dec_ms > 0 else None,
                         "peak": hbm, "unit": "GB/s",
