@@ -286,8 +286,8 @@ constexpr int kScanCountSlots = kMaxLevels * kPartSlots + 2;  // + record self-c
 constexpr int kSelfcheckSlot = kMaxLevels * kPartSlots;
 constexpr int kPendSlot = kSelfcheckSlot + 1;
 
-// Scan levels: sparse passes over every 8^k-th 128-domain tile (k >= 1, at least one tile)
-// seed the pruning bar, then the full scan.  Each level prunes with the bar the previous
+// Scan levels: sparse passes over every 8^k-th (or 4 * 8^k-th) 128-domain tile seed the
+// pruning bar, then the full scan.  Each level prunes with the bar the previous
 // ones achieved, so survivors per level stay near (level size / previous level size) x the
 // handful of candidates whose bound is within the quantisation slack of the optimum.
 std::vector<int> scan_levels(const Geometry& g) {
@@ -305,9 +305,17 @@ std::vector<int> scan_levels(const Geometry& g) {
       while (*p && *p != ',') ++p;
       if (*p == ',') ++p;
     }
-  } else if (prepass) {
+  } else if (prepass && tiles > 1024) {
     for (int s : {4096, 512, 64, 8})
       if (tiles > s) lv.push_back(s);
+  } else if (prepass) {
+    // small pools (cfg2: 123 tiles, cfg3: 501): last sparse level at stride 4, earlier ones x8
+    // while they keep >= 8 tiles.  The sparse levels evaluate only each warp's best column per
+    // range (scan_kernel, lv.select), so they are cheap and a denser last level pays off
+    // (measured: cfg2 {4} 0.56 ms vs {64, 8} 0.61; cfg3 {32, 4} 3.09 vs {64, 8} 3.65).
+    std::vector<int> rev;
+    for (int s = 4; tiles >= 8 * s; s *= 8) rev.push_back(s);
+    lv.assign(rev.rbegin(), rev.rend());
   }
   lv.push_back(1);
   return lv;

@@ -450,8 +450,7 @@ seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned
   if (tid >= (long long)g.R * kSeedPerRange) return;
   const int r = (int)(tid / kSeedPerRange), k = (int)(tid % kSeedPerRange);
   const int s = k % kSyms, w = k / kSyms;
-  const RangeMeta m = rmeta[r];
-  if (m.shadow || g.D == 0) return;
+  if (g.D == 0) return;
   int x0, y0;
   range_origin(g, r, x0, y0);
   const int b = range_slice(g, r);
@@ -460,11 +459,13 @@ seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned
   const int xi = xi0 + w / kSeedSide - kSeedHalf, yi = yi0 + w % kSeedSide - kSeedHalf;
   if (xi < 0 || yi < 0 || xi >= g.PX || yi >= g.PY) return;
   const int d = b * g.Dt + xi * g.PY + yi;
+  // all operand loads depend only on (r, d, s): issued together, one memory round trip
+  const RangeMeta m = rmeta[r];
   const DomainMetaI mi = meta_i[d];
-  if (mi.den < 0) return;
   uint32_t qw[NN / 2], bpk[NN / 4];
   load_q8_row<NN>(qpool, d, s, qw);
   load_range_words<NN>(img, g, x0, y0, bpk);
+  if (m.shadow || mi.den < 0) return;
   unsigned qs, qo;
   // an upper bound of the candidate's exact residual is a valid pruning bar
   const double v = eval_fast<NN>(g, qw, bpk, m.sb, (double)m.var / (double)NN, mi.sq, mi.den,
@@ -508,6 +509,7 @@ struct ScanLevel {
   int rounds;     // full rounds: m_tiles / G
   int rem;        // m-tiles of the last round: m_tiles % G
   int k;          // chunks per leftover m-tile
+  int select;     // 1: keep only each range's best column per warp and tile (sparse levels, see the epilogue)
 };
 
 struct Segment {
@@ -561,7 +563,10 @@ __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict_
       int x0, y0;
       range_origin(g, r, x0, y0);
       const float mean = (float)rmeta[r].sb / (float)N;  // exact: N is a power of two
-      const float scale = range_scale(thr[r]);
+      float scale = range_scale(thr[r]);
+      // a range without a usable bar keeps every column at the full level; at sparse levels its
+      // columns are the normalised correlations, so the selection there still picks the best
+      if (range_allpass(thr[r])) scale = rsqrtf((float)rmeta[r].var / (float)N + 1.0f);
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
         const int j = kc * 8 + h;
@@ -899,9 +904,32 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           for (int k = 0; k < kEpiRanges; ++k) {
             if ((groups >> k) & 1u) {
               uint32_t bits = 0;
+              const bool ap = (allpass >> k) & 1u;
+              if (ap && !lv.select) {
+                bits = 0xFFu;
+              } else if (lv.select) {
+                // sparse level: it only has to lower the bar, so of this warp's 32 domains x 8
+                // isometries only the column with the largest |X~| (the smallest unconstrained
+                // bound R*) is evaluated: the lane's best isometry, then the warp's best lane
+                // (ties: lowest isometry, lowest lane).  The full level keeps every survivor.
+                float best = fabsf(__uint_as_float(v[8 * k]));
+                uint32_t bi = 0;
 #pragma unroll
-              for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
-              if ((allpass >> k) & 1u) bits = 0xFFu;
+                for (int c = 1; c < 8; ++c) {
+                  const float a = fabsf(__uint_as_float(v[8 * k + c]));
+                  if (a > best) {
+                    best = a;
+                    bi = (uint32_t)c;
+                  }
+                }
+                const uint32_t key = (best > 1.0f || ap) ? __float_as_uint(best) : 0u;  // |x| >= 0: orders as uint
+                const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
+                const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
+                bits = (uint32_t)lane == win ? 1u << bi : 0u;
+              } else {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
+              }
               app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
             }
           }
@@ -1007,7 +1035,7 @@ __device__ __forceinline__ bool list_slot(unsigned long long i, unsigned long lo
 // the reference's fp64 arithmetic (eval_exact) against the range's current bar; an achieved
 // residual lowers the bar.  res[i] = residual (+inf when pruned or flat).
 template <int NN>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
             const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
             const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
@@ -1020,14 +1048,18 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
   const int c = blockIdx.x / per, sub = blockIdx.x % per;
   const unsigned long long n = min(counts[c], part);
   const unsigned long long base = (unsigned long long)c * part;
-  // warp-uniform trip count so the pending pushes below can use warp collectives
-  for (unsigned long long j0 = (unsigned long long)sub * blockDim.x + (threadIdx.x & ~31u); j0 < n;
-       j0 += (unsigned long long)per * blockDim.x) {
+  // warp-uniform trip count so the pending pushes below can use warp collectives; the next
+  // iteration's entry is loaded one iteration ahead
+  const unsigned long long jstep = (unsigned long long)per * blockDim.x;
+  unsigned long long j0 = (unsigned long long)sub * blockDim.x + (threadIdx.x & ~31u);
+  SurvEntry en_next = j0 + lane < n ? list[base + j0 + lane] : make_uint2(kSentinel, 0);
+  for (; j0 < n; j0 += jstep) {
     const unsigned long long j = j0 + lane, i = base + j;
+    const SurvEntry en = en_next;
+    if (j + jstep < n) en_next = list[i + jstep];
     bool pending = false;
     unsigned qs = 0, qo = 0;
     if (j < n) {
-      const SurvEntry en = list[i];
       double R = inf;
       if (en.x != kSentinel) {
         const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)(en.y & 0x7FFFFFFFu);
@@ -1521,6 +1553,10 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
   ScanLevel lv;
   const int n_tiles = scan_tiles(g);
   lv.stride = stride;
+  {
+    const char* e = std::getenv("FIC_SELECT");  // "0": sparse levels keep every survivor (A/B)
+    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? 1 : 0;
+  }
   lv.n_lvl = (n_tiles + stride - 1) / stride;
   lv.m_tiles = (g.R + kScanRanges - 1) / kScanRanges;
   lv.rounds = lv.m_tiles / G;
