@@ -6,8 +6,10 @@
 // There is no CPU fallback: every failure of the CUDA runtime surfaces as FIC_ERR_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -229,6 +231,16 @@ struct Workspace {
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
   unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
   unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
+  // CUDA graphs of the scan-path encode, keyed by everything its launches bake in
+  struct Graph {
+    std::vector<unsigned long long> key;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long launches = 0;
+    unsigned long long used = 0;
+  };
+  std::vector<Graph> graphs;
+  std::vector<unsigned long long> last_key;  // fingerprint of the previous eager encode
+  unsigned long long graph_clock = 0;
   std::mutex mu;
 };
 
@@ -455,6 +467,94 @@ void enqueue_encode_simt(Workspace& ws, const unsigned char* d_img, const Geomet
   }
 }
 
+// The scan-path encode as a CUDA graph: ~30 dependent launches, memsets and event records
+// per encode cost ~2 us of launch gap each when enqueued one by one.  The graph bakes in
+// the geometry, every buffer pointer, the list capacity, the stream and the switches read
+// from the environment, so those form its key; a key seen on two consecutive encodes is
+// captured (the first run allocated every buffer, so capture performs no allocation) and
+// replayed from then on.  FIC_NO_GRAPH=1, and encodes timed with fic_set_matcher_timing,
+// enqueue eagerly.
+std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d_img, const Geometry& g,
+                                           const fic_mapping* d_out, const unsigned long long* d_counters,
+                                           cudaStream_t st) {
+  std::vector<unsigned long long> k;
+  const int gi[] = {g.W, g.H, g.n, g.N, g.K, g.step, g.PX, g.PY, g.D, g.D_pad, g.RX, g.R, g.row_begin,
+                    g.single_x0, g.single_y0, g.flags, g.s_bits, g.o_bits, g.batch, g.H1, g.R1, g.Dt};
+  for (int v : gi) k.push_back((unsigned long long)(unsigned)v);
+  unsigned long long bits;
+  std::memcpy(&bits, &g.s_max, 8);
+  k.push_back(bits);
+  std::memcpy(&bits, &g.shadow_eps, 8);
+  k.push_back(bits);
+  (void)st;  // graphs are stream-independent (captured on the workspace stream, launched on any)
+  const void* ptrs[] = {d_img, d_out, d_counters, ws.upool.p, ws.qpool.p, ws.meta_i.p, ws.rmeta.p, ws.gbest.p,
+                        ws.win.p, ws.ropnd.p, ws.thr.p, ws.deq.p, ws.scan_counts.p, ws.list.p, ws.res.p, ws.pend.p,
+                        ws.recs.p, ws.rcounts.p};
+  for (const void* q : ptrs) k.push_back((unsigned long long)(uintptr_t)q);
+  k.push_back(ws.list_cap);
+  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER"}) {
+    const char* e = std::getenv(name);
+    unsigned long long h = 1469598103934665603ull;
+    for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;
+    k.push_back(h);
+  }
+  return k;
+}
+
+void enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b,
+                          fic_mapping* d_out, unsigned long long* d_counters, cudaStream_t st) {
+  if (std::getenv("FIC_NO_GRAPH") || g_timing.load()) {  // timed encodes (event records) run eagerly
+    enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
+    return;
+  }
+  // the list capacity this encode will use (as enqueue_encode_scan sets it)
+  ws.list_cap_grown = std::max(ws.list_cap_grown, std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128));
+  ws.list_cap = ws.list_cap_grown;
+  if (const char* lc = std::getenv("FIC_LIST_CAP")) ws.list_cap = std::strtoull(lc, nullptr, 10);
+  const std::vector<unsigned long long> key = encode_key(ws, d_img, g, d_out, d_counters, st);
+  ++ws.graph_clock;
+  for (auto& gr : ws.graphs) {
+    if (gr.key == key) {
+      CK(cudaGraphLaunch(gr.exec, st));
+      g_launches += gr.launches;
+      gr.used = ws.graph_clock;
+      return;
+    }
+  }
+  if (key != ws.last_key) {  // first sighting: eager (allocates); capture on the next one
+    enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
+    ws.last_key = encode_key(ws, d_img, g, d_out, d_counters, st);
+    return;
+  }
+  const unsigned long long l0 = g_launches.load();
+  cudaGraph_t graph = nullptr;
+  // captured on the workspace's own stream (the caller's may be the legacy default stream,
+  // which cannot be captured); nothing executes during capture
+  CK(cudaStreamBeginCapture(ws.stream, cudaStreamCaptureModeRelaxed));
+  try {
+    enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, ws.stream);
+  } catch (...) {
+    cudaStreamEndCapture(ws.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  CK(cudaStreamEndCapture(ws.stream, &graph));
+  Workspace::Graph gr;
+  gr.key = key;
+  gr.launches = g_launches.load() - l0;
+  gr.used = ws.graph_clock;
+  CK(cudaGraphInstantiate(&gr.exec, graph, 0));
+  CK(cudaGraphDestroy(graph));
+  CK(cudaGraphLaunch(gr.exec, st));
+  if (ws.graphs.size() >= 16) {  // evict the least recently used
+    auto it = std::min_element(ws.graphs.begin(), ws.graphs.end(),
+                               [](const Workspace::Graph& a, const Workspace::Graph& c) { return a.used < c.used; });
+    CK(cudaGraphExecDestroy(it->exec));
+    ws.graphs.erase(it);
+  }
+  ws.graphs.push_back(std::move(gr));
+}
+
 // Enqueue the whole encode of the region described by g and wait for it; a survivor list
 // that overflowed is grown to the count the scan reported and the encode is re-run.
 // counters[b] = flat domains and counters[batch + b] = shadow ranges of slice b (copied to
@@ -474,7 +574,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
   const ScanBufs b = scan_bufs(ws, g);
   const size_t nl = scan_levels(g).size();
   auto* hc = static_cast<unsigned long long*>(ws.h_scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
-  enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
+  enqueue_encode_graph(ws, d_img, g, b, d_out, d_counters, st);
   for (int attempt = 0;; ++attempt) {
     CK(cudaMemcpyAsync(hc, b.cnt, kScanCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (h_counters)

@@ -275,3 +275,30 @@ def test_scan_modes_cfg4_sample(oracle):
             enc = fic.encode(img, fic.CodecParams(**pv))
         got = np.concatenate([enc.mappings[r * R:(r + 1) * R] for r in rows])
         assert_same(got, want, f"cfg4 rows {scan}")
+
+
+def test_graph_replay_new_contents(oracle):
+    """Repeated encodes of one geometry run as a captured CUDA graph from the third call on;
+    replays must follow new image contents, timing switches and list-capacity changes, and
+    match the eager path (FIC_NO_GRAPH=1) and the oracle."""
+    pv = dict(n=4, step=2)
+    imgs = [oracle.noise_image(64, 70 + k) for k in range(2)] + [oracle.smooth_image(64, 71)]
+    want = [oracle.encode(im, pv) for im in imgs]
+    for rep in range(4):
+        for k, im in enumerate(imgs):
+            enc = fic.encode(im, fic.CodecParams(**pv))
+            assert_same(enc.mappings, want[k][0], f"graph rep {rep} image {k}")
+            assert enc.stats == want[k][1]
+    fic.set_matcher_timing(True)
+    try:
+        for k, im in enumerate(imgs * 3):
+            assert_same(fic.encode(im, fic.CodecParams(**pv)).mappings, want[k % 3][0], "timed graph")
+        assert fic.matcher_timing(reset=True)[1] > 0
+    finally:
+        fic.set_matcher_timing(False)
+    with env(FIC_LIST_CAP="300"):  # overflow: the full level re-runs eagerly with grown lists
+        for k, im in enumerate(imgs * 2):
+            assert_same(fic.encode(im, fic.CodecParams(**pv)).mappings, want[k % 3][0], "tiny list")
+    with env(FIC_NO_GRAPH="1"):
+        for k, im in enumerate(imgs):
+            assert_same(fic.encode(im, fic.CodecParams(**pv)).mappings, want[k][0], "eager")
