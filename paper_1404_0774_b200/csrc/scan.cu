@@ -750,6 +750,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
             const float* __restrict__ thr, MaskRec* __restrict__ recs_all,
             unsigned long long* __restrict__ rcounts, unsigned long long rcap,
+            SurvEntry* __restrict__ list_all, unsigned long long cap,
             unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const ScanSmem L = scan_smem_layout(g.K);
@@ -764,6 +765,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   uint64_t* rempty_bar = rfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(rempty_bar + 2);
   unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 448);  // CTA's reserved record slots
+  unsigned* ecount = count + 1;  // CTA's reserved entry slots (sparse levels)
   MaskRec* recs = recs_all + (unsigned long long)blockIdx.x * rcap;  // this CTA's partition of `rcap` records
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -784,6 +786,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     }
     ptx::fence_mbar_init();
     *count = 0;
+    *ecount = 0;
   }
   if (warp == 1) ptx::tmem_alloc<kScanTmemCols>(tmem_base_smem);
   ptx::tc_fence_before();
@@ -852,6 +855,10 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
     WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u};
+    const bool sel = lv.select != 0;
+    SurvEntry* elist = list_all + (unsigned long long)blockIdx.x * cap;  // sparse levels: direct entries
+    const uint32_t ecap = (uint32_t)cap;
+    uint32_t ebase = 0, eleft = 0;
     const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + part * kEpiCols;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
@@ -886,6 +893,48 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
         if (g.flags & 8) continue;                          // debug: skip the test
+        if (sel) {
+          // sparse level: it only has to lower the bar, so of this warp's 32 domains x 8
+          // isometries of each range only the column with the largest |X~| (the smallest
+          // unconstrained bound R*) is evaluated, written straight to the entry list.  For the
+          // ranges that hit, the isometry rides in the low 3 bits of the packed |x| (7 - s: ties
+          // within 2^-20 go to the lower isometry, then the lower lane), so one max tree and one
+          // warp max yield the winning lane and isometry.
+          uint32_t gmask = allpass;
+#pragma unroll
+          for (int k = 0; k < kEpiRanges; ++k) {
+            const float* f = reinterpret_cast<const float*>(v + 8 * k);
+            const float gm = fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
+                                         fmaxf(fabsf(f[4]), fabsf(f[5]))),
+                                   fmaxf(fabsf(f[6]), fabsf(f[7])));
+            gmask |= (uint32_t)(gm > 1.0f) << k;
+          }
+          const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+#pragma unroll
+          for (int k = 0; k < kEpiRanges; ++k) {
+            if ((groups >> k) & 1u) {
+              float m = 0.f;
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
+              const uint32_t key = (m > 1.0f || ((allpass >> k) & 1u)) ? __float_as_uint(m) : 0u;
+              const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
+              if (wmax == 0u) continue;
+              const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
+              if (eleft == 0) {  // warp-level chunk of entry slots
+                uint32_t nb = 0;
+                if (lane == 0) nb = atomicAdd(ecount, 32u);
+                ebase = __shfl_sync(0xffffffffu, nb, 0);
+                eleft = 32;
+              }
+              if ((uint32_t)lane == win && ebase < ecap)
+                elist[ebase] = make_uint2(rowbase + 8u * (uint32_t)k + (7u - (wmax & 7u)), d);
+              ++ebase;
+              --eleft;
+            }
+          }
+          continue;
+        }
         // |max| of each range's 8 isometry columns (4 FMNMX3 each); mask of ranges above 1
         uint32_t gmask = allpass;
 #pragma unroll
@@ -904,28 +953,8 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           for (int k = 0; k < kEpiRanges; ++k) {
             if ((groups >> k) & 1u) {
               uint32_t bits = 0;
-              const bool ap = (allpass >> k) & 1u;
-              if (ap && !lv.select) {
+              if ((allpass >> k) & 1u) {
                 bits = 0xFFu;
-              } else if (lv.select) {
-                // sparse level: it only has to lower the bar, so of this warp's 32 domains x 8
-                // isometries only the column with the largest |X~| (the smallest unconstrained
-                // bound R*) is evaluated: the lane's best isometry, then the warp's best lane
-                // (ties: lowest isometry, lowest lane).  The full level keeps every survivor.
-                float best = fabsf(__uint_as_float(v[8 * k]));
-                uint32_t bi = 0;
-#pragma unroll
-                for (int c = 1; c < 8; ++c) {
-                  const float a = fabsf(__uint_as_float(v[8 * k + c]));
-                  if (a > best) {
-                    best = a;
-                    bi = (uint32_t)c;
-                  }
-                }
-                const uint32_t key = (best > 1.0f || ap) ? __float_as_uint(best) : 0u;  // |x| >= 0: orders as uint
-                const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
-                const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
-                bits = (uint32_t)lane == win ? 1u << bi : 0u;
               } else {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
@@ -936,6 +965,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         }
       }
     }
+    // pad the warp's unused entry slots (sparse levels)
+    for (uint32_t k = (uint32_t)lane; k < eleft; k += 32)
+      if (ebase + k < ecap) elist[ebase + k] = make_uint2(kSentinel, kSentinel);
     app.close();
   }
 
@@ -943,7 +975,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   __syncthreads();
   if (threadIdx.x == 0) {
     rcounts[blockIdx.x] = *count;
-    counts[blockIdx.x] = 0;  // entries: accumulated by expand_kernel
+    counts[blockIdx.x] = *ecount;  // direct entries (sparse levels); expand_kernel adds the records' entries
   }
   if (warp == 1) {
     ptx::tc_fence_after();
@@ -1602,7 +1634,8 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   if (e != cudaSuccess) return e;
   const unsigned long long rcap = scan_rec_part(part);
   MaskRec* R = static_cast<MaskRec*>(recs);
-  scan_kernel<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts, rcap, counts);
+  scan_kernel<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts, rcap, list, part,
+                                                   counts);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
