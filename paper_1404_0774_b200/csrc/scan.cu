@@ -510,6 +510,7 @@ struct ScanLevel {
   int rem;        // m-tiles of the last round: m_tiles % G
   int k;          // chunks per leftover m-tile
   int select;     // 1: keep only each range's best column per warp and tile (sparse levels, see the epilogue)
+  int coarse;     // 1: whole-tile |max| vote before the per-range test (large pools: rare hits)
 };
 
 struct Segment {
@@ -934,6 +935,17 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             }
           }
           continue;
+        }
+        if (lv.coarse && !allpass) {
+          // large pools, hits in ~2% of warp-tiles: one |max| over all 64 columns (32 FMNMX3)
+          // and a warp vote first; the per-range breakdown only for the rare tiles with a hit
+          float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+          for (int c = 0; c < kEpiCols; c += 4) {
+            m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
+            m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[c + 2])), fabsf(__uint_as_float(v[c + 3]))));
+          }
+          if (!__any_sync(0xffffffffu, fmaxf(m0, m1) > 1.0f)) continue;
         }
         // |max| of each range's 8 isometry columns (4 FMNMX3 each); mask of ranges above 1
         uint32_t gmask = allpass;
@@ -1588,6 +1600,10 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
   {
     const char* e = std::getenv("FIC_SELECT");  // "0": sparse levels keep every survivor (A/B)
     lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? 1 : 0;
+  }
+  {
+    const char* e = std::getenv("FIC_COARSE");  // "0" / "1": force the whole-tile vote off / on (A/B)
+    lv.coarse = e ? (std::strcmp(e, "0") != 0) : (n_tiles > 1024 ? 1 : 0);
   }
   lv.n_lvl = (n_tiles + stride - 1) / stride;
   lv.m_tiles = (g.R + kScanRanges - 1) / kScanRanges;

@@ -302,3 +302,16 @@ def test_graph_replay_new_contents(oracle):
     with env(FIC_NO_GRAPH="1"):
         for k, im in enumerate(imgs):
             assert_same(fic.encode(im, fic.CodecParams(**pv)).mappings, want[k][0], "eager")
+
+
+@pytest.mark.parametrize("coarse", ["0", "1"])
+def test_coarse_vote_output_neutral(oracle, coarse):
+    """The whole-tile |max| vote (default for pools above 1024 tiles) forced on and off on
+    small images: identical codes and residual bits."""
+    for img, pv in [(oracle.noise_image(64, 9), dict(n=4, step=2)), (oracle.smooth_image(64, 5), dict(n=8, step=2)),
+                    (images.ct_slice(256, 1404002, 0.3), dict(n=8, step=4))]:
+        want, st = oracle.encode(img, pv)
+        with env(FIC_COARSE=coarse):
+            enc = fic.encode(img, fic.CodecParams(**pv))
+        assert_same(enc.mappings, want, f"coarse={coarse} {pv}")
+        assert enc.stats == st
