@@ -419,8 +419,10 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   launch_range_pass(d_img, g, b.rm, d_counters + g.batch, st);       // shadow ranges per slice
   launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
   launch_deq_tables(g, b.deq, st);
-  launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
-  g_launches += 5;
+  const char* seed_env = std::getenv("FIC_SEED");  // "0": no local seed (A/B)
+  const bool seed = !(seed_env && std::strcmp(seed_env, "0") == 0);
+  if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
+  g_launches += seed ? 5 : 4;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
   const std::vector<int> lv = scan_levels(g);
   for (size_t l = 0; l + 1 < lv.size(); ++l) enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st);
@@ -492,7 +494,7 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
                         ws.recs.p, ws.rcounts.p};
   for (const void* q : ptrs) k.push_back((unsigned long long)(uintptr_t)q);
   k.push_back(ws.list_cap);
-  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE"}) {
+  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;

@@ -509,7 +509,7 @@ struct ScanLevel {
   int rounds;     // full rounds: m_tiles / G
   int rem;        // m-tiles of the last round: m_tiles % G
   int k;          // chunks per leftover m-tile
-  int select;     // 1: keep only each range's best column per warp and tile (sparse levels, see the epilogue)
+  int select;     // 1, 2: keep only each range's best column per warp and tile (sparse levels; 2: small pools)
   int coarse;     // 1: whole-tile |max| vote before the per-range test (large pools: rare hits)
 };
 
@@ -746,6 +746,11 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 //                 scaled so the pruning test is |X~/T_r| > 1 for every column), tests each
 //                 range's 8-isometry |max| against 1 and appends the rare columns above it to
 //                 the survivor list
+// MODE: 0 full level, 1 full level with the whole-tile vote (lv.coarse), 2 sparse level with
+// the per-range test before the selection (lv.select == 1), 3 sparse level selecting from the
+// packed maxima of every range (lv.select == 2: most ranges hit in most tiles).  One
+// instantiation per mode keeps each epilogue's registers to its own path.
+template <int MODE>
 __global__ void __launch_bounds__(kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
             const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
@@ -856,7 +861,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
     WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u};
-    const bool sel = lv.select != 0;
+    constexpr bool sel = MODE >= 2;
     SurvEntry* elist = list_all + (unsigned long long)blockIdx.x * cap;  // sparse levels: direct entries
     const uint32_t ecap = (uint32_t)cap;
     uint32_t ebase = 0, eleft = 0;
@@ -894,30 +899,46 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
         if (g.flags & 8) continue;                          // debug: skip the test
-        if (sel) {
+        if constexpr (sel) {
           // sparse level: it only has to lower the bar, so of this warp's 32 domains x 8
           // isometries of each range only the column with the largest |X~| (the smallest
           // unconstrained bound R*) is evaluated, written straight to the entry list.  For the
           // ranges that hit, the isometry rides in the low 3 bits of the packed |x| (7 - s: ties
           // within 2^-20 go to the lower isometry, then the lower lane), so one max tree and one
           // warp max yield the winning lane and isometry.
+          // MODE 3: packed maxima of every range up front (most ranges hit); MODE 2: plain
+          // maxima for the hit test, packed ones only for the ranges that hit
+          uint32_t pk[kEpiRanges];
           uint32_t gmask = allpass;
 #pragma unroll
           for (int k = 0; k < kEpiRanges; ++k) {
-            const float* f = reinterpret_cast<const float*>(v + 8 * k);
-            const float gm = fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
-                                         fmaxf(fabsf(f[4]), fabsf(f[5]))),
-                                   fmaxf(fabsf(f[6]), fabsf(f[7])));
-            gmask |= (uint32_t)(gm > 1.0f) << k;
+            if constexpr (MODE == 3) {
+              float m = 0.f;
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
+              pk[k] = __float_as_uint(m);
+              gmask |= (uint32_t)(m > 1.0f) << k;
+            } else {
+              const float* f = reinterpret_cast<const float*>(v + 8 * k);
+              const float gm = fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
+                                           fmaxf(fabsf(f[4]), fabsf(f[5]))),
+                                     fmaxf(fabsf(f[6]), fabsf(f[7])));
+              gmask |= (uint32_t)(gm > 1.0f) << k;
+            }
           }
           const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
 #pragma unroll
           for (int k = 0; k < kEpiRanges; ++k) {
             if ((groups >> k) & 1u) {
               float m = 0.f;
+              if constexpr (MODE == 3) {
+                m = __uint_as_float(pk[k]);
+              } else {
 #pragma unroll
-              for (int c = 0; c < 8; ++c)
-                m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
+                for (int c = 0; c < 8; ++c)
+                  m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
+              }
               const uint32_t key = (m > 1.0f || ((allpass >> k) & 1u)) ? __float_as_uint(m) : 0u;
               const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
               if (wmax == 0u) continue;
@@ -936,7 +957,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           }
           continue;
         }
-        if (lv.coarse && !allpass) {
+        if (MODE == 1 && !allpass) {
           // large pools, hits in ~2% of warp-tiles: one |max| over all 64 columns (32 FMNMX3)
           // and a warp vote first; the per-range breakdown only for the rare tiles with a hit
           float m0 = 0.f, m1 = 0.f;
@@ -1599,7 +1620,7 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
   lv.stride = stride;
   {
     const char* e = std::getenv("FIC_SELECT");  // "0": sparse levels keep every survivor (A/B)
-    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? 1 : 0;
+    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? (n_tiles <= 1024 ? 2 : 1) : 0;
   }
   {
     const char* e = std::getenv("FIC_COARSE");  // "0" / "1": force the whole-tile vote off / on (A/B)
@@ -1646,12 +1667,13 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   }
   const ScanLevel lv = make_level(g, stride, grid);
   const ScanSmem L = scan_smem_layout(g.K);
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  const int mode = lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0));
+  auto kern = mode == 3 ? scan_kernel<3> : (mode == 2 ? scan_kernel<2> : (mode == 1 ? scan_kernel<1> : scan_kernel<0>));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const unsigned long long rcap = scan_rec_part(part);
   MaskRec* R = static_cast<MaskRec*>(recs);
-  scan_kernel<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts, rcap, list, part,
-                                                   counts);
+  kern<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts, rcap, list, part, counts);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
