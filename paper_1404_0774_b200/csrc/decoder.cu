@@ -229,9 +229,11 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     int sym, sr0, sc0;
   };
   __shared__ Blk blk[kWhole ? 1 : nb];
-  const int tiles_x = out_w / kTile, hw = out_w / 2;
-  const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
-  const int Y0 = ty * kTile, X0 = tx * kTile;
+  const int hw = out_w / 2;
+  const int Y0 = blockIdx.y * kTile, X0 = blockIdx.x * kTile;  // 2-D grid of tiles
+  // 32-bit element offsets (rasters up to 2^31 doubles) from per-tile base pointers
+  const double* cur_t = cur + (long long)Y0 * out_w + X0;
+  double* nxt_t = nxt + (long long)Y0 * out_w + X0;
   const int lane_c = threadIdx.x & (kTile - 1), row0 = threadIdx.x >> 5;  // element e = threadIdx.x + 256 k
   constexpr int kPer = kTile * kTile / kTileThreads;
   constexpr int kRowStep = kTileThreads / kTile;
@@ -241,7 +243,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
   if (partial) {
 #pragma unroll
     for (int k = 0; k < kPer; ++k)
-      cv[k] = __ldcs(cur + (long long)(Y0 + row0 + k * kRowStep) * out_w + X0 + lane_c);
+      cv[k] = __ldcs(cur_t + (row0 + k * kRowStep) * out_w + lane_c);
   }
   Blk B;     // kWhole: the tile's one block, computed by every thread (broadcast load, no sync)
   int a0 = 0, c0 = 0;  // kWhole: the tile's offset inside its range
@@ -262,7 +264,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     B.mcol0 = t.dx / 2 + B.sc0;
 #pragma unroll
     for (int k = 0; k < kPer; ++k)
-      zv[k] = __ldg(mcur + (long long)(B.mrow0 + row0 + k * kRowStep) * hw + B.mcol0 + lane_c);
+      zv[k] = __ldg(mcur + (B.mrow0 + row0 + k * kRowStep) * hw + B.mcol0 + lane_c);
   } else {
     for (int b = threadIdx.x; b < nb; b += kTileThreads) {
       const int ry = (Y0 >> LT) + b / bpr, rx = (X0 >> LT) + b % bpr;
@@ -281,7 +283,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     for (int k = 0; k < kPer; ++k) {
       const int zr = row0 + k * kRowStep, zc = lane_c;
       const Blk& Q = blk[(zr >> LT) * bpr + (zc >> LT)];
-      zv[k] = __ldg(mcur + (long long)(Q.mrow0 + (zr & (T - 1))) * hw + Q.mcol0 + (zc & (T - 1)));
+      zv[k] = __ldg(mcur + (Q.mrow0 + (zr & (T - 1))) * hw + Q.mcol0 + (zc & (T - 1)));
     }
   }
 #pragma unroll
@@ -308,7 +310,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
       o = Q.o;
     }
     const double v = __dadd_rn(__dmul_rn(s, z), o);
-    __stcs(nxt + (long long)(Y0 + orow) * out_w + X0 + ocol, v);
+    __stcs(nxt_t + orow * out_w + ocol, v);
     vs[orow][ocol] = v;
     if (partial) {
       const double dlt = __dsub_rn(cv[k], v);
@@ -321,7 +323,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     const double m = __dmul_rn(
         __dadd_rn(__dadd_rn(__dadd_rn(vs[2 * i][2 * j], vs[2 * i][2 * j + 1]), vs[2 * i + 1][2 * j]), vs[2 * i + 1][2 * j + 1]),
         0.25);
-    mnxt[(long long)(Y0 / 2 + i) * hw + X0 / 2 + j] = m;
+    mnxt[(Y0 / 2 + i) * hw + X0 / 2 + j] = m;
   }
   if (partial) {
     __shared__ double red[kTileThreads / 32];
@@ -331,7 +333,7 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < kTileThreads / 32; ++w) t = __dadd_rn(t, red[w]);
-      partial[blockIdx.x] = t;
+      partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
   }
 }
@@ -344,7 +346,7 @@ void launch_mean_raster(const double* r, double* m, int out_w, cudaStream_t st) 
 // One iteration on the mean raster (decode_mean_ok); partials as decode_partials.
 void launch_decode_mean(const double* cur, const double* mcur, double* nxt, double* mnxt, const RangeXform* xf,
                         int out_w, int kn, int ranges_x, double* partial, cudaStream_t st) {
-  const int grid = (out_w / kTile) * (out_w / kTile);
+  const dim3 grid(out_w / kTile, out_w / kTile);
 #define FIC_MEAN(LT) decode_mean_kernel<LT><<<grid, kTileThreads, 0, st>>>(cur, mcur, nxt, mnxt, xf, out_w, kn, ranges_x, partial)
   switch (kn >= kTile ? 5 : __builtin_ctz((unsigned)kn)) {
     case 1: FIC_MEAN(1); break;
