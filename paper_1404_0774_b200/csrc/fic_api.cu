@@ -69,8 +69,8 @@ int scan_padded_ranges(const Geometry&);
 bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
 size_t range_op_bytes(const Geometry&);
-void launch_range_op(const unsigned char*, const Geometry&, const RangeMeta*, const float*, unsigned char*,
-                     cudaStream_t);
+void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, const unsigned long long*, float*,
+                      unsigned char*, bool, cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
                  const double*, uint2*, unsigned long long*, int, cudaStream_t);
@@ -372,8 +372,7 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   auto* pend = static_cast<uint2*>(ws.pend.get((size_t)ws.list_cap * sizeof(uint2)));
   const int parts = scan_grid(g, stride, ws.sms);
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
-  launch_threshold(g, b.rm, b.gbest, b.thr, st);
-  if (!scan_pair_mode() || stride == first_stride) launch_range_op(d_img, g, b.rm, b.thr, b.ropnd, st);
+  launch_level_ops(d_img, g, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride, st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   void* recs = ws.recs.get(scan_rec_bytes(ws.list_cap, parts));
@@ -385,7 +384,7 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   }
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
               b.cnt + kPendSlot, ws.sms, st);
-  g_launches += scan_pair_mode() ? 5 : 6;
+  g_launches += 5;  // level ops, scan, expand (or the pair scan's range rows), evaluation, residuals
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a

@@ -587,27 +587,43 @@ __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict_
 // Per-range scan thresholds of a level (scan_threshold against the range's current bar);
 // padded to whole m-tiles.  Invalid and shadow ranges get +1e30 (never survive), flags & 1
 // (exhaustive debug mode) -1 (everything survives).
-__global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta,
-                                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr, int padded) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= padded) return;
+__device__ __forceinline__ float range_threshold(const Geometry& g, const RangeMeta* __restrict__ rmeta,
+                                                 const unsigned long long* __restrict__ gbest, int r) {
   float t = 1e30f;
   if (r < g.R) {
     const RangeMeta rm = rmeta[r];
     if (!rm.shadow) t = (g.flags & 1) ? -1.f : scan_threshold((double)rm.var / (double)g.N, load_bar(gbest, r), g.N, g.K);
   }
-  thr[r] = t;
+  return t;
+}
+
+__global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta,
+                                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr, int padded) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= padded) return;
+  thr[r] = range_threshold(g, rmeta, gbest, r);
 }
 
 // Range operands of every m-tile, built per level into global memory (one CTA per m-tile,
 // r_bytes each) so the scan loads them with one bulk copy per segment.
+// The level's per-range thresholds are computed here too (each CTA for its m-tile's 32
+// ranges, the blockIdx.y == 0 CTA writes them out for the scan epilogue), one launch per level.
 __global__ void __launch_bounds__(256)
 range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
-                const float* __restrict__ thr, unsigned char* __restrict__ ropnd) {
+                const unsigned long long* __restrict__ gbest, float* __restrict__ thr,
+                unsigned char* __restrict__ ropnd) {
+  __shared__ float s_thr[kScanRanges];
+  if (threadIdx.x < kScanRanges) {
+    const int r = blockIdx.x * kScanRanges + threadIdx.x;
+    const float t = range_threshold(g, rmeta, gbest, r);
+    s_thr[threadIdx.x] = t;
+    if (blockIdx.y == 0) thr[r] = t;
+  }
+  __syncthreads();
   // blockIdx.y splits the m-tile's 256 x K/8 chunks over several CTAs
   const int per = kScanRows * (g.K / 8) / gridDim.y;
-  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, thr, blockIdx.x,
-               blockIdx.y * per + threadIdx.x, blockDim.x, blockIdx.y * per + per);
+  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, s_thr - blockIdx.x * kScanRanges,
+               blockIdx.x, blockIdx.y * per + threadIdx.x, blockDim.x, blockIdx.y * per + per);
 }
 
 // Survivor appender of one warp: entries go straight to the CTA's list partition, into
@@ -1692,13 +1708,20 @@ size_t range_op_bytes(const Geometry& g) {
   return (size_t)((g.R + kScanRanges - 1) / kScanRanges) * kScanRows * g.K * 2;
 }
 
-void launch_range_op(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta, const float* thr,
-                     unsigned char* ropnd, cudaStream_t st) {
-  if (scan_pair_mode())  // unscaled plain rows (the pair scan compares with per-row thresholds)
-    range_op2_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, 4), 256, 0, st>>>(
-        img, g, rmeta, reinterpret_cast<unsigned short*>(ropnd));
-  else
-    range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(img, g, rmeta, thr, ropnd);
+// Thresholds of a level (thr, padded to whole m-tiles) and, when the scan needs new ones, the
+// range operands.
+void launch_level_ops(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta,
+                      const unsigned long long* gbest, float* thr, unsigned char* ropnd, bool operands,
+                      cudaStream_t st) {
+  if (scan_pair_mode()) {  // unscaled plain rows (the pair scan compares with per-row thresholds)
+    launch_threshold(g, rmeta, gbest, thr, st);
+    if (operands)
+      range_op2_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, 4), 256, 0, st>>>(
+          img, g, rmeta, reinterpret_cast<unsigned short*>(ropnd));
+  } else {
+    range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(img, g, rmeta, gbest, thr,
+                                                                                           ropnd);
+  }
 }
 
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
