@@ -70,7 +70,7 @@ bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
 size_t range_op_bytes(const Geometry&);
 void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, const unsigned long long*, float*,
-                      unsigned char*, bool, cudaStream_t);
+                      unsigned char*, bool, unsigned long long*, unsigned*, unsigned long long*, cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
                  const double*, uint2*, unsigned long long*, int, cudaStream_t);
@@ -372,7 +372,10 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   auto* pend = static_cast<uint2*>(ws.pend.get((size_t)ws.list_cap * sizeof(uint2)));
   const int parts = scan_grid(g, stride, ws.sms);
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
-  launch_level_ops(d_img, g, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride, st);
+  const bool final_level = stride == 1;  // resets the winner slots and the self-check counter too
+  launch_level_ops(d_img, g, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride,
+                   b.cnt + kPendSlot, final_level ? b.win : nullptr, final_level ? b.cnt + kSelfcheckSlot : nullptr,
+                   st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   void* recs = ws.recs.get(scan_rec_bytes(ws.list_cap, parts));
@@ -392,8 +395,6 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
 void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, size_t level,
                    fic_mapping* d_out, cudaStream_t st) {
   unsigned long long* cnt = b.cnt + level * kPartSlots;
-  CK(cudaMemsetAsync(b.win, 0xFF, (size_t)g.R * sizeof(unsigned), st));
-  CK(cudaMemsetAsync(b.cnt + kSelfcheckSlot, 0, sizeof(unsigned long long), st));
   enqueue_level(ws, d_img, g, b, 1, cnt, st);
   const bool timed = g_timing.load() != 0;
   if (timed) CK(cudaEventRecord(ws.ev1, st));
@@ -413,7 +414,8 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   ws.list_cap = ws.list_cap_grown;
   if (const char* lc = std::getenv("FIC_LIST_CAP")) ws.list_cap = std::strtoull(lc, nullptr, 10);  // tests: force overflow
   CK(cudaMemsetAsync(d_counters, 0, 2 * g.batch * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(b.cnt, 0, kScanCountSlots * sizeof(unsigned long long), st));
+  // b.cnt: the scan kernels write their partitions' counters, range_op resets the pending and
+  // self-check slots, the host reads only the partitions a level used
   launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);  // flat domains per slice
   launch_range_pass(d_img, g, b.rm, d_counters + g.batch, st);       // shadow ranges per slice
   launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
@@ -1016,7 +1018,7 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
       } else {
         launch_decode_step(a, b, xf, out_w, kn, g.RX, part, ws.stream);
       }
-      launch_rmse_finish(part, decode_partials(out_w, p.n * scale), cnt, d_rmse + it, ws.stream);
+      launch_rmse_finish(part, decode_partials(out_w, kn), cnt, d_rmse + it, ws.stream);
       g_launches += 2;
       std::swap(a, b);
       ++runs;

@@ -608,16 +608,26 @@ __global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta
 // r_bytes each) so the scan loads them with one bulk copy per segment.
 // The level's per-range thresholds are computed here too (each CTA for its m-tile's 32
 // ranges, the blockIdx.y == 0 CTA writes them out for the scan epilogue), one launch per level.
+// It also resets the level's pending-residual counter and, for the full level (win != null),
+// the winner slots and the record self-check counter (instead of separate memsets).
 __global__ void __launch_bounds__(256)
 range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr,
-                unsigned char* __restrict__ ropnd) {
+                unsigned char* __restrict__ ropnd, unsigned long long* __restrict__ pend_count,
+                unsigned* __restrict__ win, unsigned long long* __restrict__ selfcheck) {
   __shared__ float s_thr[kScanRanges];
   if (threadIdx.x < kScanRanges) {
     const int r = blockIdx.x * kScanRanges + threadIdx.x;
     const float t = range_threshold(g, rmeta, gbest, r);
     s_thr[threadIdx.x] = t;
-    if (blockIdx.y == 0) thr[r] = t;
+    if (blockIdx.y == 0) {
+      thr[r] = t;
+      if (win && r < g.R) win[r] = 0xFFFFFFFFu;
+    }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    *pend_count = 0;
+    if (selfcheck) *selfcheck = 0;
   }
   __syncthreads();
   // blockIdx.y splits the m-tile's 256 x K/8 chunks over several CTAs
@@ -1712,15 +1722,18 @@ size_t range_op_bytes(const Geometry& g) {
 // range operands.
 void launch_level_ops(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta,
                       const unsigned long long* gbest, float* thr, unsigned char* ropnd, bool operands,
-                      cudaStream_t st) {
+                      unsigned long long* pend_count, unsigned* win, unsigned long long* selfcheck, cudaStream_t st) {
   if (scan_pair_mode()) {  // unscaled plain rows (the pair scan compares with per-row thresholds)
+    cudaMemsetAsync(pend_count, 0, sizeof(unsigned long long), st);
+    if (win) cudaMemsetAsync(win, 0xFF, (size_t)g.R * sizeof(unsigned), st);
+    if (selfcheck) cudaMemsetAsync(selfcheck, 0, sizeof(unsigned long long), st);
     launch_threshold(g, rmeta, gbest, thr, st);
     if (operands)
       range_op2_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, 4), 256, 0, st>>>(
           img, g, rmeta, reinterpret_cast<unsigned short*>(ropnd));
   } else {
-    range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(img, g, rmeta, gbest, thr,
-                                                                                           ropnd);
+    range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(
+        img, g, rmeta, gbest, thr, ropnd, pend_count, win, selfcheck);
   }
 }
 
@@ -1729,8 +1742,7 @@ void launch_eval(const unsigned char* img, const Geometry& g, const unsigned sho
                  unsigned long long part, double* res, unsigned long long* gbest, const double* deq, uint2* pend,
                  unsigned long long* pend_count, int sms, cudaStream_t st) {
   const int blocks = parts * 8;
-  const DeqTables tab{deq, deq + (1 << g.s_bits)};
-  cudaMemsetAsync(pend_count, 0, sizeof(unsigned long long), st);
+  const DeqTables tab{deq, deq + (1 << g.s_bits)};  // pend_count: reset by the level's range_op pass
   if (g.N == 4) {
     eval_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
                                            pend, pend_count);

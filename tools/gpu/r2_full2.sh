@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_gpu.log
+run() { timeout 900 env $4 python bench.py --config $1 --no-cpu-baseline --steps $2 --warmup 3 $3 > gpurun_out/bench_$1.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/bench_$1.json').read().strip().splitlines()[-1]); print('$1 $4', round(d['ms_per_step'],4), 'e2e', round(d['e2e']['encode_ms_per_image'],4), 'scan', round(d['roofline']['kernel_ms'],4), 'frac', round(d['roofline']['frac'],3), 'dec', round(d['decoder']['ms'],4), round(d['decoder']['frac'],3))"; }
+run cfg2 20; run cfg3 10; run cfg4 3; run cfg5 3 "--slices 64"
+timeout 600 python tools/kineto_gaps.py cfg2 > gpurun_out/kineto_cfg2.txt 2>&1; tail -1 gpurun_out/kineto_cfg2.txt
