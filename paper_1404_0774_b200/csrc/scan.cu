@@ -509,7 +509,7 @@ struct ScanLevel {
   int rounds;     // full rounds: m_tiles / G
   int rem;        // m-tiles of the last round: m_tiles % G
   int k;          // chunks per leftover m-tile
-  int select;     // 1, 2: keep only each range's best column per warp and tile (sparse levels; 2: small pools)
+  int select;     // sparse levels: 1, 2 each range's best column per warp and tile (2: small pools), 3 per lane and segment
   int coarse;     // 1: whole-tile |max| vote before the per-range test (large pools: rare hits)
 };
 
@@ -774,8 +774,10 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 //                 the survivor list
 // MODE: 0 full level, 1 full level with the whole-tile vote (lv.coarse), 2 sparse level with
 // the per-range test before the selection (lv.select == 1), 3 sparse level selecting from the
-// packed maxima of every range (lv.select == 2: most ranges hit in most tiles).  One
-// instantiation per mode keeps each epilogue's registers to its own path.
+// packed maxima of every range (lv.select == 2: most ranges hit in most tiles), 4 sparse level
+// keeping each lane's best per range over the whole segment (lv.select == 3: short levels of
+// small pools, one segment per m-tile).  One instantiation per mode keeps each epilogue's
+// registers to its own path.
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
@@ -905,6 +907,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                    (uint32_t)range_allpass(t.z) << (k + 2) | (uint32_t)range_allpass(t.w) << (k + 3);
       }
       const uint32_t rowbase = (uint32_t)r0 * 8u;
+      // MODE 4: each lane's running best column per range over the segment's tiles, packed as
+      // (|x| truncated to 7 mantissa bits | 7 - isometry | level tile index), flushed below
+      uint32_t lbest[MODE == 4 ? kEpiRanges : 1];
+#pragma unroll
+      for (int k = 0; k < (MODE == 4 ? kEpiRanges : 1); ++k) lbest[k] = 0u;
       for (int j = S.j0; j < S.j1; ++j, ++i) {
         const int buf = i & 1;
         const uint32_t d = dslice + (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
@@ -925,6 +932,21 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
         if (g.flags & 8) continue;                          // debug: skip the test
+        if constexpr (MODE == 4) {
+          // small pools, short sparse level: per lane and range keep the best column seen in the
+          // segment (one per tile slot, like the warp's best per tile but without any cross-lane
+          // work per tile); the threshold test is applied once, when the segment is flushed
+          const uint32_t jtag = (uint32_t)j;  // < 8192 tiles (small pools only)
+#pragma unroll
+          for (int k = 0; k < kEpiRanges; ++k) {
+            float m = 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFF0000u) | ((uint32_t)(7 - c) << 13) | jtag));
+            lbest[k] = max(lbest[k], __float_as_uint(m));
+          }
+          continue;
+        }
         if constexpr (sel) {
           // sparse level: it only has to lower the bar, so of this warp's 32 domains x 8
           // isometries of each range only the column with the largest |X~| (the smallest
@@ -1021,6 +1043,31 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
               app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
             }
           }
+        }
+      }
+      if constexpr (MODE == 4) {  // flush the segment's per-lane bests: one entry per lane and range
+#pragma unroll
+        for (int k = 0; k < kEpiRanges; ++k) {
+          const uint32_t b = lbest[k];
+          const bool keep = b != 0u && (__uint_as_float(b) > 1.0f || ((allpass >> k) & 1u));
+          const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+          if (!bal) continue;
+          if (eleft < (uint32_t)__popc(bal)) {  // pad the rest of the chunk, take a new one
+            for (uint32_t q = (uint32_t)lane; q < eleft; q += 32)
+              if (ebase + q < ecap) elist[ebase + q] = make_uint2(kSentinel, kSentinel);
+            uint32_t nb = 0;
+            if (lane == 0) nb = atomicAdd(ecount, 32u);
+            ebase = __shfl_sync(0xffffffffu, nb, 0);
+            eleft = 32;
+          }
+          const uint32_t pos = ebase + __popc(bal & ((1u << lane) - 1u));
+          if (keep && pos < ecap) {
+            const uint32_t jt = b & 0x1FFFu, s_iso = 7u - ((b >> 13) & 7u);
+            const uint32_t dd = dslice + (uint32_t)(jt * lv.stride * kScanTileDom + quarter * 32 + lane);
+            elist[pos] = make_uint2(rowbase + 8u * (uint32_t)k + s_iso, dd);
+          }
+          ebase += __popc(bal);
+          eleft -= __popc(bal);
         }
       }
     }
@@ -1646,7 +1693,8 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
   lv.stride = stride;
   {
     const char* e = std::getenv("FIC_SELECT");  // "0": sparse levels keep every survivor (A/B)
-    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? (n_tiles <= 1024 ? 2 : 1) : 0;
+    const int n_lvl = (n_tiles + stride - 1) / stride;
+    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? (n_tiles <= 1024 ? (n_lvl <= 48 ? 3 : 2) : 1) : 0;
   }
   {
     const char* e = std::getenv("FIC_COARSE");  // "0" / "1": force the whole-tile vote off / on (A/B)
@@ -1657,7 +1705,8 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
   lv.rounds = lv.m_tiles / G;
   lv.rem = lv.m_tiles % G;
   lv.k = 1;
-  if (lv.rem) {  // chunks per leftover m-tile: minimise ceil(rem * k / G) / k, prefer small k
+  // (select == 3 keeps per-lane bests over a segment: whole m-tiles, one segment each)
+  if (lv.rem && lv.select != 3) {  // chunks per leftover m-tile: minimise ceil(rem * k / G) / k, prefer small k
     double best = 1e30;
     for (int k = 1; k <= 16 && k <= lv.n_lvl; ++k) {
       const double t = (double)((lv.rem * k + G - 1) / G) / k;
@@ -1693,8 +1742,12 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   }
   const ScanLevel lv = make_level(g, stride, grid);
   const ScanSmem L = scan_smem_layout(g.K);
-  const int mode = lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0));
-  auto kern = mode == 3 ? scan_kernel<3> : (mode == 2 ? scan_kernel<2> : (mode == 1 ? scan_kernel<1> : scan_kernel<0>));
+  const int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
+  auto kern = mode == 4 ? scan_kernel<4>
+              : mode == 3 ? scan_kernel<3>
+              : mode == 2 ? scan_kernel<2>
+              : mode == 1 ? scan_kernel<1>
+                          : scan_kernel<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const unsigned long long rcap = scan_rec_part(part);
