@@ -1694,7 +1694,11 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
   {
     const char* e = std::getenv("FIC_SELECT");  // "0": sparse levels keep every survivor (A/B)
     const int n_lvl = (n_tiles + stride - 1) / stride;
-    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0) ? (n_tiles <= 1024 ? (n_lvl <= 48 ? 3 : 2) : 1) : 0;
+    const char* lb = std::getenv("FIC_LANEBEST_MAX");  // longest level (tiles) using per-lane bests
+    const int lane_best_max = lb ? std::atoi(lb) : 48;
+    lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0)
+                    ? (n_tiles <= 1024 ? (n_lvl <= lane_best_max ? 3 : 2) : 1)
+                    : 0;
   }
   {
     const char* e = std::getenv("FIC_COARSE");  // "0" / "1": force the whole-tile vote off / on (A/B)
