@@ -61,6 +61,7 @@ typedef uint2 SurvEntry;
 // write the tile's fp16 operand (UMMA K-major no-swizzle core matrices, 16-byte coalesced
 // chunks: [domain/8][k/8][domain%8][8 halves]) and the exact u16 q rows.
 constexpr int kPoolThreads = 512;
+static_assert(kPoolThreads == 4 * kPoolBlock, "pool moments: four threads per domain");
 
 __global__ void __launch_bounds__(kPoolThreads)
 pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __restrict__ upool,
@@ -69,6 +70,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   extern __shared__ __align__(16) unsigned short sq_tile[];  // 128 x N contracted cells
   __shared__ double s_inv[kPoolBlock];
   __shared__ long long s_sum[kPoolBlock];
+  __shared__ long long s_sqq[kPoolBlock];
   __shared__ unsigned char s_perm[kSyms * 64];
   __shared__ unsigned s_flat;
   const int t = threadIdx.x;
@@ -100,14 +102,28 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   }
   __syncthreads();
   // moments of domain t: Sq, Sqq, den = N*Sqq - Sq^2 (exact), flat iff (double)den <= 16*shadow_eps (encoder.cpp:223)
-  if (t < kPoolBlock) {
-    const long long d = dbase + t;
+  // (kPoolThreads / kPoolBlock = 4 threads per domain, partial sums combined by shuffles)
+  {
+    const int dl = t >> 2, part = t & 3;
     long long s = 0, ss = 0;
-    for (int j = 0; j < N; ++j) {
-      const int v = sq_tile[t * N + ((j + t) % N)];  // rotated start: fewer bank conflicts
+    for (int j = part; j < N; j += 4) {
+      const int v = sq_tile[dl * N + ((j + dl) % N)];  // rotated start: fewer bank conflicts
       s += v;
       ss += (long long)v * v;
     }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    if (part == 0) {
+      s_sum[dl] = s;
+      s_sqq[dl] = ss;
+    }
+  }
+  __syncthreads();
+  if (t < kPoolBlock) {
+    const long long d = dbase + t;
+    const long long s = s_sum[t], ss = s_sqq[t];
     if (lbase + t < g.D) {
       const long long den = (long long)N * ss - s * s;
       const bool flat = (double)den <= 16.0 * g.shadow_eps;
