@@ -179,6 +179,11 @@ int32_t fic_decode_timing(double* avg_ms, double* avg_bytes, uint64_t* calls, in
 /* Survivors (candidates passing the tensor-core bound) per scan level of the calling
  * process's last tcgen05-path encode; returns the number of levels (0 for the CUDA-core path). */
 int32_t fic_last_survivors(uint64_t* counts, int32_t max_levels);
+/* (diagnostics) clock64 stamps of scan CTA 0's first 256 tiles recorded under FIC_DEBUG=32:
+ * per tile 51 slots (MMA issuer before/after the TMEM-buffer wait and after the pool tile landed,
+ * each of the 16 epilogue warps releasing the tile, finishing it, and past its per-range test).
+ * Copies up to n values. */
+int32_t fic_debug_trace(int64_t* out, int32_t n);
 
 #ifdef __cplusplus
 }

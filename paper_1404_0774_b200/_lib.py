@@ -43,6 +43,7 @@ def _declare(L):
     L.fic_set_matcher_timing.argtypes = [i32]
     L.fic_scan_timing.argtypes = [vp, vp, i32]
     L.fic_last_survivors.argtypes = [vp, i32]
+    L.fic_debug_trace.argtypes = [vp, i32]
     L.fic_decode_timing.argtypes = [vp, vp, vp, i32]
     L.fic_set_device.argtypes = [i32]
     L.fic_device_count.argtypes = [vp]
@@ -50,7 +51,7 @@ def _declare(L):
                  "fic_encode_range", "fic_encode_rows", "fic_encode_batch", "fic_encode_device",
                  "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
-                 "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device"]:
+                 "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace"]:
         getattr(L, name).restype = i32
     return L
 
@@ -76,4 +77,5 @@ EXPORTS = [
     "fic_encode_device", "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
     "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
+    "fic_debug_trace",
 ]

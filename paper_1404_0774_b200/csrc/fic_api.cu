@@ -65,6 +65,7 @@ cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const _
                         const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long, void*,
                         unsigned long long*, cudaStream_t);
 size_t scan_rec_bytes(unsigned long long, int);
+int scan_trace_copy(long long*, int);
 int scan_padded_ranges(const Geometry&);
 bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
@@ -1125,6 +1126,15 @@ int32_t fic_matcher_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
 }
 
 void fic_set_matcher_timing(int32_t enabled) { g_timing.store(enabled ? 1 : 0); }
+
+int32_t fic_debug_trace(int64_t* out, int32_t n) {
+  if (!out || n < 0) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  return guarded([&]() -> int32_t {
+    const int m = scan_trace_copy(reinterpret_cast<long long*>(out), n);
+    if (m < 0) return fail(FIC_ERR_CUDA, "trace copy failed");
+    return FIC_OK;
+  });
+}
 
 int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
   std::lock_guard<std::mutex> lock(g_timing_mu);

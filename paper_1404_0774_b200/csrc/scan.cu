@@ -490,6 +490,25 @@ seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned
   publish_best(gbest, r, v);
 }
 
+// ------------------------------------------------------------------ pipeline trace
+// FIC_DEBUG bit 5 (32): scan CTA 0 records clock64() stamps of its first kTraceTiles tiles:
+// [tile][0..2] the MMA issuer before / after waiting for the TMEM buffer and after the pool tile
+// landed, [tile][3 + e] epilogue warp e releasing the tile, [tile][19 + e] warp e done with it,
+// [tile][35 + e] warp e past the per-range test (full level).
+// Read with fic_debug_trace (tools/trace.py).
+constexpr int kTraceTiles = 256;
+constexpr int kTraceSlots = 51;
+__device__ long long g_trace[kTraceTiles * kTraceSlots];
+
+__device__ __forceinline__ void trace_stamp(const Geometry& g, int tile, int slot) {
+  if ((g.flags & 32) && blockIdx.x == 0 && tile < kTraceTiles) g_trace[tile * kTraceSlots + slot] = clock64();
+}
+
+int scan_trace_copy(long long* out, int n) {
+  const int m = n < kTraceTiles * kTraceSlots ? n : kTraceTiles * kTraceSlots;
+  return cudaMemcpyFromSymbol(out, g_trace, (size_t)m * sizeof(long long)) == cudaSuccess ? m : -1;
+}
+
 // ------------------------------------------------------------------ K2: tensor-core scan
 struct ScanSmem {
   uint32_t r_bytes, p_bytes, stages, r_off, p_off, bar_off, wbuf_off, total;
@@ -881,8 +900,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         for (int j = S.j0; j < S.j1; ++j, ++i) {
           const int s = i % stages;
           const int buf = i & 1;
+          trace_stamp(g, i, 0);
           ptx::mbar_wait(&tempty_bar[buf], ((i >> 1) & 1) ^ 1);
+          trace_stamp(g, i, 1);
           ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
+          trace_stamp(g, i, 2);
           ptx::tc_fence_after();
           const uint32_t p_base = ptx::smem_addr(sP + s * L.p_bytes);
           if (!(g.flags & 16)) {  // debug: flags & 16 skips the MMAs
@@ -930,6 +952,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       for (int k = 0; k < (MODE == 4 ? kEpiRanges : 1); ++k) lbest[k] = 0u;
       for (int j = S.j0; j < S.j1; ++j, ++i) {
         const int buf = i & 1;
+        if (lane == 0 && i > 0) trace_stamp(g, i - 1, 19 + e);  // done with the previous tile
         const uint32_t d = dslice + (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
         ptx::mbar_wait_sleep(&tfull_bar[buf], (i >> 1) & 1);
         ptx::tc_fence_after();
@@ -946,7 +969,10 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
+        if (lane == 0) {
+          ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
+          trace_stamp(g, i, 3 + e);
+        }
         if (g.flags & 8) continue;                          // debug: skip the test
         if constexpr (MODE == 4) {
           // small pools, short sparse level: per lane and range keep the best column seen in the
@@ -1043,6 +1069,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           gmask |= (uint32_t)(gm > 1.0f) << k;
         }
         const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+        if (lane == 0) trace_stamp(g, i, 35 + e);
         if (groups) {
           // ranges with a hit in some lane of the warp, one warp-uniform branch per range, so
           // only the hit ranges' column bits are formed (8 compares each)
@@ -1056,7 +1083,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
 #pragma unroll
                 for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
               }
-              app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
+              if (!(g.flags & 64)) app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);  // 64: timing only
             }
           }
         }

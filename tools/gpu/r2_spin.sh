@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+for L in libfic_b200.so libfic_b200_spin.so; do
+for c in cfg2 cfg3 cfg4; do
+st=20; [ $c = cfg4 ] && st=3
+FIC_LIB=$PWD/paper_1404_0774_b200/$L timeout 600 python bench.py --config $c --no-cpu-baseline --steps $st > gpurun_out/b.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]); print('$L $c', round(d['ms_per_step'],4), round(d['roofline']['kernel_ms'],4))"
+done; done
