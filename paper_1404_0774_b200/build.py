@@ -17,7 +17,7 @@ HEADERS = ["common.cuh", "tc_ptx.cuh", "tc2_ptx.cuh", os.path.join("..", "..", "
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + (["-DFIC_TRACE"] if os.environ.get("FIC_TRACE") else [])  # pipeline trace build
 
 
 def _stale():

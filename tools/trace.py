@@ -1,6 +1,8 @@
 """Per-tile pipeline timeline of scan CTA 0 (FIC_DEBUG=32, read with fic_debug_trace): how long
 the MMA issuer waited for a TMEM buffer / a pool tile, the tile period, and how long the
-epilogue warps took per tile.  GPU analysis tool: python tools/trace.py cfg2 [levels]."""
+epilogue warps took per tile.  GPU analysis tool; needs a trace build of the library:
+    FIC_TRACE=1 FIC_LIB=$PWD/paper_1404_0774_b200/libfic_trace.so python -m paper_1404_0774_b200.build
+    FIC_LIB=$PWD/paper_1404_0774_b200/libfic_trace.so python tools/trace.py cfg2 [extra FIC_DEBUG bits]"""
 import ctypes
 import os
 import sys
