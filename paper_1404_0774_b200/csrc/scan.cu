@@ -882,17 +882,22 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       }
     }
     if (lane == 0) {
-      int i = 0;
+      int s = 0;
+      uint32_t ring_phase = 0;
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, cta, G, sg);
         // the segment's slice pool (batched encodes: slice b's domains start at b * Dt)
         const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) +
                                    (long long)range_slice(g, S.m * kScanRanges) * g.Dt * K * 2;
-        for (int j = S.j0; j < S.j1; ++j, ++i) {
-          const int s = i % stages;
-          ptx::mbar_wait(&empty_bar[s], ((i / stages) & 1) ^ 1);
+        const long long step_bytes = (long long)lv.stride * L.p_bytes;
+        for (int j = S.j0; j < S.j1; ++j) {
+          ptx::mbar_wait(&empty_bar[s], ring_phase ^ 1u);
           ptx::mbar_arrive_expect_tx(&full_bar[s], L.p_bytes);
-          ptx::bulk_g2s(sP + s * L.p_bytes, src + (long long)j * lv.stride * L.p_bytes, L.p_bytes, &full_bar[s]);
+          ptx::bulk_g2s(sP + s * L.p_bytes, src + (long long)j * step_bytes, L.p_bytes, &full_bar[s]);
+          if (++s == stages) {
+            s = 0;
+            ring_phase ^= 1u;
+          }
         }
       }
     }
@@ -900,31 +905,38 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     // ================= MMA issuer =================
     if (lane == 0) {
       const uint32_t idesc = ptx::idesc_f16_f32(128, kScanRows);
-      int i = 0;
+      const bool do_mma = !(g.flags & 16);  // debug: flags & 16 skips the MMAs
+      // descriptors: the start address field (bits 0-13, 16-byte units) advances by 16 per
+      // K=16 step (256 bytes) and by p_bytes/16 per ring stage; everything else is constant
+      const uint64_t p_desc0 = ptx::smem_desc(ptx::smem_addr(sP), 128, K * 16);
+      const uint32_t p_stage = L.p_bytes >> 4;
+      int i = 0, s = 0;
+      uint32_t ring_phase = 0;  // phase of full_bar[s] for the current pass over the ring
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, cta, G, sg);
         ptx::mbar_wait(&rfull_bar[sg & 1], (sg >> 1) & 1);
-        const uint32_t r_base = ptx::smem_addr(sR + (sg & 1) * L.r_bytes);
+        const uint64_t r_desc = ptx::smem_desc(ptx::smem_addr(sR + (sg & 1) * L.r_bytes), 128, K * 16);
         for (int j = S.j0; j < S.j1; ++j, ++i) {
-          const int s = i % stages;
           const int buf = i & 1;
           trace_stamp(g, i, 0);
           ptx::mbar_wait(&tempty_bar[buf], ((i >> 1) & 1) ^ 1);
           trace_stamp(g, i, 1);
-          ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
+          ptx::mbar_wait(&full_bar[s], ring_phase);
           trace_stamp(g, i, 2);
           ptx::tc_fence_after();
-          const uint32_t p_base = ptx::smem_addr(sP + s * L.p_bytes);
-          if (!(g.flags & 16)) {  // debug: flags & 16 skips the MMAs
-#pragma unroll 1
-            for (int kk = 0; kk < K / 16; ++kk) {
-              const uint64_t ad = ptx::smem_desc(p_base + kk * 256, 128, K * 16);
-              const uint64_t bd = ptx::smem_desc(r_base + kk * 256, 128, K * 16);
-              ptx::mma_f16_ss(tmem_base + buf * kScanRows, ad, bd, idesc, kk > 0 ? 1u : 0u);
-            }
+          if (do_mma) {
+            const uint64_t ad0 = p_desc0 + (uint64_t)(s * p_stage);
+            const uint32_t d_tmem = tmem_base + buf * kScanRows;
+            ptx::mma_f16_ss(d_tmem, ad0, r_desc, idesc, 0u);
+            for (int kk = 1; kk < K / 16; ++kk)
+              ptx::mma_f16_ss(d_tmem, ad0 + (uint64_t)(kk * 16), r_desc + (uint64_t)(kk * 16), idesc, 1u);
           }
           ptx::tc_commit(&empty_bar[s]);
           ptx::tc_commit(&tfull_bar[buf]);
+          if (++s == stages) {
+            s = 0;
+            ring_phase ^= 1u;
+          }
         }
         ptx::tc_commit(&rempty_bar[sg & 1]);
       }
