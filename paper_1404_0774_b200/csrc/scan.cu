@@ -1534,16 +1534,21 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
   if (warp == 0) {
     // ================= producer: this CTA's half of every tile =================
     if (lane == 0) {
-      int i = 0;
+      int s = 0;
+      uint32_t ring_phase = 0;
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, pair, G, sg);
         const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) + (size_t)rank * L.p_bytes +
                                    (long long)range_slice(g, S.m * kScanRanges) * g.Dt * K * 2;
-        for (int j = S.j0; j < S.j1; ++j, ++i) {
-          const int s = i % stages;
-          ptx::mbar_wait(&empty_bar[s], ((i / stages) & 1) ^ 1);
+        const long long step_bytes = (long long)lv.stride * 2 * L.p_bytes;
+        for (int j = S.j0; j < S.j1; ++j) {
+          ptx::mbar_wait(&empty_bar[s], ring_phase ^ 1u);
           ptx::mbar_arrive_expect_tx(&full_bar[s], L.p_bytes);
-          ptx::bulk_g2s(sP + s * L.p_bytes, src + (size_t)j * lv.stride * 2 * L.p_bytes, L.p_bytes, &full_bar[s]);
+          ptx::bulk_g2s(sP + s * L.p_bytes, src + (long long)j * step_bytes, L.p_bytes, &full_bar[s]);
+          if (++s == stages) {
+            s = 0;
+            ring_phase ^= 1u;
+          }
         }
       }
     }
@@ -1551,41 +1556,54 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
     if (lane == 0 && rank == 0) {
       // ================= MMA issuer (even CTA) =================
       const uint32_t idesc = ptx::idesc_f16_f32(256, kP2Dom);
-      int i = 0;
+      const bool do_mma = !(g.flags & 16);
+      const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_addr(sP), 128, K * 16);
+      const uint32_t p_stage = L.p_bytes >> 4;
+      int s = 0, buf = 0;
+      uint32_t ring_phase = 0, buf_phase = 0;
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, pair, G, sg);
         ptx::mbar_wait_cluster(&afull_bar[sg & 1], (sg >> 1) & 1);
         const uint32_t a_base = tb + kP2ACol + (uint32_t)(sg & 1) * a_cols;
-        for (int j = S.j0; j < S.j1; ++j, ++i) {
-          const int s = i % stages;
-          const int buf = i % kP2Bufs;
-          ptx::mbar_wait_cluster(&tempty_bar[buf], ((i / kP2Bufs) & 1) ^ 1);
-          ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
-          ptx::mbar_wait_cluster(&pfull_bar[s], (i / stages) & 1);
+        for (int j = S.j0; j < S.j1; ++j) {
+          ptx::mbar_wait_cluster(&tempty_bar[buf], buf_phase ^ 1u);
+          ptx::mbar_wait(&full_bar[s], ring_phase);
+          ptx::mbar_wait_cluster(&pfull_bar[s], ring_phase);
           ptx::tc_fence_after();
-          const uint32_t b_base = ptx::smem_addr(sP + s * L.p_bytes);
-          if (!(g.flags & 16)) {
-#pragma unroll 1
-            for (int kk = 0; kk < K / 16; ++kk) {
-              const uint64_t bd = ptx::smem_desc(b_base + kk * 256, 128, K * 16);
-              ptx::mma_f16_ts_2sm(tb + buf * kP2AccCols, a_base + kk * 8, bd, idesc, kk > 0 ? 1u : 0u);
-            }
+          if (do_mma) {
+            const uint64_t bd0 = b_desc0 + (uint64_t)(s * p_stage);
+            const uint32_t d_tmem = tb + buf * kP2AccCols;
+            ptx::mma_f16_ts_2sm(d_tmem, a_base, bd0, idesc, 0u);
+            for (int kk = 1; kk < K / 16; ++kk)
+              ptx::mma_f16_ts_2sm(d_tmem, a_base + kk * 8, bd0 + (uint64_t)(kk * 16), idesc, 1u);
           }
           ptx::tc_commit_2sm_mc(&empty_bar[s], 0x3);
           ptx::tc_commit_2sm_mc(&tfull_bar[buf], 0x3);
+          if (++s == stages) {
+            s = 0;
+            ring_phase ^= 1u;
+          }
+          if (++buf == kP2Bufs) {
+            buf = 0;
+            buf_phase ^= 1u;
+          }
         }
         ptx::tc_commit_2sm_mc(&aempty_bar[sg & 1], 0x3);
       }
     } else if (lane == 0) {
       // ================= relay (odd CTA): my half landed -> even CTA's pfull =================
       const uint32_t remote = ptx::leader_addr(ptx::smem_addr(pfull_bar));
-      int i = 0;
+      int s = 0;
+      uint32_t ring_phase = 0;
       for (int sg = 0; sg < nseg; ++sg) {
         const Segment S = seg_at(lv, pair, G, sg);
-        for (int j = S.j0; j < S.j1; ++j, ++i) {
-          const int s = i % stages;
-          ptx::mbar_wait(&full_bar[s], (i / stages) & 1);
+        for (int j = S.j0; j < S.j1; ++j) {
+          ptx::mbar_wait(&full_bar[s], ring_phase);
           ptx::mbar_arrive_cluster(remote + s * 8);
+          if (++s == stages) {
+            s = 0;
+            ring_phase ^= 1u;
+          }
         }
       }
     }
