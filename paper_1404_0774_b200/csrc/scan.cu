@@ -928,8 +928,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             const uint64_t ad0 = p_desc0 + (uint64_t)(s * p_stage);
             const uint32_t d_tmem = tmem_base + buf * kScanRows;
             ptx::mma_f16_ss(d_tmem, ad0, r_desc, idesc, 0u);
-            for (int kk = 1; kk < K / 16; ++kk)
-              ptx::mma_f16_ss(d_tmem, ad0 + (uint64_t)(kk * 16), r_desc + (uint64_t)(kk * 16), idesc, 1u);
+            if (K == 64) {  // n = 8: four K=16 steps, unrolled (K is 16 otherwise)
+              ptx::mma_f16_ss(d_tmem, ad0 + 16u, r_desc + 16u, idesc, 1u);
+              ptx::mma_f16_ss(d_tmem, ad0 + 32u, r_desc + 32u, idesc, 1u);
+              ptx::mma_f16_ss(d_tmem, ad0 + 48u, r_desc + 48u, idesc, 1u);
+            }
           }
           ptx::tc_commit(&empty_bar[s]);
           ptx::tc_commit(&tfull_bar[buf]);
