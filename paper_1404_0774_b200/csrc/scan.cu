@@ -903,7 +903,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    if (lane == 0) {
+    // The whole warp runs the loop (all its values warp-uniform); one elected lane issues the
+    // MMAs and commits.  The issuing thread is on the scan's critical path.
+    {
       const uint32_t idesc = ptx::idesc_f16_f32(128, kScanRows);
       const bool do_mma = !(g.flags & 16);  // debug: flags & 16 skips the MMAs
       // descriptors: the start address field (bits 0-13, 16-byte units) advances by 16 per
@@ -924,24 +926,28 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           ptx::mbar_wait(&full_bar[s], ring_phase);
           trace_stamp(g, i, 2);
           ptx::tc_fence_after();
-          if (do_mma) {
-            const uint64_t ad0 = p_desc0 + (uint64_t)(s * p_stage);
-            const uint32_t d_tmem = tmem_base + buf * kScanRows;
-            ptx::mma_f16_ss(d_tmem, ad0, r_desc, idesc, 0u);
-            if (K == 64) {  // n = 8: four K=16 steps, unrolled (K is 16 otherwise)
-              ptx::mma_f16_ss(d_tmem, ad0 + 16u, r_desc + 16u, idesc, 1u);
-              ptx::mma_f16_ss(d_tmem, ad0 + 32u, r_desc + 32u, idesc, 1u);
-              ptx::mma_f16_ss(d_tmem, ad0 + 48u, r_desc + 48u, idesc, 1u);
+          if (ptx::elect_one()) {
+            if (do_mma) {
+              const uint64_t ad0 = p_desc0 + (uint64_t)(s * p_stage);
+              const uint32_t d_tmem = tmem_base + buf * kScanRows;
+              ptx::mma_f16_ss(d_tmem, ad0, r_desc, idesc, 0u);
+              if (K == 64) {  // n = 8: four K=16 steps, unrolled (K is 16 otherwise)
+                ptx::mma_f16_ss(d_tmem, ad0 + 16u, r_desc + 16u, idesc, 1u);
+                ptx::mma_f16_ss(d_tmem, ad0 + 32u, r_desc + 32u, idesc, 1u);
+                ptx::mma_f16_ss(d_tmem, ad0 + 48u, r_desc + 48u, idesc, 1u);
+              }
             }
+            ptx::tc_commit(&empty_bar[s]);
+            ptx::tc_commit(&tfull_bar[buf]);
           }
-          ptx::tc_commit(&empty_bar[s]);
-          ptx::tc_commit(&tfull_bar[buf]);
+          __syncwarp();
           if (++s == stages) {
             s = 0;
             ring_phase ^= 1u;
           }
         }
-        ptx::tc_commit(&rempty_bar[sg & 1]);
+        if (ptx::elect_one()) ptx::tc_commit(&rempty_bar[sg & 1]);
+        __syncwarp();
       }
     }
   } else {

@@ -59,6 +59,20 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
+// One lane of the (converged) warp: elect.sync.  The caller's values stay warp-uniform, so the
+// compiler keeps tcgen05 operands in uniform registers instead of broadcasting them per issue.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // 1-D bulk copy global -> shared, completion counted on `bar` (UBLKCP in SASS).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
