@@ -1562,8 +1562,8 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ================= MMA issuer (even CTA) =================
+    if (rank == 0) {
+      // ================= MMA issuer (even CTA): whole-warp loop, elected lane issues =================
       const uint32_t idesc = ptx::idesc_f16_f32(256, kP2Dom);
       const bool do_mma = !(g.flags & 16);
       const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_addr(sP), 128, K * 16);
@@ -1579,15 +1579,21 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
           ptx::mbar_wait(&full_bar[s], ring_phase);
           ptx::mbar_wait_cluster(&pfull_bar[s], ring_phase);
           ptx::tc_fence_after();
-          if (do_mma) {
-            const uint64_t bd0 = b_desc0 + (uint64_t)(s * p_stage);
-            const uint32_t d_tmem = tb + buf * kP2AccCols;
-            ptx::mma_f16_ts_2sm(d_tmem, a_base, bd0, idesc, 0u);
-            for (int kk = 1; kk < K / 16; ++kk)
-              ptx::mma_f16_ts_2sm(d_tmem, a_base + kk * 8, bd0 + (uint64_t)(kk * 16), idesc, 1u);
+          if (ptx::elect_one()) {
+            if (do_mma) {
+              const uint64_t bd0 = b_desc0 + (uint64_t)(s * p_stage);
+              const uint32_t d_tmem = tb + buf * kP2AccCols;
+              ptx::mma_f16_ts_2sm(d_tmem, a_base, bd0, idesc, 0u);
+              if (K == 64) {
+                ptx::mma_f16_ts_2sm(d_tmem, a_base + 8, bd0 + 16u, idesc, 1u);
+                ptx::mma_f16_ts_2sm(d_tmem, a_base + 16, bd0 + 32u, idesc, 1u);
+                ptx::mma_f16_ts_2sm(d_tmem, a_base + 24, bd0 + 48u, idesc, 1u);
+              }
+            }
+            ptx::tc_commit_2sm_mc(&empty_bar[s], 0x3);
+            ptx::tc_commit_2sm_mc(&tfull_bar[buf], 0x3);
           }
-          ptx::tc_commit_2sm_mc(&empty_bar[s], 0x3);
-          ptx::tc_commit_2sm_mc(&tfull_bar[buf], 0x3);
+          __syncwarp();
           if (++s == stages) {
             s = 0;
             ring_phase ^= 1u;
@@ -1597,7 +1603,8 @@ scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const u
             buf_phase ^= 1u;
           }
         }
-        ptx::tc_commit_2sm_mc(&aempty_bar[sg & 1], 0x3);
+        if (ptx::elect_one()) ptx::tc_commit_2sm_mc(&aempty_bar[sg & 1], 0x3);
+        __syncwarp();
       }
     } else if (lane == 0) {
       // ================= relay (odd CTA): my half landed -> even CTA's pfull =================
