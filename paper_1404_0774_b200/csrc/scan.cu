@@ -48,7 +48,6 @@ constexpr int kEpiRanges = kScanRanges / kEpiParts;    // ranges per epilogue th
 constexpr int kEpiCols = kEpiRanges * kSyms;           // TMEM columns per epilogue thread
 constexpr int kScanThreads = (2 + kScanEpiWarps) * 32;
 constexpr uint32_t kScanTmemCols = 512;
-constexpr int kWarpBuf = 64;                    // survivor staging entries per epilogue warp
 constexpr int kSmemBudget = 220 * 1024;
 
 // Survivor list entry: (encoded range r * 8 + isometry, canonical domain).
