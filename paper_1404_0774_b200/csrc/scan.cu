@@ -1078,13 +1078,17 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         if (MODE == 1 && !allpass) {
           // large pools, hits in ~2% of warp-tiles: one |max| over all 64 columns (32 FMNMX3)
           // and a warp vote first; the per-range breakdown only for the rare tiles with a hit
-          float m0 = 0.f, m1 = 0.f;
+          // four independent FMNMX3 chains (8 deep instead of 16: the test's latency, not its
+          // instruction count, is what the MMA waits on)
+          float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
 #pragma unroll
-          for (int c = 0; c < kEpiCols; c += 4) {
+          for (int c = 0; c < kEpiCols; c += 8) {
             m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
             m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[c + 2])), fabsf(__uint_as_float(v[c + 3]))));
+            m2 = fmaxf(m2, fmaxf(fabsf(__uint_as_float(v[c + 4])), fabsf(__uint_as_float(v[c + 5]))));
+            m3 = fmaxf(m3, fmaxf(fabsf(__uint_as_float(v[c + 6])), fabsf(__uint_as_float(v[c + 7]))));
           }
-          if (!__any_sync(0xffffffffu, fmaxf(m0, m1) > 1.0f)) continue;
+          if (!__any_sync(0xffffffffu, fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > 1.0f)) continue;
         }
         // |max| of each range's 8 isometry columns (4 FMNMX3 each); mask of ranges above 1
         uint32_t gmask = allpass;
