@@ -564,7 +564,10 @@ void enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geome
 // counters[b] = flat domains and counters[batch + b] = shadow ranges of slice b (copied to
 // h_counters; batch == 1 for a single image).
 void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in, fic_mapping* d_out,
-                unsigned long long* d_counters, unsigned long long* h_counters, cudaStream_t st) {
+                unsigned long long* d_counters, unsigned long long* h_counters, cudaStream_t st,
+                fic_mapping* h_out = nullptr) {
+  // h_out: the records are also copied to this (pinned) host buffer before the one synchronisation
+  // (again after an overflow re-run), so a host-API encode waits for the device once
   Geometry g = g_in;
   if (g.Dt == 0) g.Dt = (int)scan_pool_domains(g);  // per-slice pool stride (a multiple of 896)
   if (matcher_mode(g) == 0) {
@@ -572,6 +575,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
     enqueue_encode_simt(ws, d_img, g, d_out, d_counters, st);
     if (h_counters)
       CK(cudaMemcpyAsync(h_counters, d_counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    if (h_out) CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return;
   }
@@ -584,6 +588,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
     if (h_counters)
       CK(cudaMemcpyAsync(h_counters, d_counters, 2 * g.batch * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                          st));
+    if (h_out) CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const std::vector<int> lv = scan_levels(g);
     const int fparts = scan_grid(g, 1, ws.sms);
@@ -720,9 +725,7 @@ int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, f
     auto* h_out = static_cast<fic_mapping*>(ws.h_out.get((size_t)g.R * sizeof(fic_mapping)));
     auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * g.batch * sizeof(unsigned long long)));
     CK(cudaMemcpyAsync(d_img, h_img, img_bytes, cudaMemcpyHostToDevice, ws.stream));
-    run_encode(ws, d_img, g, d_out, d_cnt, h_cnt, ws.stream);
-    CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, ws.stream));
-    CK(cudaStreamSynchronize(ws.stream));
+    run_encode(ws, d_img, g, d_out, d_cnt, h_cnt, ws.stream, h_out);  // records copied before its one sync
     collect_timing(ws);
     std::memcpy(out, h_out, (size_t)g.R * sizeof(fic_mapping));
     if (g.batch > 1)
