@@ -1348,12 +1348,11 @@ __global__ void winner_kernel(const SurvEntry* __restrict__ list, const unsigned
   for (unsigned long long j = (unsigned long long)sub * blockDim.x + threadIdx.x; j < n;
        j += (unsigned long long)per * blockDim.x) {
     const unsigned long long i = (unsigned long long)c * part + j;
+    const double R = res[i];  // +inf for screened-out entries and sentinels (most of them)
+    if (!(R < __longlong_as_double(0x7ff0000000000000ll))) continue;
     const SurvEntry en = list[i];
-    if (en.x == kSentinel) continue;
     const int r = (int)(en.x >> 3);
-    const double R = res[i];
-    if (R < __longlong_as_double(0x7ff0000000000000ll) && (unsigned long long)__double_as_longlong(R) == gbest[r])
-      atomicMin(win + r, en.y * 8u + (en.x & 7u));
+    if ((unsigned long long)__double_as_longlong(R) == gbest[r]) atomicMin(win + r, en.y * 8u + (en.x & 7u));
   }
 }
 
@@ -1917,7 +1916,7 @@ void launch_eval(const unsigned char* img, const Geometry& g, const unsigned sho
 
 void launch_winner(const SurvEntry* list, const unsigned long long* counts, int parts, unsigned long long part,
                    const double* res, const unsigned long long* gbest, unsigned* win, int sms, cudaStream_t st) {
-  winner_kernel<<<parts * 4, 256, 0, st>>>(list, counts, parts, part, res, gbest, win);
+  winner_kernel<<<parts * 16, 256, 0, st>>>(list, counts, parts, part, res, gbest, win);
 }
 
 void launch_record(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
