@@ -462,31 +462,46 @@ seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned
                const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
                unsigned long long* __restrict__ gbest, DeqTables tab) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)g.R * kSeedPerRange) return;
-  const int r = (int)(tid / kSeedPerRange), k = (int)(tid % kSeedPerRange);
+  const bool in = tid < (long long)g.R * kSeedPerRange && g.D > 0;
+  const int r = in ? (int)(tid / kSeedPerRange) : -1, k = (int)(tid % kSeedPerRange);
   const int s = k % kSyms, w = k / kSyms;
-  if (g.D == 0) return;
-  int x0, y0;
-  range_origin(g, r, x0, y0);
-  const int b = range_slice(g, r);
-  const int cx = x0 - g.n / 2, cy = y0 - b * g.H1 - g.n / 2;  // slice-local
-  const int xi0 = min(max(cx / g.step, 0), g.PX - 1), yi0 = min(max(cy / g.step, 0), g.PY - 1);
-  const int xi = xi0 + w / kSeedSide - kSeedHalf, yi = yi0 + w % kSeedSide - kSeedHalf;
-  if (xi < 0 || yi < 0 || xi >= g.PX || yi >= g.PY) return;
-  const int d = b * g.Dt + xi * g.PY + yi;
-  // all operand loads depend only on (r, d, s): issued together, one memory round trip
-  const RangeMeta m = rmeta[r];
-  const DomainMetaI mi = meta_i[d];
-  uint32_t qw[NN / 2], bpk[NN / 4];
-  load_q8_row<NN>(qpool, d, s, qw);
-  load_range_words<NN>(img, g, x0, y0, bpk);
-  if (m.shadow || mi.den < 0) return;
-  unsigned qs, qo;
-  // an upper bound of the candidate's exact residual is a valid pruning bar
-  const double v = eval_fast<NN>(g, qw, bpk, m.sb, (double)m.var / (double)NN, mi.sq, mi.den,
-                                 __longlong_as_double(0x7ff0000000000000ll), false, true, tab, qpool, img, d, s, x0,
-                                 y0, qs, qo);
-  publish_best(gbest, r, v);
+  unsigned long long key = 0x7ff0000000000000ull;  // +inf
+  if (in) {
+    int x0, y0;
+    range_origin(g, r, x0, y0);
+    const int b = range_slice(g, r);
+    const int cx = x0 - g.n / 2, cy = y0 - b * g.H1 - g.n / 2;  // slice-local
+    const int xi0 = min(max(cx / g.step, 0), g.PX - 1), yi0 = min(max(cy / g.step, 0), g.PY - 1);
+    const int xi = xi0 + w / kSeedSide - kSeedHalf, yi = yi0 + w % kSeedSide - kSeedHalf;
+    if (xi >= 0 && yi >= 0 && xi < g.PX && yi < g.PY) {
+      const int d = b * g.Dt + xi * g.PY + yi;
+      // all operand loads depend only on (r, d, s): issued together, one memory round trip
+      const RangeMeta m = rmeta[r];
+      const DomainMetaI mi = meta_i[d];
+      uint32_t qw[NN / 2], bpk[NN / 4];
+      load_q8_row<NN>(qpool, d, s, qw);
+      load_range_words<NN>(img, g, x0, y0, bpk);
+      if (!m.shadow && mi.den >= 0) {
+        unsigned qs, qo;
+        // an upper bound of the candidate's exact residual is a valid pruning bar
+        const double v = eval_fast<NN>(g, qw, bpk, m.sb, (double)m.var / (double)NN, mi.sq, mi.den,
+                                       __longlong_as_double(0x7ff0000000000000ll), false, true, tab, qpool, img, d,
+                                       s, x0, y0, qs, qo);
+        key = (unsigned long long)__double_as_longlong(v);
+      }
+    }
+  }
+  // minimum over the warp's lanes of the same range (consecutive lanes: contiguous segments),
+  // one atomic per (warp, range) instead of one per candidate
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, o);
+    const int orr = __shfl_down_sync(0xffffffffu, r, o);
+    if (lane + o < 32 && orr == r && ok < key) key = ok;
+  }
+  const int prev_r = __shfl_up_sync(0xffffffffu, r, 1);
+  if (in && (lane == 0 || prev_r != r) && key < 0x7ff0000000000000ull) atomicMin(gbest + r, key);
 }
 
 // ------------------------------------------------------------------ pipeline trace
