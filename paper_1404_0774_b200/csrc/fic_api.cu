@@ -74,7 +74,7 @@ void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, c
                       unsigned char*, bool, unsigned long long*, unsigned*, unsigned long long*, cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
-                 const double*, uint2*, unsigned long long*, int, cudaStream_t);
+                 const double*, uint2*, unsigned*, int, cudaStream_t);
 void launch_winner(const uint2*, const unsigned long long*, int, unsigned long long, const double*,
                    const unsigned long long*, unsigned*, int, cudaStream_t);
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
@@ -228,7 +228,7 @@ struct Workspace {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   bool scan_timed = false;
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag, scratch, mra, mrb, recs, rcounts, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
+      diag, scratch, mra, mrb, recs, rcounts, pendc, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
   unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
   unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
@@ -370,8 +370,12 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   const int first_stride = scan_levels(g).front();  // pair mode builds the (unscaled) range operands once
   auto* list = static_cast<uint2*>(ws.list.get((size_t)ws.list_cap * sizeof(uint2)));
   auto* res = static_cast<double*>(ws.res.get((size_t)ws.list_cap * sizeof(double)));
-  auto* pend = static_cast<uint2*>(ws.pend.get((size_t)ws.list_cap * sizeof(uint2)));
   const int parts = scan_grid(g, stride, ws.sms);
+  // pending list: one segment per eval block (sized for the largest level grid, so the buffer
+  // does not move between levels)
+  // (blocks x segment <= list_cap + parts x 2048 for any parts <= kPartSlots)
+  auto* pend = static_cast<uint2*>(ws.pend.get((ws.list_cap + (size_t)kPartSlots * 2048) * sizeof(uint2)));
+  auto* pendc = static_cast<unsigned*>(ws.pendc.get((size_t)kPartSlots * 8 * sizeof(unsigned)));
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
   const bool final_level = stride == 1;  // resets the winner slots and the self-check counter too
   launch_level_ops(d_img, g, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride,
@@ -387,7 +391,7 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
     ws.scan_timed = true;
   }
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
-              b.cnt + kPendSlot, ws.sms, st);
+              pendc, ws.sms, st);
   g_launches += 5;  // level ops, scan, expand (or the pair scan's range rows), evaluation, residuals
 }
 
@@ -493,7 +497,7 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
   (void)st;  // graphs are stream-independent (captured on the workspace stream, launched on any)
   const void* ptrs[] = {d_img, d_out, d_counters, ws.upool.p, ws.qpool.p, ws.meta_i.p, ws.rmeta.p, ws.gbest.p,
                         ws.win.p, ws.ropnd.p, ws.thr.p, ws.deq.p, ws.scan_counts.p, ws.list.p, ws.res.p, ws.pend.p,
-                        ws.recs.p, ws.rcounts.p};
+                        ws.recs.p, ws.rcounts.p, ws.pendc.p};
   for (const void* q : ptrs) k.push_back((unsigned long long)(uintptr_t)q);
   k.push_back(ws.list_cap);
   for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED", "FIC_LANEBEST_MAX"}) {
@@ -631,6 +635,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
       // list + pending + residual, + the scan's mask records (40 B per two entry slots)
+      // (the pending list also carries kPartSlots x 2048 slack entries, allocated on top)
       const unsigned long long per_entry = sizeof(uint2) * 2 + sizeof(double) + 20;
       const unsigned long long limit = (ws.list.cap + ws.res.cap + ws.pend.cap + ws.recs.cap + free_b / 4) / per_entry;
       ws.list_cap = std::max(ws.list_cap, std::min(want, limit));

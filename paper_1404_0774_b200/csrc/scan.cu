@@ -1268,10 +1268,16 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
             const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
             const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
             unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab,
-            uint2* __restrict__ pend, unsigned long long* __restrict__ pend_count) {
+            uint2* __restrict__ pend, unsigned* __restrict__ pend_counts, unsigned long long seg) {
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const bool screens = !(g.flags & 2);
   const int lane = threadIdx.x & 31;
+  // pending candidates go to this block's own segment of the pending list (a shared-memory
+  // counter instead of one global counter every warp of the grid contends for)
+  __shared__ unsigned s_pend;
+  if (threadIdx.x == 0) s_pend = 0;
+  __syncthreads();
+  uint2* my_pend = pend + (unsigned long long)blockIdx.x * seg;
   const int per = gridDim.x / parts;  // blocks per partition (launch: a multiple of parts)
   const int c = blockIdx.x / per, sub = blockIdx.x % per;
   const unsigned long long n = min(counts[c], part);
@@ -1311,12 +1317,14 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
     // candidates that passed every screen: (entry, codes) to the residual pass
     const unsigned bal = __ballot_sync(0xffffffffu, pending);
     if (bal) {
-      unsigned long long b = 0;
-      if (lane == 0) b = atomicAdd(pend_count, (unsigned long long)__popc(bal));
+      unsigned b = 0;
+      if (lane == 0) b = atomicAdd(&s_pend, (unsigned)__popc(bal));
       b = __shfl_sync(0xffffffffu, b, 0);
-      if (pending) pend[b + __popc(bal & ((1u << lane) - 1u))] = make_uint2((uint32_t)i, qs | (qo << 16));
+      if (pending) my_pend[b + __popc(bal & ((1u << lane) - 1u))] = make_uint2((uint32_t)i, qs | (qo << 16));
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) pend_counts[blockIdx.x] = s_pend;
 }
 
 // Exact residuals (encoder.cpp:274-280, pixel order, each operation rounded) of the
@@ -1325,12 +1333,13 @@ template <int NN>
 __global__ void __launch_bounds__(256)
 residual_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
                 const SurvEntry* __restrict__ list, const uint2* __restrict__ pend,
-                const unsigned long long* __restrict__ pend_count, double* __restrict__ res,
+                const unsigned* __restrict__ pend_counts, unsigned long long seg, double* __restrict__ res,
                 unsigned long long* __restrict__ gbest, DeqTables tab) {
-  const unsigned long long n = *pend_count;
-  for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint2 p = pend[k];
+  // one block per eval block: its segment of the pending list
+  const unsigned n = pend_counts[blockIdx.x];
+  const uint2* my_pend = pend + (unsigned long long)blockIdx.x * seg;
+  for (unsigned k = threadIdx.x; k < n; k += blockDim.x) {
+    const uint2 p = my_pend[k];
     const SurvEntry en = list[p.x];
     const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)en.y;
     int x0, y0;
@@ -1908,24 +1917,34 @@ void launch_level_ops(const unsigned char* img, const Geometry& g, const RangeMe
   }
 }
 
+// Pending-list segment per eval block: the most entries one block can take (eval_kernel's
+// warp-strided loop over its partition).
+constexpr int kEvalPer = 8;  // eval blocks per partition
+unsigned long long eval_pend_seg(unsigned long long part) {
+  const unsigned long long stride = (unsigned long long)kEvalPer * 256;
+  return (part + stride - 1) / stride * 256;
+}
+
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
                  const RangeMeta* rmeta, const SurvEntry* list, const unsigned long long* counts, int parts,
                  unsigned long long part, double* res, unsigned long long* gbest, const double* deq, uint2* pend,
-                 unsigned long long* pend_count, int sms, cudaStream_t st) {
-  const int blocks = parts * 8;
-  const DeqTables tab{deq, deq + (1 << g.s_bits)};  // pend_count: reset by the level's range_op pass
+                 unsigned* pend_counts, int sms, cudaStream_t st) {
+  (void)sms;
+  const int blocks = parts * kEvalPer;
+  const unsigned long long seg = eval_pend_seg(part);
+  const DeqTables tab{deq, deq + (1 << g.s_bits)};
   if (g.N == 4) {
     eval_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
-                                           pend, pend_count);
-    residual_kernel<4><<<sms * 4, 256, 0, st>>>(img, g, qpool, list, pend, pend_count, res, gbest, tab);
+                                           pend, pend_counts, seg);
+    residual_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
   } else if (g.N == 16) {
     eval_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
-                                            pend, pend_count);
-    residual_kernel<16><<<sms * 4, 256, 0, st>>>(img, g, qpool, list, pend, pend_count, res, gbest, tab);
+                                            pend, pend_counts, seg);
+    residual_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
   } else {
     eval_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
-                                            pend, pend_count);
-    residual_kernel<64><<<sms * 4, 256, 0, st>>>(img, g, qpool, list, pend, pend_count, res, gbest, tab);
+                                            pend, pend_counts, seg);
+    residual_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
   }
 }
 
