@@ -20,13 +20,15 @@
 //    operands, fp32 accumulation): then R >= R* > bar, so it cannot be the minimum.  The
 //    test needs only the range's own threshold: per accumulator column it is one 3-input
 //    |max| (FMNMX3) per two columns.
-//  * Survivors (range, isometry, domain) go to a global list; eval_kernel recomputes the
-//    exact integer correlation and runs the reference's fp64 arithmetic operation by
-//    operation, lowering the range's bar (atomicMin on the IEEE bits).  The scan runs as
-//    sparse levels (every 64th / 8th tile) and then in full, each level pruning with the
-//    bar the previous ones achieved.  Every candidate whose residual equals the final bar
-//    is in the full level's list; winner_kernel takes the smallest (domain, isometry)
-//    among them and record_kernel re-evaluates it into the RangeMapping record.
+//  * Survivors (range, isometry, domain) go to a global list (full level: 40-byte mask
+//    records expanded by expand_kernel; sparse levels: one selected entry per warp and tile
+//    or per lane and segment); eval_kernel recomputes the exact integer correlation and runs
+//    the reference's fp64 arithmetic operation by operation, lowering the range's bar
+//    (atomicMin on the IEEE bits).  The scan runs as sparse levels (every s-th tile, see
+//    scan_levels in fic_api.cu) and then in full, each level pruning with the bar the
+//    previous ones achieved.  Every candidate whose residual equals the final bar is in the
+//    full level's list; winner_kernel takes the smallest (domain, isometry) among them and
+//    record_kernel re-evaluates it into the RangeMapping record.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -817,18 +819,17 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
                fmaxf(fabsf(f[6]), fabsf(f[7])));
 }
 
-// Persistent scan over the segments of ScanLevel (see there); 10 warps:
+// Persistent scan over the segments of ScanLevel (see there); 18 warps:
 //   warp 0        lane 0: bulk-copy producer, 128-domain pool tiles (contiguous 128*K*2 bytes) ->
 //                 smem ring; lane 1: range-operand loader, the segment's 256 x K operand (built
-//                 once per encode by range_op_kernel) -> one of two smem buffers
-//   warp 1        TMEM allocation; lane 0: MMA issuer, K/16 x tcgen05.mma M=128 (domains) x
-//                 N=256 (32 ranges x 8 isometries) x K=16 per tile into one of two 256-column
-//                 TMEM accumulators
+//                 per level by range_op_kernel) -> one of two smem buffers
+//   warp 1        TMEM allocation; MMA issuer (the whole warp runs the loop, an elected lane
+//                 issues): K/16 x tcgen05.mma M=128 (domains) x N=256 (32 ranges x 8
+//                 isometries) x K=16 per tile into one of two 256-column TMEM accumulators
 //   warps 2-17    epilogue: 16 warps (lane quarter x column part); for every tile a thread owns
 //                 one domain (TMEM lane) and kEpiRanges ranges x 8 isometries (kEpiCols columns,
 //                 scaled so the pruning test is |X~/T_r| > 1 for every column), tests each
-//                 range's 8-isometry |max| against 1 and appends the rare columns above it to
-//                 the survivor list
+//                 range's 8-isometry |max| against 1 and records the columns above it (MODE)
 // MODE: 0 full level, 1 full level with the whole-tile vote (lv.coarse), 2 sparse level with
 // the per-range test before the selection (lv.select == 1), 3 sparse level selecting from the
 // packed maxima of every range (lv.select == 2: most ranges hit in most tiles), 4 sparse level
@@ -1510,7 +1511,7 @@ __device__ __forceinline__ uint32_t mask_above(const uint32_t* v, float T) {
   return m;
 }
 
-// Cluster of 2 CTAs per pair; 10 warps per CTA:
+// Cluster of 2 CTAs per pair (FIC_SCAN=pair); 10 warps per CTA:
 //   warp 0        lane 0: producer of this CTA's half (112 domains) of every pool tile
 //   warp 1        TMEM allocation (cta_group::2); lane 0: MMA issuer in the even CTA, relay of
 //                 the odd CTA's "tile landed" to the even CTA's barrier in the odd one
