@@ -290,14 +290,25 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
   for (int k = 0; k < kPer; ++k) zs[row0 + k * kRowStep][lane_c] = zv[k];
   __syncthreads();
   double sq = 0.0;
+  // kWhole: the isometry is affine in (row, col), so the thread's z offsets form an
+  // arithmetic sequence over its rows: one base and one stride instead of a per-pixel switch
+  int zoff0 = 0, zstep = 0;
+  if (kWhole) {
+    int r00, c00, r10, c10, r01, c01;
+    symmetry_source(B.sym, a0 + row0, c0 + lane_c, kn, r00, c00);
+    symmetry_source(B.sym, a0 + row0 + 1, c0 + lane_c, kn, r10, c10);
+    (void)r01;
+    (void)c01;
+    zoff0 = (r00 - B.sr0) * (kTile + 1) + (c00 - B.sc0);
+    zstep = kRowStep * ((r10 - r00) * (kTile + 1) + (c10 - c00));
+  }
+  const double* zflat = &zs[0][0];
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int orow = row0 + k * kRowStep, ocol = lane_c;
     double z, s, o;
     if (kWhole) {
-      int sr, sc;
-      symmetry_source(B.sym, a0 + orow, c0 + ocol, kn, sr, sc);
-      z = zs[sr - B.sr0][sc - B.sc0];
+      z = zflat[zoff0 + k * zstep];
       s = B.s;
       o = B.o;
     } else {
