@@ -69,6 +69,7 @@ int scan_trace_copy(long long*, int);
 int scan_padded_ranges(const Geometry&);
 bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
+bool scan_use_f16acc(const Geometry&, int stride, int sms);
 size_t range_op_bytes(const Geometry&);
 void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, const unsigned long long*, float*,
                       unsigned char*, bool, unsigned long long*, unsigned*, unsigned long long*, cudaStream_t);
@@ -378,14 +379,17 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   auto* pendc = static_cast<unsigned*>(ws.pendc.get((size_t)kPartSlots * 8 * sizeof(unsigned)));
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
   const bool final_level = stride == 1;  // resets the winner slots and the self-check counter too
-  launch_level_ops(d_img, g, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride,
+  // the full level of a large pool accumulates in fp16 (flags & 256: its thresholds and its scan)
+  Geometry gl = g;
+  gl.flags = scan_use_f16acc(g, stride, ws.sms) ? (g.flags | 256) : (g.flags & ~256);
+  launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride,
                    b.cnt + kPendSlot, final_level ? b.win : nullptr, final_level ? b.cnt + kSelfcheckSlot : nullptr,
                    st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   void* recs = ws.recs.get(scan_rec_bytes(ws.list_cap, parts));
   auto* rcnt = static_cast<unsigned long long*>(ws.rcounts.get(kPartSlots * sizeof(unsigned long long)));
-  CK(launch_scan(d_img, g, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, recs, rcnt, st));
+  CK(launch_scan(d_img, gl, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, recs, rcnt, st));
   if (time_scan) {
     CK(cudaEventRecord(ws.ev3, st));
     ws.scan_timed = true;
@@ -500,7 +504,8 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
                         ws.recs.p, ws.rcounts.p, ws.pendc.p};
   for (const void* q : ptrs) k.push_back((unsigned long long)(uintptr_t)q);
   k.push_back(ws.list_cap);
-  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED", "FIC_LANEBEST_MAX"}) {
+  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED", "FIC_LANEBEST_MAX",
+                           "FIC_F16ACC"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;

@@ -193,12 +193,21 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
 // |X~| <= T  =>  R* >= bar + delta  (see the header).  err covers the fp16 rounding of both
 // operands (relative 2^-11 each, |sum u b| <= |u| |b| = sqrt(N * ssb)), the fp32
 // accumulation of K products (2^-21 relative each, generous) and fp16 subnormals.
-__device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, int K) {
+// f16acc (the full level with an fp16 accumulator, flags & 256): each of the K/16 MMAs rounds
+// the running sum to fp16 (probed: tools/f16acc_probe.cu); every partial sum is bounded by
+// sum |u_i b_i| <= |u| |b|, so the K/16 roundings add at most (K/16) 2^-10 |u| |b| (2^-10: one
+// ulp, covers round-toward-zero too).  No scaled operand (fp16) and no fp16 partial sum may
+// overflow (an inf times a zero, or meeting a -inf, gives a NaN that fails the test): a range
+// whose scaled bound |u| |b| / T (>= every |b_i - mean| / T) exceeds 60000 gets no bar.
+__device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, int K, bool f16acc = false) {
   const double t = (ssb - bar) - 1e-6 * (1.0 + bar);
   if (!(t > 0.0)) return -1.f;  // no usable bar (also bar == +inf): everything survives
   const double sqrtT = sqrt((double)N * t) * (1.0 - 1e-6);
-  const double err = (9.765625e-4 * 1.0005 + (double)K * 4.76837158203125e-7) * 1.05 * sqrt((double)N * ssb) + 0.01;
+  const double ub = sqrt((double)N * ssb);
+  double err = (9.765625e-4 * 1.0005 + (double)K * 4.76837158203125e-7) * 1.05 * ub + 0.01;
+  if (f16acc) err += (double)(K / 16) * 9.765625e-4 * 1.05 * ub;
   const double T = sqrtT - err;
+  if (T * 60000.0 < ub * 1.01) return -1.f;
   return T > 0.0 ? __double2float_rd(T) : -1.f;
 }
 
@@ -605,6 +614,9 @@ __host__ __device__ inline Segment seg_at(const ScanLevel& lv, int c, int G, int
 // (1 + 1e-6) / T >= 1/T even after rounding, so |X~ * scale| <= 1 implies |X~| <= T.
 __device__ __forceinline__ float range_scale(float T) { return T > 1e-3f && T < 1e29f ? (1.0f + 1e-6f) / T : 0.f; }
 __device__ __forceinline__ bool range_allpass(float T) { return !(T > 1e-3f); }
+// The full level accumulates in fp16 (flags & 256, FIC_F16ACC=1): halves the epilogue's TMEM
+// read (two columns per register, tcgen05.ld .pack::16b) and its |max| test (half2 VHMNMX).
+__host__ __device__ __forceinline__ bool scan_f16acc(const Geometry& g) { return (g.flags & 256) != 0; }
 
 // Range operand of m-tile `mt` into `sR` (threads [tid, tid + nthreads)): row
 // rl * 8 + s holds the centred range rl permuted by isometry s's inverse and scaled,
@@ -647,11 +659,14 @@ __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict_
 // padded to whole m-tiles.  Invalid and shadow ranges get +1e30 (never survive), flags & 1
 // (exhaustive debug mode) -1 (everything survives).
 __device__ __forceinline__ float range_threshold(const Geometry& g, const RangeMeta* __restrict__ rmeta,
-                                                 const unsigned long long* __restrict__ gbest, int r) {
+                                                 const unsigned long long* __restrict__ gbest, int r,
+                                                 bool f16acc = false) {
   float t = 1e30f;
   if (r < g.R) {
     const RangeMeta rm = rmeta[r];
-    if (!rm.shadow) t = (g.flags & 1) ? -1.f : scan_threshold((double)rm.var / (double)g.N, load_bar(gbest, r), g.N, g.K);
+    if (!rm.shadow)
+      t = (g.flags & 1) ? -1.f
+                        : scan_threshold((double)rm.var / (double)g.N, load_bar(gbest, r), g.N, g.K, f16acc);
   }
   return t;
 }
@@ -677,7 +692,7 @@ range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMe
   __shared__ float s_thr[kScanRanges];
   if (threadIdx.x < kScanRanges) {
     const int r = blockIdx.x * kScanRanges + threadIdx.x;
-    const float t = range_threshold(g, rmeta, gbest, r);
+    const float t = range_threshold(g, rmeta, gbest, r, win != nullptr && scan_f16acc(g));  // full level
     s_thr[threadIdx.x] = t;
     if (blockIdx.y == 0) {
       thr[r] = t;
@@ -834,8 +849,8 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 // the per-range test before the selection (lv.select == 1), 3 sparse level selecting from the
 // packed maxima of every range (lv.select == 2: most ranges hit in most tiles), 4 sparse level
 // keeping each lane's best per range over the whole segment (lv.select == 3: short levels of
-// small pools, one segment per m-tile).  One instantiation per mode keeps each epilogue's
-// registers to its own path.
+// small pools, one segment per m-tile); 5 and 6: modes 0 and 1 with an fp16 accumulator
+// (scan_f16acc).  One instantiation per mode keeps each epilogue's registers to its own path.
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
@@ -845,6 +860,8 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             SurvEntry* __restrict__ list_all, unsigned long long cap,
             unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(1024) unsigned char smem[];
+  constexpr bool F16 = MODE >= 5;            // fp16 accumulator (full level only)
+  constexpr int MB = F16 ? MODE - 5 : MODE;  // the epilogue mode proper
   const ScanSmem L = scan_smem_layout(g.K);
   const int K = g.K;
   unsigned char* sR = smem + L.r_off;
@@ -921,7 +938,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     // The whole warp runs the loop (all its values warp-uniform); one elected lane issues the
     // MMAs and commits.  The issuing thread is on the scan's critical path.
     {
-      const uint32_t idesc = ptx::idesc_f16_f32(128, kScanRows);
+      const uint32_t idesc = F16 ? ptx::idesc_f16_f16(128, kScanRows) : ptx::idesc_f16_f32(128, kScanRows);
       const bool do_mma = !(g.flags & 16);  // debug: flags & 16 skips the MMAs
       // descriptors: the start address field (bits 0-13, 16-byte units) advances by 16 per
       // K=16 step (256 bytes) and by p_bytes/16 per ring stage; everything else is constant
@@ -971,7 +988,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
     WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u};
-    constexpr bool sel = MODE >= 2;
+    constexpr bool sel = MB >= 2;
     SurvEntry* elist = list_all + (unsigned long long)blockIdx.x * cap;  // sparse levels: direct entries
     const uint32_t ecap = (uint32_t)cap;
     uint32_t ebase = 0, eleft = 0;
@@ -991,9 +1008,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       const uint32_t rowbase = (uint32_t)r0 * 8u;
       // MODE 4: each lane's running best column per range over the segment's tiles, packed as
       // (|x| truncated to 7 mantissa bits | 7 - isometry | level tile index), flushed below
-      uint32_t lbest[MODE == 4 ? kEpiRanges : 1];
+      uint32_t lbest[MB == 4 ? kEpiRanges : 1];
 #pragma unroll
-      for (int k = 0; k < (MODE == 4 ? kEpiRanges : 1); ++k) lbest[k] = 0u;
+      for (int k = 0; k < (MB == 4 ? kEpiRanges : 1); ++k) lbest[k] = 0u;
       for (int j = S.j0; j < S.j1; ++j, ++i) {
         const int buf = i & 1;
         if (lane == 0 && i > 0) trace_stamp(g, i - 1, 19 + e);  // done with the previous tile
@@ -1006,10 +1023,14 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           continue;
         }
         const uint32_t ta = tcol + buf * kScanRows;
-        uint32_t v[kEpiCols];
+        uint32_t v[kEpiCols];  // F16: the first kEpiCols / 2
         __syncwarp();
+        if constexpr (F16) {
+          ptx::tmem_ld_32x32b_x64_pack16(ta, v);  // register j: columns 2j, 2j + 1
+        } else {
 #pragma unroll
-        for (int c = 0; c < kEpiCols; c += 32) ptx::tmem_ld_32x32b_x32(ta + c, v + c);
+          for (int c = 0; c < kEpiCols; c += 32) ptx::tmem_ld_32x32b_x32(ta + c, v + c);
+        }
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
@@ -1018,7 +1039,49 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           trace_stamp(g, i, 3 + e);
         }
         if (g.flags & 8) continue;                          // debug: skip the test
-        if constexpr (MODE == 4) {
+        if constexpr (F16) {
+          // fp16 pairs: range k's 8 isometry columns are registers 4k .. 4k + 3; the |max| test
+          // runs on half2 (3-input VHMNMX with |.| modifiers: four columns per instruction).
+          // |x| > 1 on the bit patterns: (h & 0x7FFF) > 0x3C00 (no inf / NaN: scan_threshold)
+          const __half2* h = reinterpret_cast<const __half2*>(v);
+          if (MB == 1 && !allpass) {
+            __half2 m0 = __habs2(h[0]), m1 = __habs2(h[1]);
+#pragma unroll
+            for (int c = 2; c < kEpiCols / 2; c += 4) {
+              m0 = __hmax2(m0, __hmax2(__habs2(h[c]), __habs2(h[c + 1])));
+              m1 = __hmax2(m1, __hmax2(__habs2(h[c + 2]), __habs2(h[c + 3])));
+            }
+            const __half2 mx = __hmax2(m0, m1);
+            const uint32_t mm = *reinterpret_cast<const uint32_t*>(&mx);
+            if (!__any_sync(0xffffffffu, (mm & 0xFFFFu) > 0x3C00u || (mm >> 16) > 0x3C00u)) continue;
+          }
+          uint32_t gmask = allpass;
+#pragma unroll
+          for (int k = 0; k < kEpiRanges; ++k) {
+            const __half2 mx = __hmax2(__hmax2(__habs2(h[4 * k]), __habs2(h[4 * k + 1])),
+                                       __hmax2(__habs2(h[4 * k + 2]), __habs2(h[4 * k + 3])));
+            const uint32_t mm = *reinterpret_cast<const uint32_t*>(&mx);
+            gmask |= (uint32_t)((mm & 0xFFFFu) > 0x3C00u || (mm >> 16) > 0x3C00u) << k;
+          }
+          const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+          if (groups) {
+#pragma unroll
+            for (int k = 0; k < kEpiRanges; ++k) {
+              if ((groups >> k) & 1u) {
+                uint32_t bits = 0;
+                if ((allpass >> k) & 1u) {
+                  bits = 0xFFu;
+                } else {
+#pragma unroll
+                  for (int c = 0; c < 8; ++c)
+                    bits |= (uint32_t)(((v[4 * k + (c >> 1)] >> (16 * (c & 1))) & 0x7FFFu) > 0x3C00u) << c;
+                }
+                app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
+              }
+            }
+          }
+          continue;
+        } else if constexpr (MB == 4) {
           // small pools, short sparse level: per lane and range keep the best column seen in the
           // segment (one per tile slot, like the warp's best per tile but without any cross-lane
           // work per tile); the threshold test is applied once, when the segment is flushed
@@ -1046,7 +1109,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           uint32_t gmask = allpass;
 #pragma unroll
           for (int k = 0; k < kEpiRanges; ++k) {
-            if constexpr (MODE == 3) {
+            if constexpr (MB == 3) {
               float m = 0.f;
 #pragma unroll
               for (int c = 0; c < 8; ++c)
@@ -1066,7 +1129,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           for (int k = 0; k < kEpiRanges; ++k) {
             if ((groups >> k) & 1u) {
               float m = 0.f;
-              if constexpr (MODE == 3) {
+              if constexpr (MB == 3) {
                 m = __uint_as_float(pk[k]);
               } else {
 #pragma unroll
@@ -1091,7 +1154,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           }
           continue;
         }
-        if (MODE == 1 && !allpass) {
+        if (MB == 1 && !allpass) {
           // large pools, hits in ~2% of warp-tiles: one |max| over all 64 columns (32 FMNMX3)
           // and a warp vote first; the per-range breakdown only for the rare tiles with a hit
           // four independent FMNMX3 chains (8 deep instead of 16: the test's latency, not its
@@ -1136,7 +1199,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           }
         }
       }
-      if constexpr (MODE == 4) {  // flush the segment's per-lane bests: one entry per lane and range
+      if constexpr (MB == 4) {  // flush the segment's per-lane bests: one entry per lane and range
 #pragma unroll
         for (int k = 0; k < kEpiRanges; ++k) {
           const uint32_t b = lbest[k];
@@ -1870,8 +1933,12 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   }
   const ScanLevel lv = make_level(g, stride, grid);
   const ScanSmem L = scan_smem_layout(g.K);
-  const int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
-  auto kern = mode == 4 ? scan_kernel<4>
+  int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
+  // fp16 accumulator: the full level only (its thresholds carry the fp16 bound, range_op_kernel)
+  if (scan_f16acc(g) && stride == 1 && mode <= 1) mode += 5;
+  auto kern = mode == 6   ? scan_kernel<6>
+              : mode == 5 ? scan_kernel<5>
+              : mode == 4 ? scan_kernel<4>
               : mode == 3 ? scan_kernel<3>
               : mode == 2 ? scan_kernel<2>
               : mode == 1 ? scan_kernel<1>
@@ -1885,6 +1952,18 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   if (e != cudaSuccess) return e;
   expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
   return cudaGetLastError();
+}
+
+// Full level with an fp16 accumulator: large pools (the whole-tile vote mode, where the
+// epilogue's TMEM read and |max| test pace the MMAs: cfg4 scan 56.5 -> 51.6 ms); small pools
+// keep fp32 (the wider fp16 error bound adds survivors that cost more than the halved read).
+// FIC_F16ACC=1 / 0 forces it on / off for the full level.
+bool scan_use_f16acc(const Geometry& g, int stride, int sms) {
+  if (stride != 1 || scan_pair_mode()) return false;
+  const char* e = std::getenv("FIC_F16ACC");
+  if (e) return e[0] == '1';
+  const ScanLevel lv = make_level(g, 1, scan_grid(g, 1, sms));
+  return lv.select == 0 && lv.coarse;
 }
 
 int scan_padded_ranges(const Geometry& g) { return ((g.R + kScanRanges - 1) / kScanRanges) * kScanRanges; }

@@ -315,3 +315,23 @@ def test_coarse_vote_output_neutral(oracle, coarse):
             enc = fic.encode(img, fic.CodecParams(**pv))
         assert_same(enc.mappings, want, f"coarse={coarse} {pv}")
         assert enc.stats == st
+
+
+@pytest.mark.parametrize("coarse", ["0", "1"])
+def test_f16_accumulator_output_neutral(oracle, coarse):
+    """The full level with an fp16 accumulator (scan modes 5/6, default for large pools) forced
+    on small images, with and without the whole-tile vote: identical codes and residual bits.
+    The binary 0/255 image drives the operand/partial-sum overflow guard (ranges with a tiny
+    bar relative to their norm get no bar)."""
+    rng = np.random.default_rng(1404)
+    binary = (rng.random((64, 64)) > 0.5).astype(np.uint8) * 255
+    binary[:32, :32] = 128  # flat block: zero-variance ranges next to maximal-contrast ones
+    cases = [(oracle.noise_image(64, 9), dict(n=4, step=2)), (oracle.smooth_image(64, 5), dict(n=8, step=2)),
+             (images.ct_slice(256, 1404002, 0.3), dict(n=8, step=4)), (binary, dict(n=4, step=2)),
+             (binary, dict(n=8, step=2))]
+    for img, pv in cases:
+        want, st = oracle.encode(img, pv)
+        with env(FIC_F16ACC="1", FIC_COARSE=coarse):
+            enc = fic.encode(img, fic.CodecParams(**pv))
+        assert_same(enc.mappings, want, f"f16acc coarse={coarse} {pv}")
+        assert enc.stats == st
