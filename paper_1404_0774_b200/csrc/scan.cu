@@ -194,9 +194,9 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
 // operands (relative 2^-11 each, |sum u b| <= |u| |b| = sqrt(N * ssb)), the fp32
 // accumulation of K products (2^-21 relative each, generous) and fp16 subnormals.
 // f16acc (the full level with an fp16 accumulator, flags & 256): each of the K/16 MMAs rounds
-// the running sum to fp16 (probed: tools/f16acc_probe.cu); every partial sum is bounded by
-// sum |u_i b_i| <= |u| |b|, so the K/16 roundings add at most (K/16) 2^-10 |u| |b| (2^-10: one
-// ulp, covers round-toward-zero too).  No scaled operand (fp16) and no fp16 partial sum may
+// the running sum to fp16, to nearest even (pinned on the B200 by tools/f16acc_probe.cu: ties
+// and quarter points, inside a K=16 step and across steps); every partial sum is bounded by
+// sum |u_i b_i| <= |u| |b|, so the K/16 roundings add at most (K/16) 2^-11 |u| |b|.  No scaled operand (fp16) and no fp16 partial sum may
 // overflow (an inf times a zero, or meeting a -inf, gives a NaN that fails the test): a range
 // whose scaled bound |u| |b| / T (>= every |b_i - mean| / T) exceeds 60000 gets no bar.
 __device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, int K, bool f16acc = false) {
@@ -205,7 +205,7 @@ __device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, i
   const double sqrtT = sqrt((double)N * t) * (1.0 - 1e-6);
   const double ub = sqrt((double)N * ssb);
   double err = (9.765625e-4 * 1.0005 + (double)K * 4.76837158203125e-7) * 1.05 * ub + 0.01;
-  if (f16acc) err += (double)(K / 16) * 9.765625e-4 * 1.05 * ub;
+  if (f16acc) err += (double)(K / 16) * 4.8828125e-4 * 1.05 * ub;
   const double T = sqrtT - err;
   if (T * 60000.0 < ub * 1.01) return -1.f;
   return T > 0.0 ? __double2float_rd(T) : -1.f;

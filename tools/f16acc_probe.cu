@@ -170,6 +170,37 @@ int main() {
   std::printf("fp32 D: max |D - exact| / sum|ab| = %.3e\n", e32);
   std::printf("fp16 D, one element per column: max err / sum|ab| = %.3e, / |exact| = %.3e\n", e16lo, e16lo_rel);
   std::printf("fp16 D, two packed per column:  max err / sum|ab| = %.3e, / |exact| = %.3e\n", e16pk, e16pk_rel);
+  // rounding mode of the fp16 D: row m adds x_m = (m - 64) * 2^-13 to 1.0, either inside the
+  // first K=16 step (k = 1) or as the second step (k = 16, the running sum 1.0 read back first);
+  // predictions for round-to-nearest-even, toward zero and truncation-away
+  for (int k2 : {1, 16}) {
+    for (auto& h : hA) h = __float2half(0.f);
+    for (auto& h : hB) h = __float2half(0.f);
+    for (int m = 0; m < M; ++m) {
+      hA[core_off(m, 0)] = __float2half(1.f);
+      hA[core_off(m, k2)] = __float2half((float)(m - 64) * 0x1p-13f);
+    }
+    hB[core_off(0, 0)] = __float2half(1.f);
+    hB[core_off(0, k2)] = __float2half(1.f);
+    cudaMemcpy(dA, hA.data(), M * K * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, hB.data(), N * K * 2, cudaMemcpyHostToDevice);
+    probe<<<1, 128, smem>>>(dA, dB, d32, d16, d16p);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h16.data(), d16, M * N * 4, cudaMemcpyDeviceToHost);
+    int rn = 0, rz = 0, other = 0;
+    for (int m = 0; m < M; ++m) {
+      const double ex = 1.0 + (double)(m - 64) * 0x1p-13;
+      __half_raw hr;
+      hr.x = (unsigned short)(h16[m * N] & 0xFFFF);
+      const double got = __half2float(__half(hr));
+      const double rne = __half2float(__float2half_rn((float)ex));
+      const double rtz = __half2float(__float2half_rz((float)ex));
+      rn += got == rne;
+      rz += got == rtz;
+      other += got != rne && got != rtz;
+    }
+    std::printf("rounding probe (second term at k=%d): matches RNE %d, RZ %d, neither %d of %d\n", k2, rn, rz, other, M);
+  }
   std::printf("reference: 2^-11 = %.3e, 4 * 2^-11 = %.3e, 64 * 2^-11 = %.3e\n", std::ldexp(1.0, -11),
               4 * std::ldexp(1.0, -11), 64 * std::ldexp(1.0, -11));
   return 0;

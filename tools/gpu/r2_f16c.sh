@@ -1,0 +1,9 @@
+# fp16 accumulator bound at half an ulp per step: encode parity (forced on everywhere) + cfg4/cfg2 A/B
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_encode.py -x -q > gpurun_out/pytest_enc.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_enc.log
+timeout 900 env FIC_F16ACC=1 python -m pytest tests/test_gpu_encode.py -x -q > gpurun_out/pytest_f16.log 2>&1; echo "pytest f16 rc=$?"; tail -1 gpurun_out/pytest_f16.log
+run() { timeout 900 env $4 python bench.py --config $1 --no-cpu-baseline --steps $2 --warmup 3 $3 > gpurun_out/bench_$1_$5.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/bench_$1_$5.json').read().strip().splitlines()[-1]); print('$1 $4', round(d['ms_per_step'],4), 'e2e', round(d['e2e']['encode_ms_per_image'],4), 'scan', round(d['roofline']['kernel_ms'],4), 'frac', round(d['roofline']['frac'],3), d['survivors_per_level'], d['clocks'])"; }
+run cfg4 3 "" X=1 def; run cfg4 3 "" FIC_F16ACC=0 f32
+run cfg2 20 "" FIC_F16ACC=1 f16; run cfg2 20 "" X=1 def
+run cfg3 10 "" FIC_F16ACC=1 f16; run cfg3 10 "" X=1 def
