@@ -309,8 +309,10 @@ std::vector<int> scan_levels(const Geometry& g) {
   const int tiles = scan_tiles(g);
   const char* pp = std::getenv("FIC_PREPASS");
   const bool prepass = !(pp && std::strcmp(pp, "0") == 0);
-  // ratio 8 between levels (measured: a final ratio-4 level costs cfg4 more scan work than it
-  // saves in survivors; cfg2 is indifferent)
+  // large pools: ratio 8 between levels, the last sparse level at stride 16 (cfg4 with the fp16
+  // full level: {4096, 512, 64, 16} 65.1-65.4 ms vs {..., 8} 67.5-68.0 alternated on one box — the stride-8 level's 10.8 ms of
+  // hit-heavy selection cost more than its bar saves at the full level; 3 or 5 levels are
+  // no better: 68.3 / 64.3 ms)
   const char* sched = std::getenv("FIC_LEVELS");  // optional override, e.g. "64,8"
   if (sched) {
     for (const char* p = sched; *p;) {
@@ -320,7 +322,7 @@ std::vector<int> scan_levels(const Geometry& g) {
       if (*p == ',') ++p;
     }
   } else if (prepass && tiles > 1024) {
-    for (int s : {4096, 512, 64, 8})
+    for (int s : {4096, 512, 64, 16})
       if (tiles > s) lv.push_back(s);
   } else if (prepass) {
     // small pools (cfg2: 123 tiles, cfg3: 501): last sparse level at stride 4, earlier ones x8
