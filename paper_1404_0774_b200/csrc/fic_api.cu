@@ -310,9 +310,9 @@ std::vector<int> scan_levels(const Geometry& g) {
   const char* pp = std::getenv("FIC_PREPASS");
   const bool prepass = !(pp && std::strcmp(pp, "0") == 0);
   // large pools: ratio 8 between levels, the last sparse level at stride 16 (cfg4 with the fp16
-  // full level: {4096, 512, 64, 16} 65.1-65.4 ms vs {..., 8} 67.5-68.0 alternated on one box — the stride-8 level's 10.8 ms of
-  // hit-heavy selection cost more than its bar saves at the full level; 3 or 5 levels are
-  // no better: 68.3 / 64.3 ms)
+  // full level: {4096, 512, 64, 16} 65.1-65.4 ms vs {..., 8} 67.5-68.0, alternated on one box:
+  // the stride-8 level's 10.8 ms of hit-heavy selection cost more than its bar saves at the
+  // full level; 3 or 5 levels are no better: 68.3 / 64.3 ms)
   const char* sched = std::getenv("FIC_LEVELS");  // optional override, e.g. "64,8"
   if (sched) {
     for (const char* p = sched; *p;) {
