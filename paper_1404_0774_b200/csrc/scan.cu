@@ -849,8 +849,8 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 // the per-range test before the selection (lv.select == 1), 3 sparse level selecting from the
 // packed maxima of every range (lv.select == 2: most ranges hit in most tiles), 4 sparse level
 // keeping each lane's best per range over the whole segment (lv.select == 3: short levels of
-// small pools, one segment per m-tile); 5 and 6: modes 0 and 1 with an fp16 accumulator
-// (scan_f16acc).  One instantiation per mode keeps each epilogue's registers to its own path.
+// small pools, one segment per m-tile); 5, 6 and 7: modes 0, 1 and 2 with an fp16
+// accumulator (full level: scan_f16acc; sparse level: scan_f16sel).  One instantiation per mode keeps each epilogue's registers to its own path.
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
@@ -1064,6 +1064,35 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             gmask |= (uint32_t)((mm & 0xFFFFu) > 0x3C00u || (mm >> 16) > 0x3C00u) << k;
           }
           const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+          if constexpr (MB == 2) {
+            // sparse level (it only lowers the bar, so fp16 accuracy is enough): per hit range the
+            // warp's best column, key = |h| << 3 | (7 - isometry) (exact magnitude order; ties
+            // to the lower isometry, then the lower lane)
+#pragma unroll
+            for (int k = 0; k < kEpiRanges; ++k) {
+              if ((groups >> k) & 1u) {
+                uint32_t m = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                  m = max(m, (((v[4 * k + (c >> 1)] >> (16 * (c & 1))) & 0x7FFFu) << 3) | (uint32_t)(7 - c));
+                const uint32_t key = (m > ((0x3C00u << 3) | 7u) || ((allpass >> k) & 1u)) ? m : 0u;
+                const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
+                if (wmax == 0u) continue;
+                const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
+                if (eleft == 0) {  // warp-level chunk of entry slots
+                  uint32_t nb = 0;
+                  if (lane == 0) nb = atomicAdd(ecount, 32u);
+                  ebase = __shfl_sync(0xffffffffu, nb, 0);
+                  eleft = 32;
+                }
+                if ((uint32_t)lane == win && ebase < ecap)
+                  elist[ebase] = make_uint2(rowbase + 8u * (uint32_t)k + (7u - (wmax & 7u)), d);
+                ++ebase;
+                --eleft;
+              }
+            }
+            continue;
+          }
           if (groups) {
 #pragma unroll
             for (int k = 0; k < kEpiRanges; ++k) {
@@ -1886,6 +1915,8 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
     lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0)
                     ? (n_tiles <= 1024 ? (n_lvl <= lane_best_max ? 3 : 2) : 1)
                     : 0;
+    if (stride > 1 && e && e[0] >= '1' && e[0] <= '3' && (e[0] != '3' || n_lvl < 8192))
+      lv.select = e[0] - '0';  // "1" / "2" / "3": force a selection mode (A/B)
   }
   {
     const char* e = std::getenv("FIC_COARSE");  // "0" / "1": force the whole-tile vote off / on (A/B)
@@ -1917,6 +1948,15 @@ size_t scan_rec_bytes(unsigned long long list_cap, int parts) {
   return (size_t)scan_rec_part(list_cap / (unsigned long long)parts) * parts * sizeof(MaskRec);
 }
 
+// Hit-first sparse levels (large pools) with an fp16 accumulator (FIC_F16SEL=1, scan mode 7): a
+// sparse level only lowers the bar, so neither its test nor its selection needs a bound.  Off
+// by default: cfg4 measured no gain (stride-16 level 5.36 ms either way; that epilogue is bound
+// by the per-hit-range warp reductions, not by the TMEM read or the |max| test).
+bool scan_f16sel() {
+  const char* e = std::getenv("FIC_F16SEL");
+  return e && e[0] == '1';
+}
+
 cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride, int sms, const __half* upool,
                         const RangeMeta* rmeta, const unsigned char* ropnd, const float* thr, SurvEntry* list,
                         unsigned long long* counts, unsigned long long part, void* recs, unsigned long long* rcounts,
@@ -1936,7 +1976,9 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
   // fp16 accumulator: the full level only (its thresholds carry the fp16 bound, range_op_kernel)
   if (scan_f16acc(g) && stride == 1 && mode <= 1) mode += 5;
-  auto kern = mode == 6   ? scan_kernel<6>
+  if (mode == 2 && scan_f16sel()) mode = 7;
+  auto kern = mode == 7   ? scan_kernel<7>
+              : mode == 6 ? scan_kernel<6>
               : mode == 5 ? scan_kernel<5>
               : mode == 4 ? scan_kernel<4>
               : mode == 3 ? scan_kernel<3>

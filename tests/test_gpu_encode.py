@@ -264,17 +264,19 @@ def test_pruning_is_output_neutral(oracle, mode):
 
 
 def test_scan_modes_cfg4_sample(oracle):
-    """cfg4 (2048x2048, n=8, step 2): both tcgen05 scans agree with the reference on sampled rows."""
+    """cfg4 (2048x2048, n=8, step 2): both tcgen05 scans agree with the reference on sampled rows,
+    the default one with and without the fp16 full level (scan modes 6 vs 1) and with fp16
+    hit-first sparse levels (mode 7 instead of 2)."""
     img = images.xray(2048, 1404004)
     pv = dict(n=8, step=2)
     rows = [0, 101, 255]
     want, _ = oracle.encode_threaded(img, pv, rows=rows)
     R = 2048 // 8
-    for scan in ("1cta", "pair"):
-        with env(FIC_SCAN=scan):
+    for sw in (dict(FIC_SCAN="1cta"), dict(FIC_SCAN="pair"), dict(FIC_F16ACC="0"), dict(FIC_F16SEL="1")):
+        with env(**sw):
             enc = fic.encode(img, fic.CodecParams(**pv))
         got = np.concatenate([enc.mappings[r * R:(r + 1) * R] for r in rows])
-        assert_same(got, want, f"cfg4 rows {scan}")
+        assert_same(got, want, f"cfg4 rows {sw}")
 
 
 def test_graph_replay_new_contents(oracle):
