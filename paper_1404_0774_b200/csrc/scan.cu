@@ -1154,8 +1154,15 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             }
           }
           const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
+          if (!groups) continue;
+          // one key per range, (|x| truncated to 15 mantissa bits | 7 - isometry | 31 - lane), so
+          // one warp max yields the winning isometry AND lane; the hit ranges' maxima are
+          // independent (issued back to back), then one chunk reservation covers all entries of
+          // the tile and lane k writes range k's entry
+          uint32_t wm[kEpiRanges];
 #pragma unroll
           for (int k = 0; k < kEpiRanges; ++k) {
+            uint32_t key = 0u;
             if ((groups >> k) & 1u) {
               float m = 0.f;
               if constexpr (MB == 3) {
@@ -1165,22 +1172,35 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 for (int c = 0; c < 8; ++c)
                   m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
               }
-              const uint32_t key = (m > 1.0f || ((allpass >> k) & 1u)) ? __float_as_uint(m) : 0u;
-              const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
-              if (wmax == 0u) continue;
-              const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
-              if (eleft == 0) {  // warp-level chunk of entry slots
-                uint32_t nb = 0;
-                if (lane == 0) nb = atomicAdd(ecount, 32u);
-                ebase = __shfl_sync(0xffffffffu, nb, 0);
-                eleft = 32;
-              }
-              if ((uint32_t)lane == win && ebase < ecap)
-                elist[ebase] = make_uint2(rowbase + 8u * (uint32_t)k + (7u - (wmax & 7u)), d);
-              ++ebase;
-              --eleft;
+              const uint32_t mk = (__float_as_uint(m) & 0x7FFFFF00u) | ((__float_as_uint(m) & 7u) << 5) |
+                                  (31u - (uint32_t)lane);
+              key = (m > 1.0f || ((allpass >> k) & 1u)) ? mk : 0u;
             }
+            wm[k] = __reduce_max_sync(0xffffffffu, key);
           }
+          uint32_t hits = 0u, mine = 0u;
+#pragma unroll
+          for (int k = 0; k < kEpiRanges; ++k) {
+            hits |= (uint32_t)(wm[k] != 0u) << k;
+            if (lane == k) mine = wm[k];
+          }
+          if (!hits) continue;
+          const uint32_t nh = (uint32_t)__popc(hits);
+          if (eleft < nh) {  // pad the rest of the chunk, take a new one
+            for (uint32_t q = (uint32_t)lane; q < eleft; q += 32)
+              if (ebase + q < ecap) elist[ebase + q] = make_uint2(kSentinel, kSentinel);
+            uint32_t nb = 0;
+            if (lane == 0) nb = atomicAdd(ecount, 32u);
+            ebase = __shfl_sync(0xffffffffu, nb, 0);
+            eleft = 32;
+          }
+          if (mine != 0u) {
+            const uint32_t pos = ebase + (uint32_t)__popc(hits & ((1u << lane) - 1u));
+            const uint32_t wl = 31u - (mine & 31u), ws = 7u - ((mine >> 5) & 7u);
+            if (pos < ecap) elist[pos] = make_uint2(rowbase + 8u * (uint32_t)lane + ws, d - (uint32_t)lane + wl);
+          }
+          ebase += nh;
+          eleft -= nh;
           continue;
         }
         if (MB == 1 && !allpass) {

@@ -337,3 +337,24 @@ def test_f16_accumulator_output_neutral(oracle, coarse):
             enc = fic.encode(img, fic.CodecParams(**pv))
         assert_same(enc.mappings, want, f"f16acc coarse={coarse} {pv}")
         assert enc.stats == st
+
+
+_SELECT_WANT = {}
+
+
+@pytest.mark.parametrize("select", ["1", "2", "3"])
+def test_sparse_selection_modes_output_neutral(oracle, select):
+    """Every sparse-level selection (1 hit-first, 2 all-packed, 3 per-lane best: scan modes 2, 3,
+    4) forced: a sparse level only lowers the bar, so codes and residual bits stay the
+    reference's.  (The 256² n=4 step-2 pool, 123 tiles, is the one with a sparse level.)"""
+    cases = [(oracle.noise_image(64, 9), dict(n=4, step=2)), (oracle.smooth_image(64, 5), dict(n=8, step=2)),
+             (images.ct_slice(256, 1404002, 0.3), dict(n=8, step=4)),
+             (images.ct_slice(256, 1404003, 0.3), dict(n=4, step=2))]
+    for i, (img, pv) in enumerate(cases):
+        if i not in _SELECT_WANT:
+            _SELECT_WANT[i] = oracle.encode(img, pv)
+        want, st = _SELECT_WANT[i]
+        with env(FIC_SELECT=select):
+            enc = fic.encode(img, fic.CodecParams(**pv))
+        assert_same(enc.mappings, want, f"select={select} {pv}")
+        assert enc.stats == st
