@@ -53,8 +53,7 @@ def make_image(cfg, rank=0, world=1, slices=512):
     from paper_1404_0774_b200 import images
     if cfg == "cfg5":
         per = (slices + world - 1) // world
-        z = range(rank * per, min(slices, (rank + 1) * per))
-        return np.stack([images.ct_slice(512, 1404005 + k, k / max(slices, 1)) for k in z]), 8, 4
+        return images.volume_slices(rank * per, per, slices), 8, 4
     gen, n, step = images.CONFIGS[cfg]
     if rank == 0 or cfg not in ("cfg2", "cfg3"):
         img = gen()

@@ -80,6 +80,22 @@ typedef struct fic_stats {
   uint64_t shadow_codeblocks;
 } fic_stats;
 
+/* LinearFit (proj/include/fic/encoder.hpp:15-19). */
+typedef struct fic_linear_fit {
+  double s;
+  double o;
+  double residual;
+} fic_linear_fit;
+
+/* QuantizedFit (proj/include/fic/encoder.hpp:24-30). */
+typedef struct fic_quantized_fit {
+  uint32_t qs;
+  uint32_t qo;
+  double s;
+  double o;
+  double residual;
+} fic_quantized_fit;
+
 /* Initial raster kinds of DecodeParams (proj/include/fic/decoder.hpp:29). */
 enum { FIC_INITIAL_MID_GRAY = 0, FIC_INITIAL_BLACK = 1, FIC_INITIAL_SUPPLIED = 2 };
 
@@ -134,6 +150,23 @@ int32_t fic_encode_batch_device(const uint8_t* d_images, int32_t count, int32_t 
                                 int32_t height, const fic_params* params, fic_mapping* d_out,
                                 fic_stats* stats, void* stream);
 
+/* ---- per-candidate fit pipeline (proj/include/fic/encoder.hpp:32-45), host fp64 ----
+ * A block is `side` x `side` samples, row-major (fic::Block, proj/include/fic/transforms.hpp:13-25). */
+/* is_shadow (proj/src/encoder.cpp:60-67): *out = 1 iff N*sum(b^2) - sum(b)^2 <= eps. */
+int32_t fic_is_shadow(const double* samples, int32_t side, double eps, int32_t* out);
+/* least_squares_fit (proj/src/encoder.cpp:69-76): unconstrained fit of b ~ s*a + o.
+ * FIC_ERR_SIDE_MISMATCH when side_a != side_b. */
+int32_t fic_least_squares_fit(const double* a, int32_t side_a, const double* b, int32_t side_b,
+                              double shadow_eps, fic_linear_fit* out);
+/* least_squares_clamped (proj/src/encoder.cpp:78-88): s clamped to +-s_max, o re-fitted and
+ * clamped to +-255 (params normalised first). */
+int32_t fic_least_squares_clamped(const double* a, int32_t side_a, const double* b, int32_t side_b,
+                                  const fic_params* params, fic_linear_fit* out);
+/* least_squares (proj/src/encoder.cpp:90-102): clamped fit pushed through the quantisers,
+ * residual re-scored with the dequantised values. */
+int32_t fic_least_squares(const double* a, int32_t side_a, const double* b, int32_t side_b,
+                          const fic_params* params, fic_quantized_fit* out);
+
 /* ---- decoder (proj/include/fic/decoder.hpp:45-63) ---- */
 /* decode_step (proj/src/decoder.cpp:39-79) on fp64 rasters of (width*scale)^2 pixels. */
 int32_t fic_decode_step(const double* current, int32_t cur_width, int32_t cur_height,
@@ -179,6 +212,17 @@ int32_t fic_decode_timing(double* avg_ms, double* avg_bytes, uint64_t* calls, in
 /* Survivors (candidates passing the tensor-core bound) per scan level of the calling
  * process's last tcgen05-path encode; returns the number of levels (0 for the CUDA-core path). */
 int32_t fic_last_survivors(uint64_t* counts, int32_t max_levels);
+/* (test support) K1 read-back for n in {2, 4, 8}: builds the image's domain pool on the device
+ * and copies back, per canonical domain d < D, Sq (sum of the 2x2 group sums q), den =
+ * N*Sqq - Sq^2 (-1 for flat code blocks: (double)den <= 16*shadow_eps, encoder.cpp:223) and,
+ * if `q8` is non-NULL, the exact u16 cells per isometry q8[(d*8 + s)*N + i] = q[perm_s(i)]
+ * (encoder.cpp:205-222); `flat_count` gets the flat domains.  With probe_count > 0 it also
+ * returns corr[k] = sum_i q8[(domains[k]*8 + syms[k])*N + i] * b_i for range ranges[k] (the
+ * survivor evaluation's exact DP2A correlation, encoder.cpp:236-241). */
+int32_t fic_debug_pool(const uint8_t* image, int32_t width, int32_t height, const fic_params* params,
+                       int64_t* sq, int64_t* den, uint16_t* q8, uint64_t* flat_count,
+                       int32_t probe_count, const int32_t* ranges, const int32_t* domains,
+                       const int32_t* syms, int64_t* corr);
 /* (diagnostics) clock64 stamps of scan CTA 0's first 256 tiles recorded under FIC_DEBUG=32:
  * per tile 51 slots (MMA issuer before/after the TMEM-buffer wait and after the pool tile landed,
  * each of the 16 epilogue warps releasing the tile, finishing it, and past its per-range test).

@@ -242,6 +242,8 @@ class Reference:
         L.ref_smooth_image.argtypes = [i32, u32, vp]
         L.ref_psnr.argtypes = [vp, vp, i32, i32]
         L.ref_psnr.restype = f64
+        L.ref_least_squares.argtypes = [i32, vp, i32, vp, i32, vp, f64, vp]
+        L.ref_is_shadow.argtypes = [vp, i32, f64]
 
     def _err(self):
         return self.L.ref_last_error().decode()
@@ -334,3 +336,18 @@ class Reference:
         a = np.ascontiguousarray(a, np.uint8)
         b = np.ascontiguousarray(b, np.uint8)
         return float(self.L.ref_psnr(ptr(a), ptr(b), a.shape[1], a.shape[0]))
+
+    def least_squares(self, kind, a, b, params=None, shadow_eps=0.0):
+        """kind: 'fit' | 'clamped' | 'quantized' -> (s, o, residual, qs, qo)."""
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.zeros(5, np.float64)
+        k = {"fit": 0, "clamped": 1, "quantized": 2}[kind]
+        p = _params(params if params is not None else {})
+        _check(self.L.ref_least_squares(k, ptr(a), a.shape[0], ptr(b), b.shape[0], ctypes.byref(p),
+                                        float(shadow_eps), ptr(out)), self._err)
+        return float(out[0]), float(out[1]), float(out[2]), int(out[3]), int(out[4])
+
+    def is_shadow(self, b, eps=0.0):
+        b = np.ascontiguousarray(b, np.float64)
+        return bool(self.L.ref_is_shadow(ptr(b), b.shape[0], float(eps)))

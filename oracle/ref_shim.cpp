@@ -196,6 +196,29 @@ int64_t ref_serialize(const fic_mapping* maps, int32_t w, int32_t h, const fic_p
   return rc ? -static_cast<int64_t>(rc) : n;
 }
 
+// The public per-candidate fit pipeline (proj/src/encoder.cpp:60-102).  kind 0:
+// least_squares_fit(shadow_eps), 1: least_squares_clamped, 2: least_squares; out = {s, o,
+// residual, qs, qo}.
+int32_t ref_least_squares(int32_t kind, const double* a, int32_t side_a, const double* b, int32_t side_b,
+                          const fic_params* p, double shadow_eps, double* out) {
+  return guard([&] {
+    const fic::Block A(side_a, std::vector<double>(a, a + static_cast<size_t>(side_a) * side_a));
+    const fic::Block B(side_b, std::vector<double>(b, b + static_cast<size_t>(side_b) * side_b));
+    if (kind == 2) {
+      const fic::QuantizedFit q = fic::least_squares(A, B, to_params(p));
+      out[0] = q.s, out[1] = q.o, out[2] = q.residual, out[3] = q.qs, out[4] = q.qo;
+    } else {
+      const fic::LinearFit f =
+          kind == 0 ? fic::least_squares_fit(A, B, shadow_eps) : fic::least_squares_clamped(A, B, to_params(p));
+      out[0] = f.s, out[1] = f.o, out[2] = f.residual, out[3] = out[4] = 0;
+    }
+  });
+}
+
+int32_t ref_is_shadow(const double* b, int32_t side, double eps) {
+  return fic::is_shadow(fic::Block(side, std::vector<double>(b, b + static_cast<size_t>(side) * side)), eps) ? 1 : 0;
+}
+
 void ref_noise_image(int32_t side, uint32_t seed, uint8_t* out) {
   const auto g = fic::testing::noise_image(side, seed);
   std::memcpy(out, g.data.data(), g.data.size());

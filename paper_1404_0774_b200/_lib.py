@@ -45,13 +45,20 @@ def _declare(L):
     L.fic_last_survivors.argtypes = [vp, i32]
     L.fic_debug_trace.argtypes = [vp, i32]
     L.fic_decode_timing.argtypes = [vp, vp, vp, i32]
+    L.fic_is_shadow.argtypes = [vp, i32, f64, vp]
+    L.fic_least_squares_fit.argtypes = [vp, i32, vp, i32, f64, vp]
+    L.fic_least_squares_clamped.argtypes = [vp, i32, vp, i32, vp, vp]
+    L.fic_least_squares.argtypes = [vp, i32, vp, i32, vp, vp]
+    L.fic_debug_pool.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]
     L.fic_set_device.argtypes = [i32]
     L.fic_device_count.argtypes = [vp]
     for name in ["fic_normalize_params", "fic_validate_geometry", "fic_encode", "fic_encode_parallel",
                  "fic_encode_range", "fic_encode_rows", "fic_encode_batch", "fic_encode_device",
                  "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
-                 "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace"]:
+                 "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace",
+                 "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
+                 "fic_debug_pool"]:
         getattr(L, name).restype = i32
     return L
 
@@ -77,5 +84,6 @@ EXPORTS = [
     "fic_encode_device", "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
     "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
-    "fic_debug_trace",
+    "fic_debug_trace", "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
+    "fic_debug_pool",
 ]

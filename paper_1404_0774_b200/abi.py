@@ -71,6 +71,15 @@ class FicStats(ctypes.Structure):
         }
 
 
+class FicLinearFit(ctypes.Structure):  # LinearFit (proj/include/fic/encoder.hpp:15-19)
+    _fields_ = [("s", ctypes.c_double), ("o", ctypes.c_double), ("residual", ctypes.c_double)]
+
+
+class FicQuantizedFit(ctypes.Structure):  # QuantizedFit (proj/include/fic/encoder.hpp:24-30)
+    _fields_ = [("qs", ctypes.c_uint32), ("qo", ctypes.c_uint32), ("s", ctypes.c_double), ("o", ctypes.c_double),
+                ("residual", ctypes.c_double)]
+
+
 MAPPING_DTYPE = np.dtype(
     [("x", "<i4"), ("y", "<i4"), ("sym", "<i4"), ("qs", "<u4"), ("qo", "<u4"),
      ("reserved", "<i4"), ("residual", "<f8")]

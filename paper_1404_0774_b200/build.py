@@ -12,11 +12,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("FIC_LIB") or os.path.join(HERE, "libfic_b200.so")
-SOURCES = ["fic_api.cu", "pool.cu", "matcher_simt.cu", "scan.cu", "decoder.cu"]
-HEADERS = ["common.cuh", "tc_ptx.cuh", "tc2_ptx.cuh", os.path.join("..", "..", "include", "fic_b200.h")]
+SOURCES = ["fic_api.cu", "pool.cu", "matcher_simt.cu", "scan.cu", "decoder.cu", "fit.cu"]
+HEADERS = ["common.cuh", "tc_ptx.cuh", os.path.join("..", "..", "include", "fic_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
          "-Xptxas", "-warn-spills"] + (["-DFIC_TRACE"] if os.environ.get("FIC_TRACE") else [])  # pipeline trace build
 
 

@@ -271,6 +271,101 @@ def psnr(a, b):
     return float(20.0 * np.log10(255.0 / e))
 
 
+# ---------------------------------------------------------------- per-candidate fit pipeline
+class LinearFit:
+    """LinearFit (proj/include/fic/encoder.hpp:15-19)."""
+
+    __slots__ = ("s", "o", "residual")
+
+    def __init__(self, s=0.0, o=0.0, residual=0.0):
+        self.s, self.o, self.residual = float(s), float(o), float(residual)
+
+    def __repr__(self):
+        return f"LinearFit(s={self.s!r}, o={self.o!r}, residual={self.residual!r})"
+
+
+class QuantizedFit:
+    """QuantizedFit (proj/include/fic/encoder.hpp:24-30)."""
+
+    __slots__ = ("qs", "qo", "s", "o", "residual")
+
+    def __init__(self, qs=0, qo=0, s=0.0, o=0.0, residual=0.0):
+        self.qs, self.qo = int(qs), int(qo)
+        self.s, self.o, self.residual = float(s), float(o), float(residual)
+
+    def __repr__(self):
+        return f"QuantizedFit(qs={self.qs}, qo={self.qo}, s={self.s!r}, o={self.o!r}, residual={self.residual!r})"
+
+
+def _block(samples):
+    """A fic::Block (proj/include/fic/transforms.hpp:13-25): a square 2-D array of samples."""
+    b = np.ascontiguousarray(np.asarray(samples, dtype=np.float64))
+    if b.ndim != 2 or b.shape[0] != b.shape[1]:
+        raise ValueError("expected a square 2D block of samples (side x side)")
+    return b, int(b.shape[0])
+
+
+def is_shadow(block, eps=0.0):
+    """is_shadow (proj/src/encoder.cpp:60-67): N*sum(b^2) - sum(b)^2 <= eps."""
+    b, side = _block(block)
+    out = ctypes.c_int32()
+    _check(lib().fic_is_shadow(ptr(b), side, float(eps), ctypes.byref(out)))
+    return bool(out.value)
+
+
+def least_squares_fit(a, b, shadow_eps=0.0):
+    """least_squares_fit (proj/src/encoder.cpp:69-76): unconstrained fit of b ~ s*a + o."""
+    (a, sa), (b, sb) = _block(a), _block(b)
+    f = abi.FicLinearFit()
+    _check(lib().fic_least_squares_fit(ptr(a), sa, ptr(b), sb, float(shadow_eps), ctypes.byref(f)))
+    return LinearFit(f.s, f.o, f.residual)
+
+
+def least_squares_clamped(a, b, params=None):
+    """least_squares_clamped (proj/src/encoder.cpp:78-88): s clamped, o re-fitted and clamped."""
+    params = CodecParams() if params is None else params
+    (a, sa), (b, sb) = _block(a), _block(b)
+    f = abi.FicLinearFit()
+    _check(lib().fic_least_squares_clamped(ptr(a), sa, ptr(b), sb, ctypes.byref(params.struct), ctypes.byref(f)))
+    return LinearFit(f.s, f.o, f.residual)
+
+
+def least_squares(a, b, params=None):
+    """least_squares (proj/src/encoder.cpp:90-102): clamped fit through the quantisers."""
+    params = CodecParams() if params is None else params
+    (a, sa), (b, sb) = _block(a), _block(b)
+    f = abi.FicQuantizedFit()
+    _check(lib().fic_least_squares(ptr(a), sa, ptr(b), sb, ctypes.byref(params.struct), ctypes.byref(f)))
+    return QuantizedFit(f.qs, f.qo, f.s, f.o, f.residual)
+
+
+def debug_pool(image, params=None, probes=None, want_q8=True):
+    """(test support) K1 read-back (C-ABI fic_debug_pool): the device pool's exact moments
+    {sq, den (-1 = flat)}, its u16 cells per isometry q8[d, s, i] = q[perm_s(i)], the flat
+    count and, for `probes` = (ranges, domains, syms) index arrays, the survivor evaluation's
+    exact correlations sum_i q8[d, s, i] * b_i."""
+    params = CodecParams() if params is None else params
+    img = _u8_2d(image)
+    h, w = img.shape
+    p = params
+    D = (((w - 2 * p.n) // p.step + 1) ** 2) if w >= 2 * p.n else 0
+    sq = np.zeros(max(D, 1), np.int64)
+    den = np.zeros(max(D, 1), np.int64)
+    q8 = np.zeros((max(D, 1), 8, p.n * p.n), np.uint16) if want_q8 else None
+    flat = ctypes.c_uint64()
+    if probes is not None:
+        rr, dd, ss = (np.ascontiguousarray(x, np.int32) for x in probes)
+        corr = np.zeros(len(rr), np.int64)
+        args = (len(rr), ptr(rr), ptr(dd), ptr(ss), ptr(corr))
+    else:
+        corr = None
+        args = (0, None, None, None, None)
+    _check(lib().fic_debug_pool(ptr(img), w, h, ctypes.byref(p.struct), ptr(sq), ptr(den), ptr(q8),
+                                ctypes.byref(flat), *args))
+    return {"sq": sq[:D], "den": den[:D], "q8": q8[:D] if want_q8 else None, "flat_count": int(flat.value),
+            "corr": corr}
+
+
 def set_device(device):
     """(extension) select the CUDA device for this thread's codec calls."""
     _check(lib().fic_set_device(int(device)))

@@ -41,24 +41,27 @@ constexpr int kDecodeThreads = 256;
 
 __global__ void __launch_bounds__(kDecodeThreads)
 decode_step_kernel(const double* __restrict__ cur, double* __restrict__ nxt, const RangeXform* __restrict__ xf,
-                   int out_w, int kn, int ranges_x, double* __restrict__ partial) {
+                   int out_w, int out_h, int kn, int ranges_x, int ranges_y, double* __restrict__ partial) {
   const long long idx = (long long)blockIdx.x * kDecodeThreads + threadIdx.x;
-  const long long total = (long long)out_w * out_w;
+  const long long total = (long long)out_w * out_h;
   double sq = 0.0;
   if (idx < total) {
     const int Y = (int)(idx / out_w), X = (int)(idx % out_w);
     const int ry = Y / kn, rx = X / kn;
-    const int r = Y - ry * kn, c = X - rx * kn;
-    const RangeXform t = xf[ry * ranges_x + rx];
-    int sr, sc;
-    symmetry_source(t.sym, r, c, kn, sr, sc);
-    const double* row0 = cur + (long long)(t.dy + 2 * sr) * out_w + t.dx + 2 * sc;
-    const double* row1 = row0 + out_w;
-    // ((p00 + p01) + p10 + p11) / 4.0 then s*z + o, each op rounded (decoder.cpp:71-75); the
-    // division by 4 is an exact power-of-two scaling, identical to the multiplication by 0.25
-    const double z = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(__ldg(row0), __ldg(row0 + 1)), __ldg(row1)), __ldg(row1 + 1)),
-                               0.25);
-    const double v = __dadd_rn(__dmul_rn(t.s, z), t.o);
+    double v = 0.0;  // pixels outside the range grid keep constant_raster's 0 (decoder.cpp:56)
+    if (rx < ranges_x && ry < ranges_y) {
+      const int r = Y - ry * kn, c = X - rx * kn;
+      const RangeXform t = xf[ry * ranges_x + rx];
+      int sr, sc;
+      symmetry_source(t.sym, r, c, kn, sr, sc);
+      const double* row0 = cur + (long long)(t.dy + 2 * sr) * out_w + t.dx + 2 * sc;
+      const double* row1 = row0 + out_w;
+      // ((p00 + p01) + p10 + p11) / 4.0 then s*z + o, each op rounded (decoder.cpp:71-75); the
+      // division by 4 is an exact power-of-two scaling, identical to the multiplication by 0.25
+      const double z =
+          __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(__ldg(row0), __ldg(row0 + 1)), __ldg(row1)), __ldg(row1 + 1)), 0.25);
+      v = __dadd_rn(__dmul_rn(t.s, z), t.o);
+    }
     nxt[idx] = v;
     const double dlt = __dsub_rn(cur[idx], v);
     sq = __dmul_rn(dlt, dlt);
@@ -77,7 +80,7 @@ decode_step_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
 }
 
 // Tiled variant of decode_step_kernel for the common geometries (kn a multiple of 32, or a
-// divisor of 32 with the raster a whole number of 32 x 32 tiles).  One CTA per 32 x 32 output
+// divisor of 32 with the raster a whole number of 32 x 32 tiles, ranges covering it).  One CTA per 32 x 32 output
 // tile, i.e. (32/T)^2 blocks of T x T output pixels (T = min(kn, 32)), each block the whole
 // range (kn <= 32) or a sub-square of one (kn > 32).  An isometry maps an aligned T x T
 // sub-square of the range onto an aligned T x T sub-square of its source, so phase 1 loads
@@ -89,8 +92,8 @@ decode_step_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
 constexpr int kTile = 32;
 constexpr int kTileThreads = 256;
 
-bool decode_tiled(int out_w, int kn) {
-  if (out_w % kTile != 0) return false;
+bool decode_tiled(int out_w, int out_h, int kn) {
+  if (out_w % kTile != 0 || out_h % kTile != 0) return false;
   return kn >= kTile ? kn % kTile == 0 : (kTile % kn == 0 && kn >= 2);
 }
 
@@ -193,19 +196,21 @@ decode_tile_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
 
 // ------------------------------------------------------------------ mean-raster decoder
 // Every 2x2 mean the decoder reads, z = ((p00 + p01) + p10 + p11) / 4 at (dy + 2 sr, dx + 2 sc),
-// lies on the even grid whenever the magnified domain origins (multiples of step * scale) are
-// even.  Then an iteration needs only the half-resolution MEAN raster m(i, j) = z at
+// lies on the even grid whenever every magnified domain origin (dx, dy) is even (checked on
+// the host against the actual mappings: scale even, or every x and y even).  Then an iteration needs only the half-resolution MEAN raster m(i, j) = z at
 // (2i, 2j) of the current raster (a quarter of its size, L2-resident up to 8192^2 outputs),
 // and each output tile, being 32 x 32 at even coordinates, yields the next iteration's means
 // of its own outputs.  Per iteration the full raster is written once and read once (the
 // step RMSE's current values), instead of gathering four doubles per output pixel.  Same
 // per-value arithmetic in the same order, so every raster value is bit-identical.
-bool decode_mean_ok(int out_w, int kn, int step_scale) { return decode_tiled(out_w, kn) && step_scale % 2 == 0; }
+bool decode_mean_ok(int out_w, int out_h, int kn, bool even_origins) {
+  return decode_tiled(out_w, out_h, kn) && even_origins;
+}
 
-__global__ void mean_raster_kernel(const double* __restrict__ r, double* __restrict__ m, int out_w) {
+__global__ void mean_raster_kernel(const double* __restrict__ r, double* __restrict__ m, int out_w, int out_h) {
   const int hw = out_w / 2;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long long)hw * hw) return;
+  if (i >= (long long)hw * (out_h / 2)) return;
   const int y = (int)(i / hw), x = (int)(i % hw);
   const double* p = r + (long long)(2 * y) * out_w + 2 * x;
   m[i] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), p[out_w]), p[out_w + 1]), 0.25);
@@ -349,15 +354,15 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
   }
 }
 
-void launch_mean_raster(const double* r, double* m, int out_w, cudaStream_t st) {
-  const long long n = (long long)(out_w / 2) * (out_w / 2);
-  mean_raster_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(r, m, out_w);
+void launch_mean_raster(const double* r, double* m, int out_w, int out_h, cudaStream_t st) {
+  const long long n = (long long)(out_w / 2) * (out_h / 2);
+  mean_raster_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(r, m, out_w, out_h);
 }
 
 // One iteration on the mean raster (decode_mean_ok); partials as decode_partials.
 void launch_decode_mean(const double* cur, const double* mcur, double* nxt, double* mnxt, const RangeXform* xf,
-                        int out_w, int kn, int ranges_x, double* partial, cudaStream_t st) {
-  const dim3 grid(out_w / kTile, out_w / kTile);
+                        int out_w, int out_h, int kn, int ranges_x, double* partial, cudaStream_t st) {
+  const dim3 grid(out_w / kTile, out_h / kTile);
 #define FIC_MEAN(LT) decode_mean_kernel<LT><<<grid, kTileThreads, 0, st>>>(cur, mcur, nxt, mnxt, xf, out_w, kn, ranges_x, partial)
   switch (kn >= kTile ? 5 : __builtin_ctz((unsigned)kn)) {
     case 1: FIC_MEAN(1); break;
@@ -369,10 +374,14 @@ void launch_decode_mean(const double* cur, const double* mcur, double* nxt, doub
 #undef FIC_MEAN
 }
 
-// Sums the per-block partials in index order and writes rmse = sqrt(sum / count).
+// Sums the per-block partials in index order and writes rmse = sqrt(sum / count); block k
+// finishes iteration k (partials partial[k * blocks ...], result out[k]), so a decode without
+// a convergence test reduces every iteration's partials in one launch at the end.
 __global__ void rmse_finish_kernel(const double* __restrict__ partial, int blocks, long long count,
                                    double* __restrict__ out) {
   __shared__ double red[1024];
+  partial += (long long)blockIdx.x * blocks;
+  out += blockIdx.x;
   double s = 0.0;
   for (int i = threadIdx.x; i < blocks; i += blockDim.x) s = __dadd_rn(s, partial[i]);
   red[threadIdx.x] = s;
@@ -401,28 +410,35 @@ __global__ void quantize_raster_kernel(const double* __restrict__ r, long long c
 int decode_blocks(long long count) { return (int)((count + kDecodeThreads - 1) / kDecodeThreads); }
 
 // Partials one decode step writes.
-int decode_partials(int out_w, int kn) {
-  if (decode_tiled(out_w, kn) && !std::getenv("FIC_DECODE_FLAT")) return (out_w / kTile) * (out_w / kTile);
-  return decode_blocks((long long)out_w * out_w);
+int decode_partials(int out_w, int out_h, int kn, bool covers) {
+  if (covers && decode_tiled(out_w, out_h, kn) && !std::getenv("FIC_DECODE_FLAT"))
+    return (out_w / kTile) * (out_h / kTile);
+  return decode_blocks((long long)out_w * out_h);
 }
 
 void launch_xform(const fic_mapping* maps, int count, int scale, const Geometry& g, RangeXform* xf, cudaStream_t st) {
   xform_kernel<<<(count + 255) / 256, 256, 0, st>>>(maps, count, scale, g.s_bits, g.s_max, g.o_bits, xf);
 }
 
-void launch_decode_step(const double* cur, double* nxt, const RangeXform* xf, int out_w, int kn, int ranges_x,
-                        double* partial, cudaStream_t st) {
-  const long long count = (long long)out_w * out_w;
-  if (decode_tiled(out_w, kn) && !std::getenv("FIC_DECODE_FLAT")) {
-    decode_tile_kernel<<<(out_w / kTile) * (out_w / kTile), kTileThreads, 0, st>>>(cur, nxt, xf, out_w, kn, ranges_x,
+// ranges_x x ranges_y ranges of kn x kn pixels; the tiled kernel needs them to cover the raster
+// (fic_decode passes covers = width % n == 0 && height % n == 0).
+void launch_decode_step(const double* cur, double* nxt, const RangeXform* xf, int out_w, int out_h, int kn,
+                        int ranges_x, int ranges_y, double* partial, cudaStream_t st) {
+  const long long count = (long long)out_w * out_h;
+  const bool covers = (long long)ranges_x * kn == out_w && (long long)ranges_y * kn == out_h;
+  if (covers && decode_tiled(out_w, out_h, kn) && !std::getenv("FIC_DECODE_FLAT")) {
+    decode_tile_kernel<<<(out_w / kTile) * (out_h / kTile), kTileThreads, 0, st>>>(cur, nxt, xf, out_w, kn, ranges_x,
                                                                                    partial);
     return;
   }
-  decode_step_kernel<<<decode_blocks(count), kDecodeThreads, 0, st>>>(cur, nxt, xf, out_w, kn, ranges_x, partial);
+  decode_step_kernel<<<decode_blocks(count), kDecodeThreads, 0, st>>>(cur, nxt, xf, out_w, out_h, kn, ranges_x,
+                                                                      ranges_y, partial);
 }
 
-void launch_rmse_finish(const double* partial, int blocks, long long count, double* out, cudaStream_t st) {
-  rmse_finish_kernel<<<1, 1024, 0, st>>>(partial, blocks, count, out);
+// `iterations` reductions of `blocks` partials each (consecutive), one block per iteration.
+void launch_rmse_finish(const double* partial, int blocks, long long count, double* out, int iterations,
+                        cudaStream_t st) {
+  rmse_finish_kernel<<<iterations, 1024, 0, st>>>(partial, blocks, count, out);
 }
 
 void launch_raster_init(double* r, long long count, int kind, const unsigned char* supplied, cudaStream_t st) {

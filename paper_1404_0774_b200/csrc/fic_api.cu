@@ -39,14 +39,14 @@ struct RangeXform {
   int pad;
 };
 int decode_blocks(long long);
-int decode_partials(int, int);
+int decode_partials(int, int, int, bool);
 void launch_xform(const fic_mapping*, int, int, const Geometry&, RangeXform*, cudaStream_t);
-void launch_decode_step(const double*, double*, const RangeXform*, int, int, int, double*, cudaStream_t);
-void launch_rmse_finish(const double*, int, long long, double*, cudaStream_t);
-bool decode_mean_ok(int, int, int);
-void launch_mean_raster(const double*, double*, int, cudaStream_t);
-void launch_decode_mean(const double*, const double*, double*, double*, const RangeXform*, int, int, int, double*,
-                        cudaStream_t);
+void launch_decode_step(const double*, double*, const RangeXform*, int, int, int, int, int, double*, cudaStream_t);
+void launch_rmse_finish(const double*, int, long long, double*, int, cudaStream_t);
+bool decode_mean_ok(int, int, int, bool);
+void launch_mean_raster(const double*, double*, int, int, cudaStream_t);
+void launch_decode_mean(const double*, const double*, double*, double*, const RangeXform*, int, int, int, int,
+                        double*, cudaStream_t);
 void launch_raster_init(double*, long long, int, const unsigned char*, cudaStream_t);
 void launch_quantize_raster(const double*, long long, unsigned char*, cudaStream_t);
 // scan.cu (tcgen05 path, n in {2, 4, 8})
@@ -67,12 +67,11 @@ cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const _
 size_t scan_rec_bytes(unsigned long long, int);
 int scan_trace_copy(long long*, int);
 int scan_padded_ranges(const Geometry&);
-bool scan_pair_mode();
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
 bool scan_use_f16acc(const Geometry&, int stride, int sms);
 size_t range_op_bytes(const Geometry&);
 void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, const unsigned long long*, float*,
-                      unsigned char*, bool, unsigned long long*, unsigned*, unsigned long long*, cudaStream_t);
+                      unsigned char*, unsigned long long*, unsigned*, unsigned long long*, cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
                  const double*, uint2*, unsigned*, int, cudaStream_t);
@@ -81,6 +80,8 @@ void launch_winner(const uint2*, const unsigned long long*, int, unsigned long l
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
                    const RangeMeta*, const unsigned*, const unsigned long long*, fic_mapping*, unsigned long long*,
                    cudaStream_t);
+void launch_probe_corr(const unsigned char*, const Geometry&, const unsigned short*, int, const int*, const int*,
+                       const int*, long long*, cudaStream_t);
 }  // namespace ficb
 
 using namespace ficb;
@@ -333,6 +334,9 @@ std::vector<int> scan_levels(const Geometry& g) {
     for (int s = 4; tiles >= 8 * s; s *= 8) rev.push_back(s);
     lv.assign(rev.rbegin(), rev.rend());
   }
+  // the host keeps kMaxLevels counter partitions (sparse levels + the full one): an override
+  // with more levels keeps its last (densest) kMaxLevels - 1 sparse levels
+  if (lv.size() > (size_t)kMaxLevels - 1) lv.erase(lv.begin(), lv.end() - (kMaxLevels - 1));
   lv.push_back(1);
   return lv;
 }
@@ -370,7 +374,6 @@ ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
 // their exact evaluation.  cnt: the level's kPartSlots counters.
 void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, int stride,
                    unsigned long long* cnt, cudaStream_t st) {
-  const int first_stride = scan_levels(g).front();  // pair mode builds the (unscaled) range operands once
   auto* list = static_cast<uint2*>(ws.list.get((size_t)ws.list_cap * sizeof(uint2)));
   auto* res = static_cast<double*>(ws.res.get((size_t)ws.list_cap * sizeof(double)));
   const int parts = scan_grid(g, stride, ws.sms);
@@ -384,8 +387,7 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   // the full level of a large pool accumulates in fp16 (flags & 256: its thresholds and its scan)
   Geometry gl = g;
   gl.flags = scan_use_f16acc(g, stride, ws.sms) ? (g.flags | 256) : (g.flags & ~256);
-  launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, !scan_pair_mode() || stride == first_stride,
-                   b.cnt + kPendSlot, final_level ? b.win : nullptr, final_level ? b.cnt + kSelfcheckSlot : nullptr,
+  launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, b.cnt + kPendSlot, final_level ? b.win : nullptr, final_level ? b.cnt + kSelfcheckSlot : nullptr,
                    st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
@@ -398,7 +400,7 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   }
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
               pendc, ws.sms, st);
-  g_launches += 5;  // level ops, scan, expand (or the pair scan's range rows), evaluation, residuals
+  g_launches += 5;  // level ops, scan, expand, evaluation, residuals
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a
@@ -748,12 +750,17 @@ int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, f
   });
 }
 
-// dequantize range check of decode_step (format.hpp:34-40) plus window bounds
-int32_t check_mappings(const fic_mapping* maps, int w, int h, const fic_params& p) {
+// dequantize range check of decode_step (format.hpp:34-40) plus window bounds.  `odd` (may be
+// null) is set when some domain origin has an odd coordinate (the mean-raster decoder then
+// does not apply at odd magnifications).
+int32_t check_mappings(const fic_mapping* maps, int w, int h, const fic_params& p, bool* odd = nullptr) {
   const unsigned smc = (1u << p.s_bits) - 1u, omc = (1u << p.o_bits) - 1u;
   const long count = (long)(w / p.n) * (h / p.n);
+  if (count > 0 && !maps) return fail(FIC_ERR_BAD_PARAMS, "null mapping buffer");
+  if (odd) *odd = false;
   for (long i = 0; i < count; ++i) {
     const fic_mapping& m = maps[i];
+    if (odd && ((m.x | m.y) & 1)) *odd = true;
     if (m.qs > smc) return fail(FIC_ERR_OUT_OF_RANGE, "code " + std::to_string(m.qs) + " exceeds " + std::to_string(smc));
     if (m.qo > omc) return fail(FIC_ERR_OUT_OF_RANGE, "code " + std::to_string(m.qo) + " exceeds " + std::to_string(omc));
     if (m.sym < 0 || m.sym > 7) return fail(FIC_ERR_OUT_OF_RANGE, "symmetry index " + std::to_string(m.sym));
@@ -765,6 +772,10 @@ int32_t check_mappings(const fic_mapping* maps, int w, int h, const fic_params& 
 }
 
 }  // namespace
+
+namespace ficb {
+int32_t api_fail(int32_t code, const std::string& detail) { return fail(code, detail); }
+}  // namespace ficb
 
 extern "C" {
 
@@ -936,31 +947,93 @@ int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height,
   });
 }
 
+// (test support) K1 read-back and the survivor evaluation's exact correlations.
+int32_t fic_debug_pool(const uint8_t* image, int32_t width, int32_t height, const fic_params* params, int64_t* sq,
+                       int64_t* den, uint16_t* q8, uint64_t* flat_count, int32_t probe_count, const int32_t* ranges,
+                       const int32_t* domains, const int32_t* syms, int64_t* corr) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  if (!image) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  Geometry g = make_geometry(width, height, p);
+  if (!scan_supported(g)) return fail(FIC_ERR_BAD_PARAMS, "the tcgen05 pool covers n in {2, 4, 8}");
+  if (probe_count < 0 || (probe_count > 0 && (!ranges || !domains || !syms || !corr)))
+    return fail(FIC_ERR_BAD_PARAMS, "probe buffers");
+  for (int32_t i = 0; i < probe_count; ++i)
+    if (ranges[i] < 0 || ranges[i] >= g.R || domains[i] < 0 || domains[i] >= g.D || syms[i] < 0 || syms[i] > 7)
+      return fail(FIC_ERR_OUT_OF_RANGE, "probe " + std::to_string(i));
+  g.Dt = (int)scan_pool_domains(g);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    const size_t img_bytes = (size_t)g.W * g.H;
+    auto* d_img = static_cast<unsigned char*>(ws.img.get(img_bytes));
+    const ScanBufs b = scan_bufs(ws, g);
+    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
+    CK(cudaMemcpyAsync(d_img, image, img_bytes, cudaMemcpyHostToDevice, ws.stream));
+    CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), ws.stream));
+    launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_cnt, ws.stream);
+    g_launches += 1;
+    std::vector<DomainMetaI> mi(g.D);
+    CK(cudaMemcpyAsync(mi.data(), b.mi, (size_t)g.D * sizeof(DomainMetaI), cudaMemcpyDeviceToHost, ws.stream));
+    if (q8)
+      CK(cudaMemcpyAsync(q8, b.qpool, (size_t)g.D * kSyms * g.N * sizeof(uint16_t), cudaMemcpyDeviceToHost,
+                         ws.stream));
+    unsigned long long flat = 0;
+    CK(cudaMemcpyAsync(&flat, d_cnt, sizeof flat, cudaMemcpyDeviceToHost, ws.stream));
+    if (probe_count > 0) {
+      auto* dcorr = static_cast<long long*>(ws.scratch.get((size_t)probe_count * (3 * sizeof(int) + sizeof(long long))));
+      auto* buf = reinterpret_cast<int*>(dcorr + probe_count);
+      CK(cudaMemcpyAsync(buf, ranges, probe_count * sizeof(int), cudaMemcpyHostToDevice, ws.stream));
+      CK(cudaMemcpyAsync(buf + probe_count, domains, probe_count * sizeof(int), cudaMemcpyHostToDevice, ws.stream));
+      CK(cudaMemcpyAsync(buf + 2 * probe_count, syms, probe_count * sizeof(int), cudaMemcpyHostToDevice, ws.stream));
+      launch_probe_corr(d_img, g, b.qpool, probe_count, buf, buf + probe_count, buf + 2 * probe_count, dcorr,
+                        ws.stream);
+      g_launches += 1;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(corr, dcorr, probe_count * sizeof(long long), cudaMemcpyDeviceToHost, ws.stream));
+    }
+    CK(cudaStreamSynchronize(ws.stream));
+    for (int d = 0; d < g.D; ++d) {
+      if (sq) sq[d] = mi[d].sq;
+      if (den) den[d] = mi[d].den;
+    }
+    if (flat_count) *flat_count = flat;
+    return FIC_OK;
+  });
+}
+
 int32_t fic_decode_step(const double* current, int32_t cur_width, int32_t cur_height, const fic_mapping* maps,
                         int32_t width, int32_t height, const fic_params* params, int32_t scale, double* next) {
+  // decode_step (decoder.cpp:39-50) validation order
   if (scale < 1) return fail(FIC_ERR_BAD_PARAMS, "scale must be >= 1");
   fic_params p;
   int32_t e = normalize(params, &p);
   if (e) return e;
+  if (width < 0 || height < 0) return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
   const int out_w = width * scale, out_h = height * scale;
   if (cur_width != out_w || cur_height != out_h)
     return fail(FIC_ERR_SCALE_MISMATCH, "raster is " + std::to_string(cur_width) + "x" + std::to_string(cur_height) +
                                             ", expected " + std::to_string(out_w) + "x" + std::to_string(out_h));
-  if (width != height || width % p.n != 0) return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
   if ((e = check_mappings(maps, width, height, p))) return e;
+  const long long cnt = (long long)out_w * out_h;
+  if (cnt == 0) return FIC_OK;
+  if (!current || !next) return fail(FIC_ERR_BAD_PARAMS, "null raster");
   const Geometry g = make_geometry(width, height, p);
   return guarded([&]() -> int32_t {
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> lock(ws.mu);
-    const long long cnt = (long long)out_w * out_h;
-    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
-    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)g.R * sizeof(RangeXform)));
+    const int rx = width / p.n, ry = height / p.n;
+    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)std::max(1, rx * ry) * sizeof(fic_mapping)));
+    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)std::max(1, rx * ry) * sizeof(RangeXform)));
     auto* a = static_cast<double*>(ws.ra.get((size_t)cnt * 8));
     auto* b = static_cast<double*>(ws.rb.get((size_t)cnt * 8));
-    CK(cudaMemcpyAsync(d_maps, maps, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
+    if (rx * ry > 0)
+      CK(cudaMemcpyAsync(d_maps, maps, (size_t)rx * ry * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
     CK(cudaMemcpyAsync(a, current, (size_t)cnt * 8, cudaMemcpyHostToDevice, ws.stream));
-    launch_xform(d_maps, g.R, scale, g, xf, ws.stream);
-    launch_decode_step(a, b, xf, out_w, p.n * scale, g.RX, nullptr, ws.stream);
+    if (rx * ry > 0) launch_xform(d_maps, rx * ry, scale, g, xf, ws.stream);
+    launch_decode_step(a, b, xf, out_w, out_h, p.n * scale, rx, ry, nullptr, ws.stream);
     CK(cudaGetLastError());
     g_launches += 2;
     CK(cudaMemcpyAsync(next, b, (size_t)cnt * 8, cudaMemcpyDeviceToHost, ws.stream));
@@ -973,9 +1046,11 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
                    int32_t iterations, int32_t initial_kind, const uint8_t* supplied, int32_t supplied_width,
                    int32_t supplied_height, int32_t has_eps, double convergence_eps, uint8_t* out, double* step_rmse,
                    int32_t* iterations_run) {
-  // decode_traced (decoder.cpp:113-128) validation order
+  // decode_traced (decoder.cpp:113-128) validation order: scale, iterations, initial raster
+  // (initial_raster, decoder.cpp:83-97), then decode_step's (params, mapping count)
   if (scale < 1) return fail(FIC_ERR_BAD_PARAMS, "scale must be >= 1");
   if (iterations < 1) return fail(FIC_ERR_BAD_PARAMS, "iterations must be >= 1");
+  if (width < 0 || height < 0) return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
   const int out_w = width * scale, out_h = height * scale;
   if (initial_kind == FIC_INITIAL_SUPPLIED) {
     if (!supplied) return fail(FIC_ERR_BAD_PARAMS, "no supplied initial image");
@@ -987,62 +1062,85 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
   fic_params p;
   int32_t e = normalize(params, &p);
   if (e) return e;
-  if (width != height || width <= 0 || width % p.n != 0)
-    return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
-  if ((e = check_mappings(maps, width, height, p))) return e;
+  bool odd = false;
+  if ((e = check_mappings(maps, width, height, p, &odd))) return e;
+  const long long cnt = (long long)out_w * out_h;
+  if (cnt > 0 && !out) return fail(FIC_ERR_BAD_PARAMS, "null output buffer");
   const Geometry g = make_geometry(width, height, p);
   return guarded([&]() -> int32_t {
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> lock(ws.mu);
-    const long long cnt = (long long)out_w * out_h;
-    const int blocks = decode_blocks(cnt);
-    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
-    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)g.R * sizeof(RangeXform)));
-    auto* a = static_cast<double*>(ws.ra.get((size_t)cnt * 8));
-    auto* b = static_cast<double*>(ws.rb.get((size_t)cnt * 8));
-    auto* part = static_cast<double*>(ws.partial_sums.get((size_t)blocks * 8));
+    const int rx = width / p.n, ry = height / p.n;
+    const int kn = p.n * scale;
+    const bool covers = rx * p.n == width && ry * p.n == height;
+    // mean-raster iterations when every 2x2 mean lies on the even grid (decoder.cu): every
+    // magnified domain origin even, checked on the actual mappings
+    const bool mean = covers && cnt > 0 && decode_mean_ok(out_w, out_h, kn, scale % 2 == 0 || !odd) &&
+                      !std::getenv("FIC_DECODE_FLAT") && !std::getenv("FIC_DECODE_TILE");
+    const int nparts = cnt > 0 ? decode_partials(out_w, out_h, kn, covers) : 1;
+    const size_t cnt_b = (size_t)std::max<long long>(cnt, 1);
+    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)std::max(1, rx * ry) * sizeof(fic_mapping)));
+    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)std::max(1, rx * ry) * sizeof(RangeXform)));
+    auto* a = static_cast<double*>(ws.ra.get(cnt_b * 8));
+    auto* b = static_cast<double*>(ws.rb.get(cnt_b * 8));
+    // step-RMSE partials of every iteration (reduced once at the end without a convergence test)
+    const int slots = has_eps ? 1 : iterations;
+    auto* part = static_cast<double*>(ws.partial_sums.get((size_t)nparts * slots * 8));
     auto* d_rmse = static_cast<double*>(ws.rmse.get((size_t)iterations * 8));
-    auto* d_u8 = static_cast<unsigned char*>(ws.u8out.get((size_t)cnt));
+    auto* d_u8 = static_cast<unsigned char*>(ws.u8out.get(cnt_b));
     auto* h_rmse = static_cast<double*>(ws.h_rmse.get((size_t)iterations * 8));
-    CK(cudaMemcpyAsync(d_maps, maps, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
+    if (cnt == 0) {  // empty raster: every step RMSE is sqrt(0 / 0) = NaN (raster_rmse, decoder.cpp:28-37),
+                     // which never passes the convergence test
+      for (int it = 0; it < iterations; ++it)
+        if (step_rmse) step_rmse[it] = std::nan("");
+      if (iterations_run) *iterations_run = iterations;
+      return FIC_OK;
+    }
+    if (rx * ry > 0)
+      CK(cudaMemcpyAsync(d_maps, maps, (size_t)rx * ry * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
     const unsigned char* d_sup = nullptr;
     if (initial_kind == FIC_INITIAL_SUPPLIED) {
       CK(cudaMemcpyAsync(d_u8, supplied, (size_t)cnt, cudaMemcpyHostToDevice, ws.stream));
       d_sup = d_u8;
     }
     launch_raster_init(a, cnt, initial_kind, d_sup, ws.stream);
-    launch_xform(d_maps, g.R, scale, g, xf, ws.stream);
-    g_launches += 2;
+    g_launches += 1;
+    if (rx * ry > 0) {
+      launch_xform(d_maps, rx * ry, scale, g, xf, ws.stream);
+      g_launches += 1;
+    }
     const bool timed = g_timing.load() != 0 && !has_eps;
     if (timed) CK(cudaEventRecord(ws.ev0, ws.stream));
     int runs = 0;
-    // mean-raster iterations when every 2x2 mean lies on the even grid (decoder.cu)
-    const int kn = p.n * scale;
-    const bool mean = decode_mean_ok(out_w, kn, p.step * scale) && !std::getenv("FIC_DECODE_FLAT") &&
-                      !std::getenv("FIC_DECODE_TILE");
     double *ma = nullptr, *mb = nullptr;
     if (mean) {
       ma = static_cast<double*>(ws.mra.get((size_t)cnt / 4 * 8));
       mb = static_cast<double*>(ws.mrb.get((size_t)cnt / 4 * 8));
-      launch_mean_raster(a, ma, out_w, ws.stream);
+      launch_mean_raster(a, ma, out_w, out_h, ws.stream);
       g_launches += 1;
     }
     for (int it = 0; it < iterations; ++it) {
+      double* pt = part + (has_eps ? 0 : (size_t)it * nparts);
       if (mean) {
-        launch_decode_mean(a, ma, b, mb, xf, out_w, kn, g.RX, part, ws.stream);
+        launch_decode_mean(a, ma, b, mb, xf, out_w, out_h, kn, rx, pt, ws.stream);
         std::swap(ma, mb);
       } else {
-        launch_decode_step(a, b, xf, out_w, kn, g.RX, part, ws.stream);
+        launch_decode_step(a, b, xf, out_w, out_h, kn, rx, ry, pt, ws.stream);
       }
-      launch_rmse_finish(part, decode_partials(out_w, kn), cnt, d_rmse + it, ws.stream);
-      g_launches += 2;
+      g_launches += 1;
       std::swap(a, b);
       ++runs;
-      if (has_eps) {
+      if (has_eps) {  // the convergence test needs this iteration's RMSE on the host now
+        launch_rmse_finish(part, nparts, cnt, d_rmse + it, 1, ws.stream);
+        g_launches += 1;
         CK(cudaMemcpyAsync(h_rmse + it, d_rmse + it, 8, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaStreamSynchronize(ws.stream));
         if (h_rmse[it] < convergence_eps) break;
       }
+    }
+    if (!has_eps) {  // every iteration's step RMSE in one launch
+      launch_rmse_finish(part, nparts, cnt, d_rmse, runs, ws.stream);
+      g_launches += 1;
     }
     if (timed) CK(cudaEventRecord(ws.ev1, ws.stream));
     launch_quantize_raster(a, cnt, d_u8, ws.stream);
@@ -1070,39 +1168,47 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
 
 int32_t fic_collage_error(const uint8_t* image, int32_t img_width, int32_t img_height, const fic_mapping* maps,
                           int32_t width, int32_t height, const fic_params* params, double* out) {
+  // collage_error (decoder.cpp:134-140): geometry first, then decode_step's checks
   if (img_width != width || img_height != height)
     return fail(FIC_ERR_DIMENSION_MISMATCH, "image does not match the encoding's geometry");
   fic_params p;
   int32_t e = normalize(params, &p);
   if (e) return e;
-  if (width != height || width <= 0 || width % p.n != 0)
-    return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
+  if (width < 0 || height < 0) return fail(FIC_ERR_BAD_PARAMS, "mapping count does not cover the range grid");
   if ((e = check_mappings(maps, width, height, p))) return e;
+  const long long cnt = (long long)width * height;
+  if (cnt > 0 && !image) return fail(FIC_ERR_BAD_PARAMS, "null image");
+  if (cnt == 0) {
+    if (out) *out = std::nan("");  // raster_rmse of empty rasters: sqrt(0 / 0)
+    return FIC_OK;
+  }
   const Geometry g = make_geometry(width, height, p);
   return guarded([&]() -> int32_t {
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> lock(ws.mu);
-    const long long cnt = (long long)width * height;
-    const int blocks = decode_blocks(cnt);
-    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
-    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)g.R * sizeof(RangeXform)));
+    const int rx = width / p.n, ry = height / p.n;
+    const bool covers = rx * p.n == width && ry * p.n == height;
+    const int nparts = decode_partials(width, height, p.n, covers);
+    auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)std::max(1, rx * ry) * sizeof(fic_mapping)));
+    auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)std::max(1, rx * ry) * sizeof(RangeXform)));
     auto* a = static_cast<double*>(ws.ra.get((size_t)cnt * 8));
     auto* b = static_cast<double*>(ws.rb.get((size_t)cnt * 8));
-    auto* part = static_cast<double*>(ws.partial_sums.get((size_t)blocks * 8));
+    auto* part = static_cast<double*>(ws.partial_sums.get((size_t)nparts * 8));
     auto* d_rmse = static_cast<double*>(ws.rmse.get(8));
     auto* d_u8 = static_cast<unsigned char*>(ws.u8out.get((size_t)cnt));
-    CK(cudaMemcpyAsync(d_maps, maps, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
+    if (rx * ry > 0)
+      CK(cudaMemcpyAsync(d_maps, maps, (size_t)rx * ry * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
     CK(cudaMemcpyAsync(d_u8, image, (size_t)cnt, cudaMemcpyHostToDevice, ws.stream));
     launch_raster_init(a, cnt, FIC_INITIAL_SUPPLIED, d_u8, ws.stream);
-    launch_xform(d_maps, g.R, 1, g, xf, ws.stream);
-    launch_decode_step(a, b, xf, width, p.n, g.RX, part, ws.stream);
-    launch_rmse_finish(part, decode_partials(width, p.n), cnt, d_rmse, ws.stream);
+    if (rx * ry > 0) launch_xform(d_maps, rx * ry, 1, g, xf, ws.stream);
+    launch_decode_step(a, b, xf, width, height, p.n, rx, ry, part, ws.stream);
+    launch_rmse_finish(part, nparts, cnt, d_rmse, 1, ws.stream);
     g_launches += 4;
     CK(cudaGetLastError());
     double r = 0;
     CK(cudaMemcpyAsync(&r, d_rmse, 8, cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
-    *out = r;
+    if (out) *out = r;
     return FIC_OK;
   });
 }

@@ -35,7 +35,6 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
-#include "tc2_ptx.cuh"
 
 namespace ficb {
 
@@ -196,9 +195,12 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
 // f16acc (the full level with an fp16 accumulator, flags & 256): each of the K/16 MMAs rounds
 // the running sum to fp16, to nearest even (pinned on the B200 by tools/f16acc_probe.cu: ties
 // and quarter points, inside a K=16 step and across steps); every partial sum is bounded by
-// sum |u_i b_i| <= |u| |b|, so the K/16 roundings add at most (K/16) 2^-11 |u| |b|.  No scaled operand (fp16) and no fp16 partial sum may
-// overflow (an inf times a zero, or meeting a -inf, gives a NaN that fails the test): a range
-// whose scaled bound |u| |b| / T (>= every |b_i - mean| / T) exceeds 60000 gets no bar.
+// sum |u_i b_i| <= |u| |b|, so the K/16 roundings add at most (K/16) 2^-11 |u| |b|.
+// Invariant: no scaled operand (fp16) and no fp16 partial sum may overflow, because the
+// epilogue's tests do not agree on non-finite values (the fp16 bit-pattern test counts inf and
+// NaN as hits, while __hmax2 in the whole-tile vote and the per-range max drops NaN operands).
+// The guard below keeps them unreachable: a range whose scaled bound |u| |b| / T (>= every
+// |b_i - mean| / T) exceeds 60000 gets no bar (all its columns pass).
 __device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, int K, bool f16acc = false) {
   const double t = (ssb - bar) - 1e-6 * (1.0 + bar);
   if (!(t > 0.0)) return -1.f;  // no usable bar (also bar == +inf): everything survives
@@ -1549,339 +1551,47 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
   out[r] = o;
 }
 
+// (test support, fic_debug_correlations) the exact integer correlation sum_i q_{perm_s(i)} b_i of
+// given (range, domain, isometry) triples, through the same q8-row / packed-range loads and
+// DP2A dot product the survivor evaluation uses (eval_fast -> dot_q_b).
+template <int NN>
+__global__ void probe_corr_kernel(const unsigned char* __restrict__ img, Geometry g,
+                                  const unsigned short* __restrict__ qpool, int count, const int* __restrict__ rr,
+                                  const int* __restrict__ dd, const int* __restrict__ ss, long long* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  int x0, y0;
+  range_origin(g, rr[i], x0, y0);
+  uint32_t qw[NN / 2], bpk[NN / 4];
+  load_q8_row<NN>(qpool, dd[i], ss[i], qw);
+  load_range_words<NN>(img, g, x0, y0, bpk);
+  out[i] = dot_q_b<NN>(qw, bpk);
+}
+
+void launch_probe_corr(const unsigned char* img, const Geometry& g, const unsigned short* qpool, int count,
+                       const int* r, const int* d, const int* s, long long* out, cudaStream_t st) {
+  const int blocks = (count + 127) / 128;
+  if (blocks == 0) return;
+  if (g.N == 4) probe_corr_kernel<4><<<blocks, 128, 0, st>>>(img, g, qpool, count, r, d, s, out);
+  else if (g.N == 16) probe_corr_kernel<16><<<blocks, 128, 0, st>>>(img, g, qpool, count, r, d, s, out);
+  else probe_corr_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, count, r, d, s, out);
+}
+
 __global__ void fill_u64_kernel(unsigned long long* p, long long n, unsigned long long v) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = v;
 }
 
-// ================================================================== CTA-pair scan
-// The same contraction with the roles the hardware favours for this shape: the ranges are
-// the resident operand A, kept in TMEM (no shared-memory reads per MMA), the pool tiles the
-// streamed operand B, split across the two CTAs of a cluster (each SM streams and holds 112
-// of the 224 domains of a tile).  tcgen05.mma.cta_group::2 M=256 (each CTA's 128 (range,
-// isometry) rows) x N=224 x K=16, accumulators in two 224-column TMEM buffers per CTA.
-// Per SM and tile: 14 KB of pool streamed and read once by the tensor core, 28672 results,
-// 448 cycles of MMA at K=64.  Each epilogue thread owns one (range, isometry) row, so its
-// threshold is a register and the test is |x| > T over 112 columns.
-constexpr int kP2Dom = 224;                     // domains per pair tile (MMA N)
-constexpr int kP2Half = kP2Dom / 2;             // domains per CTA
-constexpr int kP2Bufs = 2;                      // TMEM accumulator buffers
-constexpr int kP2Epi = 8;                       // epilogue warps per CTA
-constexpr int kP2Threads = (2 + kP2Epi) * 32;
-constexpr uint32_t kP2AccCols = kP2Dom;         // per TMEM accumulator buffer
-constexpr uint32_t kP2ACol = kP2Bufs * kP2AccCols;  // A (ranges) buffers start here: 2 x K/2 columns
-
-struct Scan2Smem {
-  uint32_t p_bytes, stages, p_off, bar_off, wbuf_off, total;
-};
-
-__host__ __device__ inline Scan2Smem scan2_smem_layout(int K) {
-  Scan2Smem L;
-  L.p_bytes = kP2Half * K * 2;
-  L.p_off = 0;
-  const uint32_t fixed = 1024;
-  uint32_t st = (kSmemBudget - fixed) / L.p_bytes;
-  L.stages = st > kScanMaxStages ? kScanMaxStages : st;
-  L.bar_off = L.p_off + L.stages * L.p_bytes;
-  L.wbuf_off = L.bar_off + 1024;
-  L.total = L.wbuf_off;
-  return L;
-}
-
-// Plain row-major range operand of every m-tile (256 rows x K fp16, unscaled): row
-// rl * 8 + s holds the centred range rl permuted by isometry s's inverse (as build_ranges).
-__global__ void __launch_bounds__(256)
-range_op2_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
-                 unsigned short* __restrict__ ropnd) {
-  const int K = g.K, N = g.N, n = g.n;
-  const int mt = blockIdx.x;
-  for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < kScanRows * K; c += blockDim.x * gridDim.y) {
-    const int row = c / K, j = c % K;
-    const int rl = row >> 3, s = row & 7;
-    const int r = mt * kScanRanges + rl;
-    const int sinv = s == 1 ? 3 : (s == 3 ? 1 : s);
-    unsigned short h = 0;
-    if (r < g.R && j < N) {
-      int x0, y0;
-      range_origin(g, r, x0, y0);
-      const float mean = (float)rmeta[r].sb / (float)N;
-      int ir, ic;
-      symmetry_source(sinv, j / n, j % n, n, ir, ic);  // i with perm_s(i) = j
-      h = __half_as_ushort(__float2half_rn((float)img[(long long)(y0 + ir) * g.W + x0 + ic] - mean));
-    }
-    ropnd[((long long)mt * kScanRows + row) * K + j] = h;
-  }
-}
-
-// 112-column |max| test of one epilogue thread's row against its threshold, appending the
-// columns above it (entries (rowid, d0 + column)).
-template <int W>
-__device__ __forceinline__ uint32_t mask_above(const uint32_t* v, float T) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int c = 0; c < W; ++c) m |= (uint32_t)(fabsf(__uint_as_float(v[c])) > T) << c;
-  return m;
-}
-
-// Cluster of 2 CTAs per pair (FIC_SCAN=pair); 10 warps per CTA:
-//   warp 0        lane 0: producer of this CTA's half (112 domains) of every pool tile
-//   warp 1        TMEM allocation (cta_group::2); lane 0: MMA issuer in the even CTA, relay of
-//                 the odd CTA's "tile landed" to the even CTA's barrier in the odd one
-//   warps 2-9     epilogue: lane quarter x column half (112 columns); the four warps of column
-//                 half 0 also write the segment's range rows into TMEM (A)
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP2Threads, 1)
-scan2_kernel(Geometry g, ScanLevel lv, const __half* __restrict__ upool, const unsigned short* __restrict__ ropnd,
-             const float* __restrict__ thr, SurvEntry* __restrict__ list_all,
-             unsigned long long* __restrict__ counts, unsigned long long cap) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  const Scan2Smem L = scan2_smem_layout(g.K);
-  const int K = g.K;
-  unsigned char* sP = smem + L.p_off;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bar_off);
-  uint64_t* empty_bar = full_bar + kScanMaxStages;
-  uint64_t* pfull_bar = empty_bar + kScanMaxStages;   // even CTA: the odd CTA's half has landed
-  uint64_t* tfull_bar = pfull_bar + kScanMaxStages;
-  uint64_t* tempty_bar = tfull_bar + kP2Bufs;
-  uint64_t* afull_bar = tempty_bar + kP2Bufs;
-  uint64_t* aempty_bar = afull_bar + 2;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(aempty_bar + 2);
-  unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 960);
-  SurvEntry* list = list_all + (unsigned long long)blockIdx.x * cap;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const int G = gridDim.x >> 1, pair = blockIdx.x >> 1;
-  const int nseg = seg_count(lv, pair, G);
-  const int stages = (int)L.stages;
-  const uint32_t a_cols = (uint32_t)K / 2;  // TMEM columns of one A buffer
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
-      ptx::mbar_init(&pfull_bar[s], 1);
-    }
-    for (int b = 0; b < kP2Bufs; ++b) {
-      ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], 2 * kP2Epi);  // every epilogue warp of both CTAs
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&afull_bar[b], 8);            // the 4 A-writer warps of both CTAs
-      ptx::mbar_init(&aempty_bar[b], 1);
-    }
-    ptx::fence_mbar_init();
-    *count = 0;
-  }
-  if (warp == 1) ptx::tmem_alloc_2sm<512>(tmem_base_smem);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  const uint32_t tb = *tmem_base_smem;
-
-  if (warp == 0) {
-    // ================= producer: this CTA's half of every tile =================
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ring_phase = 0;
-      for (int sg = 0; sg < nseg; ++sg) {
-        const Segment S = seg_at(lv, pair, G, sg);
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(upool) + (size_t)rank * L.p_bytes +
-                                   (long long)range_slice(g, S.m * kScanRanges) * g.Dt * K * 2;
-        const long long step_bytes = (long long)lv.stride * 2 * L.p_bytes;
-        for (int j = S.j0; j < S.j1; ++j) {
-          ptx::mbar_wait(&empty_bar[s], ring_phase ^ 1u);
-          ptx::mbar_arrive_expect_tx(&full_bar[s], L.p_bytes);
-          ptx::bulk_g2s(sP + s * L.p_bytes, src + (long long)j * step_bytes, L.p_bytes, &full_bar[s]);
-          if (++s == stages) {
-            s = 0;
-            ring_phase ^= 1u;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (rank == 0) {
-      // ================= MMA issuer (even CTA): whole-warp loop, elected lane issues =================
-      const uint32_t idesc = ptx::idesc_f16_f32(256, kP2Dom);
-      const bool do_mma = !(g.flags & 16);
-      const uint64_t b_desc0 = ptx::smem_desc(ptx::smem_addr(sP), 128, K * 16);
-      const uint32_t p_stage = L.p_bytes >> 4;
-      int s = 0, buf = 0;
-      uint32_t ring_phase = 0, buf_phase = 0;
-      for (int sg = 0; sg < nseg; ++sg) {
-        const Segment S = seg_at(lv, pair, G, sg);
-        ptx::mbar_wait_cluster(&afull_bar[sg & 1], (sg >> 1) & 1);
-        const uint32_t a_base = tb + kP2ACol + (uint32_t)(sg & 1) * a_cols;
-        for (int j = S.j0; j < S.j1; ++j) {
-          ptx::mbar_wait_cluster(&tempty_bar[buf], buf_phase ^ 1u);
-          ptx::mbar_wait(&full_bar[s], ring_phase);
-          ptx::mbar_wait_cluster(&pfull_bar[s], ring_phase);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            if (do_mma) {
-              const uint64_t bd0 = b_desc0 + (uint64_t)(s * p_stage);
-              const uint32_t d_tmem = tb + buf * kP2AccCols;
-              ptx::mma_f16_ts_2sm(d_tmem, a_base, bd0, idesc, 0u);
-              if (K == 64) {
-                ptx::mma_f16_ts_2sm(d_tmem, a_base + 8, bd0 + 16u, idesc, 1u);
-                ptx::mma_f16_ts_2sm(d_tmem, a_base + 16, bd0 + 32u, idesc, 1u);
-                ptx::mma_f16_ts_2sm(d_tmem, a_base + 24, bd0 + 48u, idesc, 1u);
-              }
-            }
-            ptx::tc_commit_2sm_mc(&empty_bar[s], 0x3);
-            ptx::tc_commit_2sm_mc(&tfull_bar[buf], 0x3);
-          }
-          __syncwarp();
-          if (++s == stages) {
-            s = 0;
-            ring_phase ^= 1u;
-          }
-          if (++buf == kP2Bufs) {
-            buf = 0;
-            buf_phase ^= 1u;
-          }
-        }
-        if (ptx::elect_one()) ptx::tc_commit_2sm_mc(&aempty_bar[sg & 1], 0x3);
-        __syncwarp();
-      }
-    } else if (lane == 0) {
-      // ================= relay (odd CTA): my half landed -> even CTA's pfull =================
-      const uint32_t remote = ptx::leader_addr(ptx::smem_addr(pfull_bar));
-      int s = 0;
-      uint32_t ring_phase = 0;
-      for (int sg = 0; sg < nseg; ++sg) {
-        const Segment S = seg_at(lv, pair, G, sg);
-        for (int j = S.j0; j < S.j1; ++j) {
-          ptx::mbar_wait(&full_bar[s], ring_phase);
-          ptx::mbar_arrive_cluster(remote + s * 8);
-          if (++s == stages) {
-            s = 0;
-            ring_phase ^= 1u;
-          }
-        }
-      }
-    }
-  } else {
-    // ================= epilogue =================
-    const int e = warp - 2;
-    const int half = e >> 2;
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;                 // TMEM lane = this CTA's (range, isometry) row
-    WarpAppender app{list, count, (uint32_t)cap, 0u, 0u};
-    const uint32_t tlane = tb + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t tempty_remote = ptx::leader_addr(ptx::smem_addr(tempty_bar));
-    const uint32_t afull_remote = ptx::leader_addr(ptx::smem_addr(afull_bar));
-    // A (range rows) of segment sg into TMEM buffer sg & 1 (column-half-0 warps)
-    auto write_a = [&](int sg) {
-      const Segment S = seg_at(lv, pair, G, sg);
-      if (sg >= 2) ptx::mbar_wait(&aempty_bar[sg & 1], ((sg >> 1) - 1) & 1);
-      const uint4* src = reinterpret_cast<const uint4*>(ropnd + ((long long)S.m * kScanRows + rank * 128 + row) * K);
-      const uint32_t ta = tlane + kP2ACol + (uint32_t)(sg & 1) * a_cols;
-      if (K == 64) {
-        uint32_t v[32];
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const uint4 q = __ldg(src + w);
-          v[4 * w] = q.x; v[4 * w + 1] = q.y; v[4 * w + 2] = q.z; v[4 * w + 3] = q.w;
-        }
-        ptx::tmem_st_32x32b_x32(ta, v);
-      } else {  // K == 16
-        uint32_t v[8];
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          const uint4 q = __ldg(src + w);
-          v[4 * w] = q.x; v[4 * w + 1] = q.y; v[4 * w + 2] = q.z; v[4 * w + 3] = q.w;
-        }
-        ptx::tmem_st_32x32b_x8(ta, v);
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(afull_remote + (sg & 1) * 8);
-    };
-    if (half == 0 && nseg > 0) write_a(0);
-    int i = 0;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const Segment S = seg_at(lv, pair, G, sg);
-      if (half == 0 && sg + 1 < nseg) write_a(sg + 1);
-      const int r = S.m * kScanRanges + (int)rank * 16 + (row >> 3);
-      const float T = r < g.R ? __ldg(thr + r) : 1e30f;  // shadow / padding: 1e30 (never), no bar: -1 (all)
-      const uint32_t rowid = (uint32_t)r * 8u + (uint32_t)(row & 7);
-      for (int j = S.j0; j < S.j1; ++j, ++i) {
-        const int buf = i % kP2Bufs;
-        ptx::mbar_wait(&tfull_bar[buf], (i / kP2Bufs) & 1);
-        ptx::tc_fence_after();
-        const uint32_t ta = tlane + buf * kP2AccCols + half * kP2Half;
-        uint32_t v[kP2Half];
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c + 32 <= kP2Half; c += 32) ptx::tmem_ld_32x32b_x32(ta + c, v + c);
-        if constexpr (kP2Half % 32 == 16) ptx::tmem_ld_32x32b_x16(ta + kP2Half - 16, v + kP2Half - 16);
-        ptx::tmem_ld_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(tempty_remote + buf * 8);
-        if (g.flags & 8) continue;
-        constexpr int Q = kP2Half / 4;  // four independent FMNMX3 chains
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
-#pragma unroll
-        for (int c = 0; c < Q; c += 2) {
-          m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
-          m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[Q + c])), fabsf(__uint_as_float(v[Q + 1 + c]))));
-          m2 = fmaxf(m2, fmaxf(fabsf(__uint_as_float(v[2 * Q + c])), fabsf(__uint_as_float(v[2 * Q + 1 + c]))));
-          m3 = fmaxf(m3, fmaxf(fabsf(__uint_as_float(v[3 * Q + c])), fabsf(__uint_as_float(v[3 * Q + 1 + c]))));
-        }
-        const bool hit = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > T;
-        if (__any_sync(0xffffffffu, hit)) {
-          const uint32_t d0 =
-              (uint32_t)(range_slice(g, r) * g.Dt) + (uint32_t)(j * lv.stride * kP2Dom + half * kP2Half);
-          constexpr int NQ = (kP2Half + 31) / 32;
-          uint32_t mk[NQ];
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) mk[q] = 0;
-          if (hit) {
-#pragma unroll
-            for (int q = 0; q < kP2Half / 32; ++q) mk[q] = mask_above<32>(v + 32 * q, T);
-            if constexpr (kP2Half % 32 == 16) mk[NQ - 1] = mask_above<16>(v + kP2Half - 16, T);
-          }
-#pragma unroll
-          for (int q = 0; q < NQ; ++q)
-            if (__any_sync(0xffffffffu, mk[q] != 0))
-              app.cols(mk[q], rowid, d0 + 32u * q);
-        }
-      }
-    }
-    app.close();
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::cluster_sync();
-  if (threadIdx.x == 0) counts[blockIdx.x] = *count;
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc_2sm<512>(tb);
-  }
-}
-
 // ------------------------------------------------------------------ host launchers
 bool scan_supported(const Geometry& g) { return g.N == 4 || g.N == 16 || g.N == 64; }
 
-// Single-CTA scan (default) or the CTA-pair scan (FIC_SCAN=pair).
-bool scan_pair_mode() {
-  const char* e = std::getenv("FIC_SCAN");
-  return e && std::strcmp(e, "pair") == 0;
-}
-
 int scan_tiles(const Geometry& g) {
-  const int t = scan_pair_mode() ? kP2Dom : kScanTileDom;
-  return (g.D + t - 1) / t;
+  return (g.D + kScanTileDom - 1) / kScanTileDom;
 }
 
 // Padded domain count of the pools (a multiple of the pool-builder block).
 long long scan_pool_domains(const Geometry& g) {
-  const long long q = 896;  // multiple of the pool-builder block (128) and the pair tile (224)
+  const long long q = kPoolBlock;
   return (g.D + q - 1) / q * q;
 }
 
@@ -1916,11 +1626,11 @@ void launch_seed_v3(const unsigned char* img, const Geometry& g, const unsigned 
   else seed_v3_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
 }
 
-// Scan CTAs (= list partitions) of a level: one per SM (an even number in pair mode).
+// Scan CTAs (= list partitions) of a level: one per SM.
 int scan_grid(const Geometry& g, int stride, int sms) {
   (void)g;
   (void)stride;
-  return scan_pair_mode() ? sms & ~1 : sms;
+  return sms;
 }
 
 static ScanLevel make_level(const Geometry& g, int stride, int G) {
@@ -1982,15 +1692,6 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
                         unsigned long long* counts, unsigned long long part, void* recs, unsigned long long* rcounts,
                         cudaStream_t st) {
   const int grid = scan_grid(g, stride, sms);
-  if (scan_pair_mode()) {
-    const ScanLevel lv = make_level(g, stride, grid / 2);
-    const Scan2Smem L2 = scan2_smem_layout(g.K);
-    cudaError_t e = cudaFuncSetAttribute(scan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L2.total);
-    if (e != cudaSuccess) return e;
-    scan2_kernel<<<grid, kP2Threads, L2.total, st>>>(g, lv, upool, reinterpret_cast<const unsigned short*>(ropnd),
-                                                     thr, list, counts, part);
-    return cudaGetLastError();
-  }
   const ScanLevel lv = make_level(g, stride, grid);
   const ScanSmem L = scan_smem_layout(g.K);
   int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
@@ -2022,7 +1723,7 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
 // (the wider bound adds survivors that cost more than the halved read: cfg2 0.375 vs 0.372 ms,
 // cfg5 13.51 vs 13.31 ms).  FIC_F16ACC=1 / 0 forces it on / off for the full level.
 bool scan_use_f16acc(const Geometry& g, int stride, int sms) {
-  if (stride != 1 || scan_pair_mode()) return false;
+  if (stride != 1) return false;
   const char* e = std::getenv("FIC_F16ACC");
   if (e) return e[0] == '1';
   const ScanLevel lv = make_level(g, 1, scan_grid(g, 1, sms));
@@ -2044,20 +1745,10 @@ size_t range_op_bytes(const Geometry& g) {
 // Thresholds of a level (thr, padded to whole m-tiles) and, when the scan needs new ones, the
 // range operands.
 void launch_level_ops(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta,
-                      const unsigned long long* gbest, float* thr, unsigned char* ropnd, bool operands,
+                      const unsigned long long* gbest, float* thr, unsigned char* ropnd,
                       unsigned long long* pend_count, unsigned* win, unsigned long long* selfcheck, cudaStream_t st) {
-  if (scan_pair_mode()) {  // unscaled plain rows (the pair scan compares with per-row thresholds)
-    cudaMemsetAsync(pend_count, 0, sizeof(unsigned long long), st);
-    if (win) cudaMemsetAsync(win, 0xFF, (size_t)g.R * sizeof(unsigned), st);
-    if (selfcheck) cudaMemsetAsync(selfcheck, 0, sizeof(unsigned long long), st);
-    launch_threshold(g, rmeta, gbest, thr, st);
-    if (operands)
-      range_op2_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, 4), 256, 0, st>>>(
-          img, g, rmeta, reinterpret_cast<unsigned short*>(ropnd));
-  } else {
-    range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(
-        img, g, rmeta, gbest, thr, ropnd, pend_count, win, selfcheck);
-  }
+  range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(
+      img, g, rmeta, gbest, thr, ropnd, pend_count, win, selfcheck);
 }
 
 // Pending-list segment per eval block: the most entries one block can take (eval_kernel's

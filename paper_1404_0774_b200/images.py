@@ -142,6 +142,12 @@ def volume(count=512, side=512, seed=1404005):
     return np.stack([ct_slice(side, seed + z, z / max(count, 1)) for z in range(count)])
 
 
+def volume_slices(first, count, total=512, side=512, seed=1404005):
+    """Slices [first, first + count) of volume(total, side, seed) (a rank's shard of cfg5)."""
+    z = range(first, min(total, first + count))
+    return np.stack([ct_slice(side, seed + k, k / max(total, 1)) for k in z])
+
+
 CONFIGS = {
     # name: (generator, n, step)
     "cfg1": (lambda: phantom(256, 1404001), 8, 8),

@@ -52,10 +52,8 @@ class env:
                 os.environ[k] = v
 
 
-# "tc": the single-CTA tcgen05 scan (default), "pair": the CTA-pair scan (cta_group::2),
-# "simt": the CUDA-core matcher (parity anchor, n >= 16 path)
-MATCHERS = {"tc": dict(FIC_MATCHER="tc", FIC_SCAN="1cta"), "pair": dict(FIC_MATCHER="tc", FIC_SCAN="pair"),
-            "simt": dict(FIC_MATCHER="simt", FIC_SCAN="1cta")}
+# "tc": the tcgen05 scan (default), "simt": the CUDA-core matcher (parity anchor, n >= 16 path)
+MATCHERS = {"tc": dict(FIC_MATCHER="tc"), "simt": dict(FIC_MATCHER="simt")}
 
 
 @pytest.fixture(params=list(MATCHERS))
@@ -159,15 +157,108 @@ def test_cfg2_ct_slice_full(oracle):
     assert enc.stats == st
 
 
-def test_cfg3_sampled_rows(oracle):
+def test_cfg2_full_vs_compiled_reference():
+    """cfg2 in full against the unmodified reference itself (oracle/_ref: its encode_parallel,
+    proj/src/encoder.cpp:368-427, over every host thread): records, residual bits, stats."""
+    from oracle import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    img = images.ct_slice(512, 1404002)
+    pv = dict(n=8, step=4)
+    want, st = Reference().encode(img, pv, workers=os.cpu_count() or 1)
+    enc = fic.encode(img, fic.CodecParams(**pv))
+    assert_same(enc.mappings, want, "cfg2 vs reference")
+    assert enc.stats == st
+
+
+def test_cfg3_full(oracle):
+    """cfg3 (512x512, 4x4 ranges, domain stride 2) in full: all 16,384 ranges."""
     img = images.ct_slice(512, 1404002)
     pv = dict(n=4, step=2)
     enc = fic.encode(img, fic.CodecParams(**pv))
-    rows = [0, 37, 64, 101, 127]
-    want, _ = oracle.encode_threaded(img, pv, rows=rows)
-    R = 512 // 4
-    got = np.concatenate([enc.mappings[r * R:(r + 1) * R] for r in rows])
-    assert_same(got, want, "cfg3 rows")
+    want, st = oracle.encode_threaded(img, pv)
+    assert_same(enc.mappings, want, "cfg3")
+    assert enc.stats == st
+
+
+def _oracle_rows_many(oracle, jobs, pv):
+    """Oracle records of (image, range row) jobs, spread over every host thread."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = pv["n"]
+
+    def one(job):
+        img, row = job
+        RX = img.shape[1] // n
+        xs = np.arange(RX, dtype=np.int32) * n
+        ys = np.full(RX, row * n, np.int32)
+        return oracle.encode_ranges(img, pv, xs, ys)[0]
+
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        return list(ex.map(one, jobs))
+
+
+def test_cfg5_as_benched(oracle):
+    """cfg5 exactly as bench.py runs it: one stacked 64-slice pass of the benched volume
+    (images.volume_slices, 512x512 CT slices, n=8, step 4) through fic_encode_batch_device.
+    Every slice is checked against the oracle on 4 seeded-random range rows (rows 0 and 63
+    included across the volume), and each slice's EncodeStats contribution against the
+    oracle's domain pool flat count and the ranges' variances."""
+    import torch
+    from paper_1404_0774_b200.abi import MAPPING_DTYPE
+    count, side, n = 64, 512, 8
+    pv = dict(n=n, step=4)
+    vol = images.volume_slices(0, count, 512)
+    per = (side // n) ** 2
+    d_img = torch.from_numpy(vol).cuda()
+    d_out = torch.zeros(count * per * MAPPING_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    st = fic.encode_batch_device(d_img.data_ptr(), count, side, side, d_out.data_ptr(), fic.CodecParams(**pv))
+    got = d_out.cpu().numpy().view(MAPPING_DTYPE).reshape(count, per)
+    rng = np.random.default_rng(1404005)
+    jobs, where = [], []
+    for z in range(count):
+        rows = rng.choice(64, 4, replace=False)
+        if z == 0:
+            rows[0] = 0
+        if z == count - 1:
+            rows[0] = 63
+        for r in rows:
+            jobs.append((vol[z], int(r)))
+            where.append((z, int(r)))
+    wants = _oracle_rows_many(oracle, jobs, pv)
+    for (z, r), want in zip(where, wants):
+        assert_same(got[z, r * 64:(r + 1) * 64], want, f"cfg5 slice {z} row {r}")
+    # stats: candidates_tested = 8 (R - shadow)(D - flat) per slice (encoder.hpp:49-53)
+    total = {"candidates_tested": 0, "shadow_ranges": 0, "shadow_codeblocks": 0}
+    for z in range(count):
+        _, _, _, flat = oracle.domain_pool(vol[z], pv)
+        b = vol[z].astype(np.int64).reshape(64, n, 64, n).transpose(0, 2, 1, 3).reshape(per, n * n)
+        shadow = int(np.sum(n * n * np.sum(b * b, 1) - np.sum(b, 1) ** 2 <= 0))
+        D, F = len(flat), int(flat.sum())
+        total["candidates_tested"] += 8 * (per - shadow) * (D - F)
+        total["shadow_ranges"] += shadow
+        total["shadow_codeblocks"] += 8 * (per - shadow) * F
+    assert st == total
+
+
+def test_cfg4_reference_rows():
+    """cfg4 (2048x2048, n=8, step 2) on 16 full range rows (first, last and 14 seeded random;
+    each includes the first and last columns) against the UNMODIFIED reference's records
+    (tests/golden/cfg4_rows.npz, generated by tests/golden/make_cfg4_rows.py: ~37 s of reference
+    search per row on 16 threads), with the default fp16 full level (scan mode 6), with it forced
+    off (mode 1) and with fp16 hit-first sparse levels (mode 7 instead of 2)."""
+    import hashlib
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg4_rows.npz")
+    fx = np.load(path)
+    img = images.xray(2048, 1404004)
+    assert hashlib.sha256(img.tobytes()).digest() == fx["image_sha256"].tobytes()
+    rows = [int(r) for r in fx["rows"]]
+    want = fx["maps"]
+    R = 2048 // 8
+    for sw in (dict(), dict(FIC_F16ACC="0"), dict(FIC_F16SEL="1")):
+        with env(**sw):
+            enc = fic.encode(img, fic.CodecParams(n=8, step=2))
+        got = np.concatenate([enc.mappings[r * R:(r + 1) * R] for r in rows])
+        assert_same(got, want, f"cfg4 rows {sw}")
 
 
 def test_parallel_api_and_rows(oracle):
@@ -196,7 +287,7 @@ def test_batch(oracle):
     assert st["candidates_tested"] == total
 
 
-@pytest.mark.parametrize("scan", ["tc", "pair"])
+@pytest.mark.parametrize("scan", ["tc"])
 @pytest.mark.parametrize("pv,chunk", [(dict(n=4, step=2), "64"), (dict(n=8, step=3), "2"), (dict(n=2, step=1), "3")])
 def test_batch_stacked(oracle, scan, pv, chunk):
     """Slices stacked into one encode pass (slice-offset pools, one scan over every slice's
@@ -245,14 +336,14 @@ def test_batch_device_cfg5_shape(oracle):
     assert_same(got[2 * per:2 * per + len(rows)], rows, "slice 2 oracle rows")
 
 
-@pytest.mark.parametrize("mode", ["exhaustive", "no_prepass", "tiny_list", "pair_tiny_list"])
+@pytest.mark.parametrize("mode", ["exhaustive", "no_prepass", "tiny_list"])
 def test_pruning_is_output_neutral(oracle, mode):
     """The scan's bound, the sparse levels and the survivor-list overflow path never change the
     result: exhaustive evaluation (every candidate through the exact path), a single full level,
     and a list so small that every level overflows and the full level is re-run all give the
     reference's records."""
     settings = {"exhaustive": dict(FIC_DEBUG=1), "no_prepass": dict(FIC_PREPASS=0),
-                "tiny_list": dict(FIC_LIST_CAP=4096), "pair_tiny_list": dict(FIC_LIST_CAP=4096, FIC_SCAN="pair")}
+                "tiny_list": dict(FIC_LIST_CAP=4096)}
     img = oracle.noise_image(64, 911)
     img[:16, :16] = 90  # some shadow ranges and flat domains
     for pv in (dict(n=4, step=1), dict(n=8, step=2), dict(n=2, step=3)):
@@ -261,22 +352,6 @@ def test_pruning_is_output_neutral(oracle, mode):
             enc = fic.encode(img, fic.CodecParams(**pv))
         assert_same(enc.mappings, want, f"{mode} {pv}")
         assert enc.stats == st
-
-
-def test_scan_modes_cfg4_sample(oracle):
-    """cfg4 (2048x2048, n=8, step 2): both tcgen05 scans agree with the reference on sampled rows,
-    the default one with and without the fp16 full level (scan modes 6 vs 1) and with fp16
-    hit-first sparse levels (mode 7 instead of 2)."""
-    img = images.xray(2048, 1404004)
-    pv = dict(n=8, step=2)
-    rows = [0, 101, 255]
-    want, _ = oracle.encode_threaded(img, pv, rows=rows)
-    R = 2048 // 8
-    for sw in (dict(FIC_SCAN="1cta"), dict(FIC_SCAN="pair"), dict(FIC_F16ACC="0"), dict(FIC_F16SEL="1")):
-        with env(**sw):
-            enc = fic.encode(img, fic.CodecParams(**pv))
-        got = np.concatenate([enc.mappings[r * R:(r + 1) * R] for r in rows])
-        assert_same(got, want, f"cfg4 rows {sw}")
 
 
 def test_graph_replay_new_contents(oracle):
@@ -321,8 +396,9 @@ def test_coarse_vote_output_neutral(oracle, coarse):
 
 @pytest.mark.parametrize("coarse", ["0", "1"])
 def test_f16_accumulator_output_neutral(oracle, coarse):
-    """The full level with an fp16 accumulator (scan modes 5/6, default for large pools) forced
-    on small images, with and without the whole-tile vote: identical codes and residual bits.
+    """The full level with an fp16 accumulator (scan modes 5/6, default for large pools and
+    K = 16) forced on small images of every range size (n = 2, 4, 8), with and without the
+    whole-tile vote: identical codes and residual bits.
     The binary 0/255 image drives the operand/partial-sum overflow guard (ranges with a tiny
     bar relative to their norm get no bar)."""
     rng = np.random.default_rng(1404)
@@ -330,7 +406,9 @@ def test_f16_accumulator_output_neutral(oracle, coarse):
     binary[:32, :32] = 128  # flat block: zero-variance ranges next to maximal-contrast ones
     cases = [(oracle.noise_image(64, 9), dict(n=4, step=2)), (oracle.smooth_image(64, 5), dict(n=8, step=2)),
              (images.ct_slice(256, 1404002, 0.3), dict(n=8, step=4)), (binary, dict(n=4, step=2)),
-             (binary, dict(n=8, step=2))]
+             (binary, dict(n=8, step=2)), (oracle.noise_image(64, 10), dict(n=2, step=1)),
+             (oracle.smooth_image(64, 6), dict(n=2, step=3)), (binary, dict(n=2, step=1)),
+             (images.ct_slice(128, 1404003, 0.5), dict(n=2, step=1))]
     for img, pv in cases:
         want, st = oracle.encode(img, pv)
         with env(FIC_F16ACC="1", FIC_COARSE=coarse):
