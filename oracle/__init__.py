@@ -289,18 +289,20 @@ class Reference:
         _check(self.L.ref_oracle_encode(ptr(img), w, h, ctypes.byref(p), ptr(out)), self._err)
         return out
 
-    def decode_step(self, cur, maps, width, params, scale=1):
+    def decode_step(self, cur, maps, width, params, scale=1, height=None):
         cur = np.ascontiguousarray(cur, np.float64)
         nxt = np.empty_like(cur)
         maps = np.ascontiguousarray(maps, MAPPING_DTYPE)
-        _check(self.L.ref_decode_step(ptr(cur), ptr(maps), width, width, ctypes.byref(_params(params)), scale,
+        height = width if height is None else height
+        _check(self.L.ref_decode_step(ptr(cur), ptr(maps), width, height, ctypes.byref(_params(params)), scale,
                                       ptr(nxt)), self._err)
         return nxt
 
-    def decode(self, maps, width, params, scale=1, iterations=16, initial="mid-gray", convergence_eps=None):
+    def decode(self, maps, width, params, scale=1, iterations=16, initial="mid-gray", convergence_eps=None,
+               height=None):
         maps = np.ascontiguousarray(maps, MAPPING_DTYPE)
-        kw = width * scale
-        out = np.empty((kw, kw), np.uint8)
+        height = width if height is None else height
+        out = np.empty((height * scale, width * scale), np.uint8)
         rm = np.zeros(max(iterations, 1), np.float64)
         runs = ctypes.c_int32(0)
         sup = None
@@ -309,7 +311,7 @@ class Reference:
         else:
             kind = 2
             sup = np.ascontiguousarray(initial, np.uint8)
-        _check(self.L.ref_decode(ptr(maps), width, width, ctypes.byref(_params(params)), scale, iterations, kind,
+        _check(self.L.ref_decode(ptr(maps), width, height, ctypes.byref(_params(params)), scale, iterations, kind,
                                  ptr(sup), int(convergence_eps is not None), float(convergence_eps or 0.0),
                                  ptr(out), ptr(rm), ctypes.byref(runs)), self._err)
         return out, rm[: runs.value].copy(), runs.value

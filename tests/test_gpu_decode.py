@@ -133,3 +133,65 @@ def test_decode_step_tiled_geometries(oracle, W, n, step, scale):
     wout, wrm, _ = oracle.decode(maps, W, pv, scale, 3)
     assert np.array_equal(out, wout)
     np.testing.assert_allclose(rm, wrm, rtol=1e-12, atol=1e-300)
+
+
+def _random_maps_wh(rng, w, h, n, count, s_bits=5, o_bits=7, step=1):
+    """Valid random mappings (every 2n-wide window inside the w x h image)."""
+    from paper_1404_0774_b200.abi import MAPPING_DTYPE
+    m = np.zeros(count, MAPPING_DTYPE)
+    m["x"] = rng.integers(0, (w - 2 * n) // step + 1, count) * step
+    m["y"] = rng.integers(0, (h - 2 * n) // step + 1, count) * step
+    m["sym"] = rng.integers(0, 8, count)
+    m["qs"] = rng.integers(0, 1 << s_bits, count)
+    m["qo"] = rng.integers(0, 1 << o_bits, count)
+    return m
+
+
+@pytest.mark.parametrize("scale", [1, 2, 3])
+def test_decode_off_grid_origins(oracle, scale):
+    """Mappings edited off the encoder's step grid (odd x / y with an even step): the
+    mean-raster decoder must not be used at odd magnifications (its 2x2 means sit on the
+    even grid); every raster value stays bit-exact with the reference decoder."""
+    img = oracle.smooth_image(64, 64)
+    pv = dict(n=4, step=2)
+    maps, _ = oracle.encode(img, pv)
+    maps = maps.copy()
+    rng = np.random.default_rng(77)
+    idx = rng.choice(len(maps), 40, replace=False)
+    maps["x"][idx] = np.minimum(maps["x"][idx] + 1, 64 - 8)
+    maps["y"][idx[::2]] = np.minimum(maps["y"][idx[::2]] + 1, 64 - 8)
+    assert np.any(maps["x"] % 2 == 1)
+    enc = fic.EncodedImage(64, 64, fic.CodecParams(**pv), maps)
+    out, rm, runs = fic.decode_traced(enc, scale=scale, iterations=6)
+    wout, wrm, wruns = oracle.decode(maps, 64, pv, scale, 6)
+    assert np.array_equal(out, wout)
+    np.testing.assert_allclose(rm, wrm, rtol=1e-12, atol=1e-300)
+    assert abs(fic.collage_error(img, enc) - oracle.collage_error(img, maps, pv)) <= 1e-12 * oracle.collage_error(
+        img, maps, pv)
+
+
+@pytest.mark.parametrize("w,h,n,scale", [(64, 32, 4, 1), (32, 64, 8, 2), (36, 20, 8, 1), (96, 64, 4, 3),
+                                         (256, 128, 8, 1)])
+def test_decode_non_square(w, h, n, scale):
+    """decode / decode_step on non-square geometries (a deserialised FIC1 header may be
+    non-square, format.cpp:145-185) and sides that are not multiples of n (pixels outside the
+    range grid stay 0, decoder.cpp:56) against the compiled reference decoder."""
+    import os
+    from oracle import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    ref = Reference()
+    rng = np.random.default_rng(w * 1000 + h)
+    count = (w // n) * (h // n)
+    maps = _random_maps_wh(rng, w, h, n, count)
+    pv = dict(n=n, s_max=0.8)
+    enc = fic.EncodedImage(w, h, fic.CodecParams(**pv), maps)
+    out, rm, runs = fic.decode_traced(enc, scale=scale, iterations=5)
+    wout, wrm, wruns = ref.decode(maps, w, pv, scale, 5, height=h)
+    assert out.shape == (h * scale, w * scale)
+    assert np.array_equal(out, wout)
+    np.testing.assert_allclose(rm, wrm, rtol=1e-12, atol=1e-300)
+    cur = rng.uniform(-10, 270, (h * scale, w * scale))
+    got = fic.decode_step(cur, enc, scale)
+    want = ref.decode_step(cur, maps, w, pv, scale, height=h)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

@@ -1,0 +1,32 @@
+"""The boundary, proven end to end: the reference's own pybind11 module
+(proj/python/bindings/module.cpp) rebuilt on libfic_b200.so by integration/Makefile
+(encoder.cpp / decoder.cpp swapped for integration/encoder_b200.cpp / decoder_b200.cpp,
+every signature unchanged), and the reference's Python smoke test
+(proj/tests/python/test_smoke.py) run UNMODIFIED against it, staged the way the reference's
+CMake stages it (proj/python/CMakeLists.txt:24-37).  All 10 tests must pass on the GPU."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "integration", "_build")
+
+
+def test_reference_python_smoke_unmodified():
+    smoke = os.path.join(BUILD, "tests", "test_smoke.py")
+    if not os.path.exists(smoke):
+        pytest.skip("integration/_build not staged (make -C integration needs /root/reference at build time)")
+    env = dict(os.environ, PYTHONPATH=os.path.join(BUILD, "python"))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", smoke], cwd=BUILD, env=env,
+                       capture_output=True, text=True, timeout=600)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "10 passed" in r.stdout, tail
+    # the module that ran is the rebuilt one, linked to this repository's CUDA library
+    probe = subprocess.run([sys.executable, "-c", "import fic, fic._core as c; print(c.__file__)"], cwd=BUILD,
+                           env=env, capture_output=True, text=True, timeout=120)
+    assert probe.stdout.strip().startswith(os.path.join(BUILD, "python", "fic")), probe.stdout + probe.stderr
