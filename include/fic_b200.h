@@ -141,6 +141,15 @@ int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height,
                           const fic_params* params, fic_mapping* d_out, fic_stats* stats,
                           void* stream);
 
+/* Device-resident range-row shard (the multi-GPU split of one image, cfg4): encodes range rows
+ * [row_begin, row_end) of the device image into `d_out` ((row_end-row_begin)*(width/n)
+ * records, device memory), enqueued on `stream`; every rank holds the whole image and builds
+ * the whole (replicated) domain pool.  Synchronises `stream` once (the survivor-list check);
+ * stats cover the encoded rows. */
+int32_t fic_encode_rows_device(const uint8_t* d_image, int32_t width, int32_t height,
+                               const fic_params* params, int32_t row_begin, int32_t row_end,
+                               fic_mapping* d_out, fic_stats* stats, void* stream);
+
 /* Device-resident batch (cfg5 volume): `d_images` holds `count` slices back to back,
  * `d_out` count * (side/n)^2 records, both device pointers.  Up to 64 slices are stacked
  * into one encode pass (one pool, one scan over every slice's ranges; each range only
@@ -209,6 +218,10 @@ int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset);
  * (16 B per output pixel and iteration: the next raster written, the current one read) and
  * the number of timed calls; timing is enabled with fic_set_matcher_timing. */
 int32_t fic_decode_timing(double* avg_ms, double* avg_bytes, uint64_t* calls, int32_t reset);
+/* Device time (ms) of the K1 pool builder (pool_v3_kernel) in timed encodes, its algorithmic
+ * bytes per launch (the image read once + the pool written once: per padded domain 2K bytes of
+ * fp16 operand, 8*N u16 exact cells and 16 bytes of moments) and the number of timed launches. */
+int32_t fic_pool_timing(double* avg_ms, double* avg_bytes, uint64_t* launches, int32_t reset);
 /* Survivors (candidates passing the tensor-core bound) per scan level of the calling
  * process's last tcgen05-path encode; returns the number of levels (0 for the CUDA-core path). */
 int32_t fic_last_survivors(uint64_t* counts, int32_t max_levels);

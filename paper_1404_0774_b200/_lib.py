@@ -34,6 +34,7 @@ def _declare(L):
     L.fic_encode_batch.argtypes = [vp, i32, i32, i32, vp, vp, vp]
     L.fic_encode_device.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.fic_encode_batch_device.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
+    L.fic_encode_rows_device.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp, vp]
     L.fic_decode_step.argtypes = [vp, i32, i32, vp, i32, i32, vp, i32, vp]
     L.fic_decode.argtypes = [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, i32, f64, vp, vp, vp]
     L.fic_collage_error.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp]
@@ -45,6 +46,7 @@ def _declare(L):
     L.fic_last_survivors.argtypes = [vp, i32]
     L.fic_debug_trace.argtypes = [vp, i32]
     L.fic_decode_timing.argtypes = [vp, vp, vp, i32]
+    L.fic_pool_timing.argtypes = [vp, vp, vp, i32]
     L.fic_is_shadow.argtypes = [vp, i32, f64, vp]
     L.fic_least_squares_fit.argtypes = [vp, i32, vp, i32, f64, vp]
     L.fic_least_squares_clamped.argtypes = [vp, i32, vp, i32, vp, vp]
@@ -58,7 +60,7 @@ def _declare(L):
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
                  "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace",
                  "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
-                 "fic_debug_pool"]:
+                 "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device"]:
         getattr(L, name).restype = i32
     return L
 
@@ -85,5 +87,5 @@ EXPORTS = [
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
     "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
     "fic_debug_trace", "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
-    "fic_debug_pool",
+    "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device",
 ]

@@ -383,6 +383,18 @@ def encode_device(d_image_ptr, width, height, d_out_ptr, params=None, stream=0, 
     return st.as_dict() if stats else None
 
 
+def encode_rows_device(d_image_ptr, width, height, row_begin, row_end, d_out_ptr, params=None, stream=0):
+    """(extension) device-resident range-row shard: rows [row_begin, row_end) of the range grid
+    of a device image into (row_end - row_begin) * (width/n) device records (the multi-GPU
+    split of one image).  Synchronises `stream`; returns the shard's stats."""
+    params = CodecParams() if params is None else params
+    st = FicStats()
+    _check(lib().fic_encode_rows_device(ctypes.c_void_p(d_image_ptr), int(width), int(height),
+                                        ctypes.byref(params.struct), int(row_begin), int(row_end),
+                                        ctypes.c_void_p(d_out_ptr), ctypes.byref(st), ctypes.c_void_p(stream)))
+    return st.as_dict()
+
+
 def encode_batch_device(d_images_ptr, count, width, height, d_out_ptr, params=None, stream=0):
     """(extension) device-resident volume encode: `count` uint8 slices back to back at
     `d_images_ptr`, count x (width/n)^2 records at `d_out_ptr`; up to 64 slices per encode
@@ -426,6 +438,15 @@ def decode_timing(reset=False):
     by = ctypes.c_double()
     n = ctypes.c_uint64()
     lib().fic_decode_timing(ctypes.byref(ms), ctypes.byref(by), ctypes.byref(n), int(reset))
+    return ms.value, by.value, n.value
+
+
+def pool_timing(reset=False):
+    """(extension) (average ms, average algorithmic bytes, timed launches) of the K1 pool builder."""
+    ms = ctypes.c_double()
+    by = ctypes.c_double()
+    n = ctypes.c_uint64()
+    lib().fic_pool_timing(ctypes.byref(ms), ctypes.byref(by), ctypes.byref(n), int(reset))
     return ms.value, by.value, n.value
 
 

@@ -105,6 +105,9 @@ unsigned long long g_scan_n = 0;
 double g_decode_ms = 0.0;          // decode iterations (decode_step + RMSE partials), device time
 unsigned long long g_decode_n = 0;
 double g_decode_bytes = 0.0;       // their algorithmic bytes
+double g_pool_ms = 0.0;            // K1 pool builder, device time
+unsigned long long g_pool_n = 0;
+double g_pool_bytes = 0.0;         // its algorithmic bytes (image read + pool written)
 std::mutex g_surv_mu;
 std::vector<unsigned long long> g_last_surv;  // survivors per level of the last encode (tcgen05 path)
 
@@ -227,8 +230,9 @@ struct Workspace {
   int device = -1;
   int sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr, ev5 = nullptr;
   bool scan_timed = false;
+  double pool_bytes = 0.0;  // > 0: ev4/ev5 bracket a pool build of this many algorithmic bytes
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
       diag, scratch, mra, mrb, recs, rcounts, pendc, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
@@ -264,6 +268,8 @@ Workspace& workspace() {
     CK(cudaEventCreate(&w->ev1));
     CK(cudaEventCreate(&w->ev2));
     CK(cudaEventCreate(&w->ev3));
+    CK(cudaEventCreate(&w->ev4));
+    CK(cudaEventCreate(&w->ev5));
     g_ws[dev] = w;
   }
   return *g_ws[dev];
@@ -429,7 +435,16 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   CK(cudaMemsetAsync(d_counters, 0, 2 * g.batch * sizeof(unsigned long long), st));
   // b.cnt: the scan kernels write their partitions' counters, range_op resets the pending and
   // self-check slots, the host reads only the partitions a level used
+  const bool time_pool = g_timing.load() != 0;
+  if (time_pool) CK(cudaEventRecord(ws.ev4, st));
   launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);  // flat domains per slice
+  if (time_pool) {
+    CK(cudaEventRecord(ws.ev5, st));
+    // algorithmic bytes: the image read once, the pool written once (fp16 operand 2K, exact
+    // cells 8 x N u16, meta 16 B per padded domain)
+    const double Dt = (double)g.Dt * g.batch;
+    ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0);
+  }
   launch_range_pass(d_img, g, b.rm, d_counters + g.batch, st);       // shadow ranges per slice
   launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
   launch_deq_tables(g, b.deq, st);
@@ -668,6 +683,13 @@ void collect_timing(Workspace& ws) {
     g_scan_n += 1;
   }
   ws.scan_timed = false;
+  if (ws.pool_bytes > 0 && cudaEventElapsedTime(&ms, ws.ev4, ws.ev5) == cudaSuccess) {
+    std::lock_guard<std::mutex> lock(g_timing_mu);
+    g_pool_ms += ms;
+    g_pool_n += 1;
+    g_pool_bytes += ws.pool_bytes;
+  }
+  ws.pool_bytes = 0.0;
 }
 
 // EncodeStats summed over the slices of a batch (flat[b] = h[b], shadow[b] = h[batch + b]).
@@ -934,6 +956,40 @@ int32_t fic_encode_device(const uint8_t* d_image, int32_t width, int32_t height,
   if (e) return e;
   if ((e = geometry_check(width, height, p))) return e;
   const Geometry g = make_geometry(width, height, p);
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
+    auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * sizeof(unsigned long long)));
+    run_encode(ws, d_image, g, d_out, d_cnt, h_cnt, st);
+    if (stats) fill_stats(stats, g, h_cnt[0], h_cnt[1]);
+    collect_timing(ws);
+    return FIC_OK;
+  });
+}
+
+// Range rows [row_begin, row_end) of a device-resident image into device records (the
+// multi-GPU shard of one image: every rank holds the whole image and builds the whole pool).
+int32_t fic_encode_rows_device(const uint8_t* d_image, int32_t width, int32_t height, const fic_params* params,
+                               int32_t row_begin, int32_t row_end, fic_mapping* d_out, fic_stats* stats,
+                               void* stream) {
+  fic_params p;
+  int32_t e = normalize(params, &p);
+  if (e) return e;
+  if ((e = geometry_check(width, height, p))) return e;
+  Geometry g = make_geometry(width, height, p);
+  const int rows = height / p.n;
+  if (row_begin < 0 || row_end > rows || row_begin > row_end)
+    return fail(FIC_ERR_BAD_PARAMS, "range rows [" + std::to_string(row_begin) + ", " + std::to_string(row_end) +
+                                        ") outside [0, " + std::to_string(rows) + ")");
+  if (!d_image || (!d_out && row_end > row_begin)) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
+  if (row_end == row_begin) {
+    if (stats) *stats = fic_stats{0, 0, 0};
+    return FIC_OK;
+  }
+  g.row_begin = row_begin;
+  g.R = (row_end - row_begin) * g.RX;
   return guarded([&]() -> int32_t {
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> lock(ws.mu);
@@ -1264,6 +1320,18 @@ int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
   if (reset) {
     g_scan_ms = 0.0;
     g_scan_n = 0;
+  }
+  return FIC_OK;
+}
+
+int32_t fic_pool_timing(double* avg_ms, double* avg_bytes, uint64_t* launches, int32_t reset) {
+  std::lock_guard<std::mutex> lock(g_timing_mu);
+  if (avg_ms) *avg_ms = g_pool_n ? g_pool_ms / (double)g_pool_n : 0.0;
+  if (avg_bytes) *avg_bytes = g_pool_n ? g_pool_bytes / (double)g_pool_n : 0.0;
+  if (launches) *launches = g_pool_n;
+  if (reset) {
+    g_pool_ms = g_pool_bytes = 0.0;
+    g_pool_n = 0;
   }
   return FIC_OK;
 }

@@ -103,3 +103,34 @@ def encode_volume_sharded(volume, params, group=None, device="cpu", encode_batch
         return None, stats
     return [codec.EncodedImage(vol.shape[2], vol.shape[1], params, full[i * per:(i + 1) * per].copy())
             for i in range(vol.shape[0])], stats
+
+
+def encode_sharded_device(d_image, width, height, params, group=None, stream=None):
+    """Range-sharded encode of one device-resident image (torch uint8 tensor, every rank holds
+    the whole image): rank r encodes its block of range rows into device records
+    (fic_encode_rows_device, a replicated pool per GPU) and the records are gathered to rank 0
+    over the process group (NCCL: NVLink on one box).  Rank 0 gets a (ranges x 32) uint8
+    device tensor of every record in range order; all ranks get the summed stats."""
+    import torch
+    import torch.distributed as dist
+
+    from . import codec
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    rows = height // params.n
+    rx = width // params.n
+    plan = plan_rows(rows, world)
+    b, e = plan[rank]
+    maxc = max(pe - pb for pb, pe in plan) * rx
+    shard = torch.zeros(maxc * 32, dtype=torch.uint8, device=d_image.device)
+    st_handle = stream if stream is not None else torch.cuda.current_stream(d_image.device).cuda_stream
+    st = codec.encode_rows_device(d_image.data_ptr(), width, height, b, e, shard.data_ptr(), params, st_handle)
+    if dist.get_backend(group) != "nccl":  # gloo (tests: several ranks on one GPU) gathers host tensors
+        shard = shard.cpu()
+    out = [torch.empty_like(shard) for _ in range(world)] if rank == 0 else None
+    dist.gather(shard, gather_list=out, dst=0, group=group)
+    stats = _sum_stats(st, group, shard.device)
+    if rank != 0:
+        return None, stats
+    full = torch.cat([out[r][: (pe - pb) * rx * 32] for r, (pb, pe) in enumerate(plan)])
+    return full, stats
