@@ -262,10 +262,18 @@ def run_ours(args):
     local = _env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         args.gpus = world
-    torch.cuda.set_device(local)
-    fic.set_device(local)
+    # one rank per GPU over NCCL; more ranks than GPUs (a 2-rank check on a 1-GPU box) share
+    # devices and exchange over gloo (NCCL refuses two ranks on one device)
+    ndev = max(torch.cuda.device_count(), 1)
+    dev = local % ndev
+    backend = "nccl" if world <= ndev else "gloo"
+    torch.cuda.set_device(dev)
+    fic.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
 
     cfg = args.config
     img, n, step = make_image(cfg, rank, world, args.slices)
@@ -282,7 +290,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     d_img = torch.from_numpy(img).cuda()
     d_out = torch.zeros(shard * 32, dtype=torch.uint8, device="cuda")
-    gathered = [torch.empty_like(d_out) for _ in range(world)] if world > 1 and rank == 0 else None
+    gather_dev = "cuda" if backend == "nccl" else "cpu"
+    gathered = ([torch.empty(shard * 32, dtype=torch.uint8, device=gather_dev) for _ in range(world)]
+                if world > 1 and rank == 0 else None)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def encode_step():
@@ -299,14 +309,14 @@ def run_ours(args):
     comps_rank = stats["candidates_tested"]  # this rank's own comparisons per step
     comps = comps_rank
     if world > 1:
-        t = torch.tensor([comps_rank], dtype=torch.int64, device="cuda")
+        t = torch.tensor([comps_rank], dtype=torch.int64, device=gather_dev)
         dist.all_reduce(t)
         comps = int(t.item())  # every rank's comparisons per step (whole job)
 
     def step_fn():
         encode_step()
         if world > 1:  # code records gathered to rank 0 over NCCL (NVLink)
-            dist.gather(d_out, gather_list=gathered, dst=0)
+            dist.gather(d_out if backend == "nccl" else d_out.cpu(), gather_list=gathered, dst=0)
 
     def barrier():
         if world > 1:
@@ -319,7 +329,7 @@ def run_ours(args):
     # ---- device-resident timed region (per-step events, L2 flushed between steps) ----
     launches0 = fic.kernel_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             barrier()
@@ -347,7 +357,7 @@ def run_ours(args):
     pool_ms, pool_bytes, pool_n = fic.pool_timing(reset=True)
     survivors = fic.last_survivors()
     fic.set_matcher_timing(False)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=gather_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -361,7 +371,7 @@ def run_ours(args):
         if volume:
             return fic.encode_batch(img, params)[0][-1]
         if rows_mode:  # range-sharded public path: fic_encode_rows per rank, records gathered to rank 0
-            return encode_sharded(img, params, device="cuda")
+            return encode_sharded(img, params, device=gather_dev)
         return fic.encode(img, params)
 
     for _ in range(2):
@@ -374,7 +384,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         enc = public_encode()
         e2e_times.append(time.perf_counter() - t0)
-    e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
+    e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=gather_dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = comps * e2e_steps / float(e2e_s.item())
@@ -418,10 +428,11 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": ("1 GPU" if world == 1 else
                                        f"{world} ranks x range rows {plan} of one image (replicated pool), "
-                                       "records gathered to rank 0 over NCCL" if rows_mode else
+                                       f"records gathered to rank 0 over {backend}" if rows_mode else
                                        f"{world} rank(s) x {count} slice(s) of a {args.slices}-slice volume, "
-                                       "records gathered to rank 0 over NCCL" if volume else
-                                       f"weak: {world} ranks x 1 image each, records gathered to rank 0 over NCCL")},
+                                       f"records gathered to rank 0 over {backend}" if volume else
+                                       f"weak: {world} ranks x 1 image each, records gathered to rank 0 over "
+                                       f"{backend}") + ("" if world <= ndev else f" ({world} ranks on {ndev} GPU(s))")},
             "encode_ms_per_image": ms_per_step / count if not rows_mode else ms_per_step,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": count * side * side,
                     "d2h_bytes_per_step": count * R * 32 + 16,

@@ -176,6 +176,27 @@ int32_t fic_least_squares_clamped(const double* a, int32_t side_a, const double*
 int32_t fic_least_squares(const double* a, int32_t side_a, const double* b, int32_t side_b,
                           const fic_params* params, fic_quantized_fit* out);
 
+/* ---- FIC1 container (proj/include/fic/format.hpp:50-70, proj/src/format.cpp:72-185) ----
+ * Record packing / unpacking run on the device (one thread per record). */
+/* record_layout (format.cpp:78-89): fields[0..6] = x bits, y bits, 3, s_bits, o_bits,
+ * positions per axis x, y; *record_bytes = ceil(sum of the widths / 8).  Host only. */
+int32_t fic_record_layout(int32_t width, int32_t height, const fic_params* params, int32_t* fields,
+                          int32_t* record_bytes);
+/* serialize (format.cpp:105-141) of the (width/n)*(height/n) host records: *size gets the byte
+ * count; the bytes are written when `out` holds `cap` >= *size bytes (else size query only).
+ * FIC_ERR_OUT_OF_RANGE names the first record off the step grid / outside the grid. */
+int32_t fic_serialize(const fic_mapping* maps, int32_t width, int32_t height, const fic_params* params,
+                      uint8_t* out, int64_t cap, int64_t* size);
+/* The same from device records into device memory on `stream` (e.g. rank 0's gathered codes,
+ * so only the packed bytes cross to the host); synchronises `stream` for the error check. */
+int32_t fic_serialize_device(const fic_mapping* d_maps, int32_t width, int32_t height,
+                             const fic_params* params, uint8_t* d_out, int64_t cap, int64_t* size,
+                             void* stream);
+/* deserialize (format.cpp:143-185): header fields to *width / *height / *params (normalised),
+ * the record count to *count; records (residual 0) to `out` when it holds cap >= count. */
+int32_t fic_deserialize(const uint8_t* data, int64_t size, int32_t* width, int32_t* height,
+                        fic_params* params, fic_mapping* out, int64_t cap, int64_t* count);
+
 /* ---- decoder (proj/include/fic/decoder.hpp:45-63) ---- */
 /* decode_step (proj/src/decoder.cpp:39-79) on fp64 rasters of (width*scale)^2 pixels. */
 int32_t fic_decode_step(const double* current, int32_t cur_width, int32_t cur_height,

@@ -35,6 +35,11 @@ def _declare(L):
     L.fic_encode_device.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.fic_encode_batch_device.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp]
     L.fic_encode_rows_device.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp, vp]
+    i64 = ctypes.c_int64
+    L.fic_record_layout.argtypes = [i32, i32, vp, vp, vp]
+    L.fic_serialize.argtypes = [vp, i32, i32, vp, vp, i64, vp]
+    L.fic_serialize_device.argtypes = [vp, i32, i32, vp, vp, i64, vp, vp]
+    L.fic_deserialize.argtypes = [vp, i64, vp, vp, vp, vp, i64, vp]
     L.fic_decode_step.argtypes = [vp, i32, i32, vp, i32, i32, vp, i32, vp]
     L.fic_decode.argtypes = [vp, i32, i32, vp, i32, i32, i32, vp, i32, i32, i32, f64, vp, vp, vp]
     L.fic_collage_error.argtypes = [vp, i32, i32, vp, i32, i32, vp, vp]
@@ -60,7 +65,8 @@ def _declare(L):
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
                  "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace",
                  "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
-                 "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device"]:
+                 "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device", "fic_record_layout",
+                 "fic_serialize", "fic_serialize_device", "fic_deserialize"]:
         getattr(L, name).restype = i32
     return L
 
@@ -87,5 +93,6 @@ EXPORTS = [
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
     "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
     "fic_debug_trace", "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
-    "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device",
+    "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device", "fic_record_layout", "fic_serialize",
+    "fic_serialize_device", "fic_deserialize",
 ]

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("FIC_LIB") or os.path.join(HERE, "libfic_b200.so")
-SOURCES = ["fic_api.cu", "pool.cu", "matcher_simt.cu", "scan.cu", "decoder.cu", "fit.cu"]
+SOURCES = ["fic_api.cu", "pool.cu", "matcher_simt.cu", "scan.cu", "decoder.cu", "fit.cu", "fic1.cu"]
 HEADERS = ["common.cuh", "tc_ptx.cuh", os.path.join("..", "..", "include", "fic_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

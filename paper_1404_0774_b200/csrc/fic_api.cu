@@ -797,6 +797,7 @@ int32_t check_mappings(const fic_mapping* maps, int w, int h, const fic_params& 
 
 namespace ficb {
 int32_t api_fail(int32_t code, const std::string& detail) { return fail(code, detail); }
+void note_launches(unsigned long long n) { g_launches += n; }
 }  // namespace ficb
 
 extern "C" {

@@ -1,12 +1,13 @@
-"""CPU: host-side pieces around the accelerated path — FIC1 container packing (SURVEY §8
-row F1, proj/src/format.cpp:105-185), PGM I/O, EncodedImage semantics, synthetic inputs."""
+"""CPU: host-side pieces around the accelerated path — the FIC1 record layout (SURVEY §8 row F1,
+proj/src/format.cpp:78-89; the packing itself runs on the device, tests/test_gpu_fic1.py), PGM I/O,
+EncodedImage semantics, synthetic inputs."""
 import numpy as np
 import pytest
 
 import paper_1404_0774_b200 as fic
 from paper_1404_0774_b200 import images
 from paper_1404_0774_b200.abi import MAPPING_DTYPE
-from paper_1404_0774_b200.fic1 import deserialize, record_layout, serialize
+from paper_1404_0774_b200.fic1 import record_layout
 
 
 def gradient_image(side):
@@ -27,57 +28,20 @@ def test_pgm_round_trip_and_errors():
     assert np.array_equal(fic.load_pgm(b"P2\n# c\n2 2\n255\n1 2\n3 4\n"), np.array([[1, 2], [3, 4]], np.uint8))
 
 
-def _random_encoding(rng, side=64):
-    n = int(rng.choice([2, 4, 8]))
-    step = int(rng.integers(1, 2 * n + 1))
-    p = fic.CodecParams(n=n, step=step, s_bits=int(rng.integers(1, 10)), o_bits=int(rng.integers(1, 12)),
-                        s_max=float(rng.uniform(0.1, 2.0)))
-    px, py, _, _ = record_layout(side, side, p)
-    count = (side // n) ** 2
-    m = np.zeros(count, MAPPING_DTYPE)
-    m["x"] = rng.integers(0, px, count) * step
-    m["y"] = rng.integers(0, py, count) * step
-    m["sym"] = rng.integers(0, 8, count)
-    m["qs"] = rng.integers(0, 1 << p.s_bits, count)
-    m["qo"] = rng.integers(0, 1 << p.o_bits, count)
-    return fic.EncodedImage(side, side, p, m)
-
-
-def test_fic1_round_trip_random():
-    rng = np.random.default_rng(7)
-    for _ in range(40):
-        enc = _random_encoding(rng)
-        blob = serialize(enc)
-        assert blob[:4] == b"FIC1"
-        back = deserialize(blob)
-        assert back == enc
-        assert serialize(back) == blob
-
-
 def test_fic1_record_width():
     # test_format.cpp:76-96: 27-bit records pad to 4 bytes (e.g. 256^2, n=4, step=4: 6+6+3+5+7)
     _, _, widths, nbytes = record_layout(256, 256, fic.CodecParams(n=4, step=4))
     assert sum(widths) == 27 and nbytes == 4
-
-
-def test_fic1_errors():
-    enc = _random_encoding(np.random.default_rng(1))
-    blob = serialize(enc)
-    with pytest.raises(fic.CodecError, match="TruncatedData"):
-        deserialize(blob[:10])
-    with pytest.raises(fic.CodecError, match="MalformedHeader"):
-        deserialize(b"XXXX" + blob[4:])
-    with pytest.raises(fic.CodecError, match="TruncatedData"):
-        deserialize(blob[:-1])
-    bad = fic.EncodedImage(enc.width, enc.height, enc.params, enc.mappings.copy())
-    bad.mappings["x"][0] += 1
-    if enc.params.step > 1:
-        with pytest.raises(fic.CodecError, match="OutOfRange"):
-            serialize(bad)
+    px, py, widths, nbytes = record_layout(512, 512, fic.CodecParams(n=8, step=4))
+    assert (px, py, widths, nbytes) == (125, 125, [7, 7, 3, 5, 7], 4)
+    with pytest.raises(fic.CodecError, match="NoValidPositions"):
+        record_layout(8, 8, fic.CodecParams(n=8))
 
 
 def test_encoded_image_equality_ignores_residual():
-    enc = _random_encoding(np.random.default_rng(3))
+    m = np.zeros(16, MAPPING_DTYPE)
+    m["qo"] = np.arange(16)
+    enc = fic.EncodedImage(16, 16, fic.CodecParams(), m)
     other = fic.EncodedImage(enc.width, enc.height, enc.params, enc.mappings.copy())
     other.mappings["residual"] += 1.0
     assert enc == other

@@ -7,8 +7,7 @@ import numpy as np
 import pytest
 
 from paper_1404_0774_b200 import images
-from paper_1404_0774_b200.fic1 import serialize
-from paper_1404_0774_b200.codec import EncodedImage, CodecParams
+
 
 KEYS = ["x", "y", "sym", "qs", "qo"]
 
@@ -112,9 +111,7 @@ def test_noise32_variants(oracle, golden, i, pv):
     same(m, golden[f"noise32_v{i}_maps"])
     assert s == st(golden[f"noise32_v{i}_stats"])
     b, _ = oracle.encode(img, pv, brute=True)  # pruning never changes the answer
-    same(b, m)
-    enc = EncodedImage(32, 32, CodecParams(**pv), m)  # host FIC1 packing == reference bytes
-    assert serialize(enc) == golden[f"noise32_v{i}_fic1"].tobytes()
+    same(b, m)  # (the device FIC1 packing of these records: tests/test_gpu_fic1.py)
 
 
 @pytest.mark.parametrize("seed", range(201, 206))
