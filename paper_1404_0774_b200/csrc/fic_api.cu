@@ -63,7 +63,9 @@ void launch_deq_tables(const Geometry&, double*, cudaStream_t);
 int scan_grid(const Geometry&, int, int);
 cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const __half*, const RangeMeta*,
                         const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long, void*,
-                        unsigned long long*, cudaStream_t);
+                        unsigned long long*, const unsigned short*, const DomainMetaI*, unsigned long long*, void*,
+                        const double*, bool, cudaStream_t);
+bool scan_fused();
 size_t scan_rec_bytes(unsigned long long, int);
 int scan_trace_copy(long long*, int);
 int scan_padded_ranges(const Geometry&);
@@ -71,14 +73,15 @@ void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long lon
 bool scan_use_f16acc(const Geometry&, int stride, int sms);
 size_t range_op_bytes(const Geometry&);
 void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, const unsigned long long*, float*,
-                      unsigned char*, unsigned long long*, unsigned*, unsigned long long*, cudaStream_t);
+                      unsigned char*, unsigned long long*, bool, unsigned long long*, cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
-                 const double*, uint2*, unsigned*, int, cudaStream_t);
+                 const double*, uint2*, unsigned*, void*, bool, int, cudaStream_t);
+bool eval_inline();
 void launch_winner(const uint2*, const unsigned long long*, int, unsigned long long, const double*,
-                   const unsigned long long*, unsigned*, int, cudaStream_t);
+                   const unsigned long long*, void*, int, cudaStream_t);
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
-                   const RangeMeta*, const unsigned*, const unsigned long long*, fic_mapping*, unsigned long long*,
+                   const RangeMeta*, const void*, const unsigned long long*, fic_mapping*, unsigned long long*,
                    cudaStream_t);
 void launch_probe_corr(const unsigned char*, const Geometry&, const unsigned short*, int, const int*, const int*,
                        const int*, long long*, cudaStream_t);
@@ -353,7 +356,7 @@ struct ScanBufs {
   DomainMetaI* mi;
   RangeMeta* rm;
   unsigned long long* gbest;
-  unsigned* win;
+  void* win;  // per range: 128-bit (residual bits, domain * 8 + isometry) minimum
   unsigned long long* cnt;
   unsigned char* ropnd;
   float* thr;
@@ -368,7 +371,7 @@ ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
   b.mi = static_cast<DomainMetaI*>(ws.meta_i.get((size_t)Dt * sizeof(DomainMetaI)));
   b.rm = static_cast<RangeMeta*>(ws.rmeta.get((size_t)g.R * sizeof(RangeMeta)));
   b.gbest = static_cast<unsigned long long*>(ws.gbest.get((size_t)g.R * sizeof(unsigned long long)));
-  b.win = static_cast<unsigned*>(ws.win.get((size_t)g.R * sizeof(unsigned)));
+  b.win = ws.win.get((size_t)g.R * 16);
   b.ropnd = static_cast<unsigned char*>(ws.ropnd.get(range_op_bytes(g)));
   b.thr = static_cast<float*>(ws.thr.get((size_t)scan_padded_ranges(g) * sizeof(float)));
   b.deq = static_cast<double*>(ws.deq.get(deq_table_entries(g) * sizeof(double)));
@@ -393,20 +396,27 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   // the full level of a large pool accumulates in fp16 (flags & 256: its thresholds and its scan)
   Geometry gl = g;
   gl.flags = scan_use_f16acc(g, stride, ws.sms) ? (g.flags | 256) : (g.flags & ~256);
-  launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, b.cnt + kPendSlot, final_level ? b.win : nullptr, final_level ? b.cnt + kSelfcheckSlot : nullptr,
-                   st);
+  launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, b.cnt + kPendSlot, final_level,
+                   final_level ? b.cnt + kSelfcheckSlot : nullptr, st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   void* recs = ws.recs.get(scan_rec_bytes(ws.list_cap, parts));
   auto* rcnt = static_cast<unsigned long long*>(ws.rcounts.get(kPartSlots * sizeof(unsigned long long)));
-  CK(launch_scan(d_img, gl, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, recs, rcnt, st));
+  const bool fused = scan_fused();
+  CK(launch_scan(d_img, gl, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, recs, rcnt, b.qpool,
+                 b.mi, b.gbest, b.win, b.deq, fused, st));
   if (time_scan) {
     CK(cudaEventRecord(ws.ev3, st));
     ws.scan_timed = true;
   }
+  if (fused) {  // the scan evaluated its survivors itself
+    g_launches += 2;  // level ops, scan
+    return;
+  }
+  const bool inl = eval_inline();
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
-              pendc, ws.sms, st);
-  g_launches += 5;  // level ops, scan, expand, evaluation, residuals
+              pendc, b.win, inl, ws.sms, st);
+  g_launches += inl ? 4 : 5;  // level ops, scan, expand, evaluation (+ residuals)
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a
@@ -418,10 +428,13 @@ void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   const bool timed = g_timing.load() != 0;
   if (timed) CK(cudaEventRecord(ws.ev1, st));
   const int parts = scan_grid(g, 1, ws.sms);
-  launch_winner(static_cast<uint2*>(ws.list.p), cnt, parts, ws.list_cap / (unsigned long long)parts,
-                static_cast<double*>(ws.res.p), b.gbest, b.win, ws.sms, st);
+  if (!scan_fused() && !eval_inline()) {
+    launch_winner(static_cast<uint2*>(ws.list.p), cnt, parts, ws.list_cap / (unsigned long long)parts,
+                  static_cast<double*>(ws.res.p), b.gbest, b.win, ws.sms, st);
+    g_launches += 1;
+  }
   launch_record(d_img, g, b.qpool, b.mi, b.rm, b.win, b.gbest, d_out, b.cnt + kSelfcheckSlot, st);
-  g_launches += 2;
+  g_launches += 1;
   CK(cudaGetLastError());
 }
 
@@ -447,11 +460,12 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   }
   launch_range_pass(d_img, g, b.rm, d_counters + g.batch, st);       // shadow ranges per slice
   launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
+  launch_fill_u64(static_cast<unsigned long long*>(b.win), 2ll * g.R, ~0ull, st);  // no winner yet
   launch_deq_tables(g, b.deq, st);
   const char* seed_env = std::getenv("FIC_SEED");  // "0": no local seed (A/B)
   const bool seed = !(seed_env && std::strcmp(seed_env, "0") == 0);
   if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
-  g_launches += seed ? 5 : 4;
+  g_launches += seed ? 6 : 5;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
   const std::vector<int> lv = scan_levels(g);
   for (size_t l = 0; l + 1 < lv.size(); ++l) enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st);
@@ -523,8 +537,8 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
                         ws.recs.p, ws.rcounts.p, ws.pendc.p};
   for (const void* q : ptrs) k.push_back((unsigned long long)(uintptr_t)q);
   k.push_back(ws.list_cap);
-  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SCAN", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED", "FIC_LANEBEST_MAX",
-                           "FIC_F16ACC", "FIC_F16SEL"}) {
+  for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED",
+                           "FIC_LANEBEST_MAX", "FIC_F16ACC", "FIC_F16SEL", "FIC_FUSED", "FIC_EVAL_SPLIT"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;

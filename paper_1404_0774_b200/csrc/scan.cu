@@ -48,8 +48,13 @@ constexpr int kEpiParts = kScanEpiWarps / 4;
 constexpr int kEpiRanges = kScanRanges / kEpiParts;    // ranges per epilogue thread
 constexpr int kEpiCols = kEpiRanges * kSyms;           // TMEM columns per epilogue thread
 constexpr int kScanThreads = (2 + kScanEpiWarps) * 32;
+// fused scan (scan + exact evaluation in one kernel): kEvalWarps consumer warps evaluate the
+// epilogue's survivors while the tensor core runs; every other warp joins them once its own
+// role is done
+constexpr int kEvalWarps = 2;
+constexpr int kFusedThreads = (2 + kScanEpiWarps + kEvalWarps) * 32;
 constexpr uint32_t kScanTmemCols = 512;
-constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemBudget = 226 * 1024;
 
 // Survivor list entry: (encoded range r * 8 + isometry, canonical domain).
 typedef uint2 SurvEntry;
@@ -422,7 +427,17 @@ __device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* q
       *pending = true;
       return inf;
     }
-    return residual_reload<NN>(g, qpool, img, d, s, x0, y0, s_deq, o_deq);
+    // the exact residual (encoder.cpp:274-280, pixel order, each operation rounded) from the
+    // operands already in registers
+    double r_val = 0.0;
+#pragma unroll
+    for (int i = 0; i < NN; ++i) {
+      const double ai = __dmul_rn((double)q_at(qw, i), 0.25);
+      const double bi = (double)((bpk[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+      const double dd = __dsub_rn(__dadd_rn(__dmul_rn(s_deq, ai), o_deq), bi);
+      r_val = __dadd_rn(r_val, __dmul_rn(dd, dd));
+    }
+    return r_val;
   }
 exact:
   return eval_exact_reload<NN>(g, qpool, img, d, s, x0, y0, sb, ssb, sqv, denv, upper_only ? inf : thr,
@@ -549,20 +564,41 @@ struct ScanSmem {
   uint32_t r_bytes, p_bytes, stages, r_off, p_off, bar_off, wbuf_off, total;
 };
 
+// ------------------------------------------------------------------ fused evaluation
+// The epilogue warps publish finished chunks of survivors (16 mask records at the full level,
+// 32 direct entries at sparse levels) into a CTA-local bounded queue (Vyukov: seq[i] == t: slot
+// free for ticket t, == t + 1: filled by ticket t); consumer warps take chunks in ticket order,
+// expand records into a per-warp buffer of entries and evaluate 32 at a time with the exact
+// arithmetic of eval_fast (encoder.cpp:236-287), lowering the range's bar and keeping the
+// lexicographic (residual, domain * 8 + isometry) minimum of every evaluated candidate in a
+// 128-bit key per range — so no survivor list round trip, expand / eval / residual / winner pass.
+constexpr uint32_t kRing = 512;
+constexpr int kEvalBuf = 64;
+constexpr uint32_t kChunkEntries = 0x80000000u;  // chunk id flag: an entry chunk (sparse levels)
+constexpr uint32_t kRingEmpty = 0xFFFFFFFFu;
+
+struct EvalRing {
+  uint32_t seq[kRing];
+  uint32_t ids[kRing];
+  unsigned head, tail, done, entries;
+};
+constexpr uint32_t kEvalConsumers = kScanEpiWarps + 2 + kEvalWarps;  // every warp consumes eventually
+constexpr uint32_t kEvalSmem = (uint32_t)sizeof(EvalRing) + kEvalConsumers * kEvalBuf * 8;
+
 // Shared memory: two range operands (256 rows x K fp16 each), a ring of pool tiles
-// (128 domains x K fp16), barriers, per-warp survivor staging.
-__host__ __device__ inline ScanSmem scan_smem_layout(int K) {
+// (128 domains x K fp16), barriers, (fused) the evaluation queue and per-warp entry buffers.
+__host__ __device__ inline ScanSmem scan_smem_layout(int K, bool fused = false) {
   ScanSmem L;
   L.r_bytes = kScanRows * K * 2;
   L.p_bytes = kScanTileDom * K * 2;
   L.r_off = 0;
   L.p_off = 2 * L.r_bytes;
-  const uint32_t fixed = L.p_off + 512;
+  const uint32_t fixed = L.p_off + 512 + (fused ? kEvalSmem : 0u);
   uint32_t st = (kSmemBudget - fixed) / L.p_bytes;
   L.stages = st > kScanMaxStages ? kScanMaxStages : st;
   L.bar_off = L.p_off + L.stages * L.p_bytes;
   L.wbuf_off = L.bar_off + 512;
-  L.total = L.wbuf_off;
+  L.total = L.wbuf_off + (fused ? kEvalSmem : 0u);
   return L;
 }
 
@@ -684,22 +720,19 @@ __global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta
 // r_bytes each) so the scan loads them with one bulk copy per segment.
 // The level's per-range thresholds are computed here too (each CTA for its m-tile's 32
 // ranges, the blockIdx.y == 0 CTA writes them out for the scan epilogue), one launch per level.
-// It also resets the level's pending-residual counter and, for the full level (win != null),
-// the winner slots and the record self-check counter (instead of separate memsets).
+// It also resets the level's pending-residual counter and, for the full level, the record
+// self-check counter (instead of separate memsets).
 __global__ void __launch_bounds__(256)
 range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr,
-                unsigned char* __restrict__ ropnd, unsigned long long* __restrict__ pend_count,
-                unsigned* __restrict__ win, unsigned long long* __restrict__ selfcheck) {
+                unsigned char* __restrict__ ropnd, unsigned long long* __restrict__ pend_count, int full_level,
+                unsigned long long* __restrict__ selfcheck) {
   __shared__ float s_thr[kScanRanges];
   if (threadIdx.x < kScanRanges) {
     const int r = blockIdx.x * kScanRanges + threadIdx.x;
-    const float t = range_threshold(g, rmeta, gbest, r, win != nullptr && scan_f16acc(g));  // full level
+    const float t = range_threshold(g, rmeta, gbest, r, full_level && scan_f16acc(g));
     s_thr[threadIdx.x] = t;
-    if (blockIdx.y == 0) {
-      thr[r] = t;
-      if (win && r < g.R) win[r] = 0xFFFFFFFFu;
-    }
+    if (blockIdx.y == 0) thr[r] = t;
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     *pend_count = 0;
@@ -785,6 +818,26 @@ struct WarpAppender {
   }
 };
 
+// ---- fused evaluation: producer side ----
+// One lane publishes chunk `id` (the warp's writes to it fenced first by the caller).
+__device__ __forceinline__ void ring_publish(EvalRing* rg, uint32_t id) {
+  const unsigned t = atomicAdd(&rg->tail, 1u);
+  volatile uint32_t* seq = rg->seq;
+  while (seq[t % kRing] != t) __nanosleep(64);  // full: wait for the consumer of ticket t - kRing
+  reinterpret_cast<volatile uint32_t*>(rg->ids)[t % kRing] = id;
+  __threadfence_block();
+  seq[t % kRing] = t + 1;
+}
+
+// Warp-uniform: publish the warp's finished chunk `cur` (no-op when none / not fused).
+__device__ __forceinline__ void publish_chunk(EvalRing* rg, uint32_t cur) {
+  if (!rg || cur == kSentinel) return;
+  __threadfence_block();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) ring_publish(rg, cur);
+  __syncwarp();
+}
+
 // Mask records: the scan epilogue writes one record per (warp, tile, range) with a hit: the
 // range's encoded index r * 8, the pool index of the warp's first domain and, per lane (one
 // domain each), the 8-bit mask of its isometry columns above the threshold.  One 8-byte
@@ -803,14 +856,18 @@ struct WarpRecAppender {
   uint32_t cap;      // partition size (records)
   uint32_t base;
   uint32_t left;
+  uint32_t cur;      // first record of the warp's current chunk (kSentinel: none)
+  EvalRing* ring;    // fused scan: finished chunks are published to the consumers
 
   // Warp-uniform: every lane passes its mask (0 for none).
   __device__ __forceinline__ void put(uint32_t bits, uint32_t r8, uint32_t d0) {
     const uint32_t lane = threadIdx.x & 31;
     if (left == 0) {
+      if (cur < cap) publish_chunk(ring, cur);
       uint32_t nb = 0;
       if (lane == 0) nb = atomicAdd(count, kRecChunk);
       base = __shfl_sync(0xffffffffu, nb, 0);
+      cur = base;
       left = kRecChunk;
     }
     if (base < cap) {
@@ -826,8 +883,171 @@ struct WarpRecAppender {
     for (uint32_t k = lane; k < left; k += 32)
       if (base + k < cap) recs[base + k].r8 = kSentinel;
     left = 0;
+    if (cur < cap) publish_chunk(ring, cur);
+    cur = kSentinel;
   }
 };
+
+// Lexicographic minimum of (residual, domain * 8 + isometry) per range: one 128-bit CAS loop on
+// (IEEE bits of the residual, candidate index) — non-negative doubles order like their bits.
+__device__ __forceinline__ void win_min(unsigned __int128* w, double R, uint32_t idx) {
+  const unsigned __int128 key = ((unsigned __int128)(unsigned long long)__double_as_longlong(R) << 64) | idx;
+  const volatile unsigned long long* h = reinterpret_cast<const volatile unsigned long long*>(w);
+  unsigned __int128 old = ((unsigned __int128)h[1] << 64) | h[0];
+  while (key < old) {
+    const unsigned __int128 prev = atomicCAS(w, old, key);
+    if (prev == old) break;
+    old = prev;
+  }
+}
+
+// Sparse levels: a warp's 32-slot chunks of direct entries in its CTA's list partition.
+struct EntryChunks {
+  SurvEntry* list;
+  unsigned* count;
+  uint32_t cap, base, left, cur;
+  EvalRing* ring;
+  // Room for `need` more entries: pads and publishes the current chunk if it is too short.
+  __device__ __forceinline__ void reserve(uint32_t need) {
+    if (left >= need) return;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t q = lane; q < left; q += 32)
+      if (base + q < cap) list[base + q] = make_uint2(kSentinel, kSentinel);
+    if (cur < cap) publish_chunk(ring, kChunkEntries | cur);
+    uint32_t nb = 0;
+    if (lane == 0) nb = atomicAdd(count, 32u);
+    base = __shfl_sync(0xffffffffu, nb, 0);
+    cur = base;
+    left = 32;
+  }
+  __device__ __forceinline__ void close() {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t q = lane; q < left; q += 32)
+      if (base + q < cap) list[base + q] = make_uint2(kSentinel, kSentinel);
+    left = 0;
+    if (cur < cap) publish_chunk(ring, kChunkEntries | cur);
+    cur = kSentinel;
+  }
+};
+
+// ---- fused evaluation: consumer side ----
+struct EvalCtx {
+  const unsigned char* img;
+  const unsigned short* qpool;
+  const DomainMetaI* meta_i;
+  const RangeMeta* rmeta;
+  unsigned long long* gbest;
+  unsigned __int128* win;
+  DeqTables tab;
+};
+
+// One lane's survivor, evaluated exactly (eval_kernel's body with the residual inline).
+template <int NN>
+__device__ __forceinline__ void eval_entry(const Geometry& g, const EvalCtx& c, uint2 en) {
+  if (en.x == kSentinel) return;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const int r = (int)(en.x >> 3), s = (int)(en.x & 7), d = (int)(en.y & 0x7FFFFFFFu);
+  const DomainMetaI mi = c.meta_i[d];
+  const RangeMeta rm = c.rmeta[r];
+  const double bar = load_bar(c.gbest, r);
+  int x0, y0;
+  range_origin(g, r, x0, y0);
+  uint32_t qw[NN / 2], bpk[NN / 4];
+  load_q8_row<NN>(c.qpool, d, s, qw);
+  load_range_words<NN>(c.img, g, x0, y0, bpk);
+  if (mi.den < 0) return;  // flat code blocks are never candidates (encoder.cpp:223-229)
+  unsigned qs = 0, qo = 0;
+  const double R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar,
+                                 !(g.flags & 2), false, c.tab, c.qpool, c.img, d, s, x0, y0, qs, qo);
+  if (R < inf) {
+    publish_best(c.gbest, r, R);
+    win_min(c.win + r, R, (uint32_t)d * 8u + (uint32_t)s);
+  }
+}
+
+// Consumer loop of one warp: takes published chunks until every producer is done and the
+// queue is empty.  `buf`: this warp's kEvalBuf-entry staging buffer (shared memory).
+template <int NN>
+__device__ void consume(const Geometry& g, const EvalCtx& c, EvalRing* rg, uint2* buf, const MaskRec* recs,
+                        uint32_t rcap, const SurvEntry* elist, uint32_t ecap, unsigned producers) {
+  const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+  uint32_t nb = 0;        // warp-uniform: entries staged in buf
+  unsigned taken = 0;     // entries this warp evaluated
+  auto drain = [&]() {    // evaluate buf[0..31], keep the rest
+    eval_entry<NN>(g, c, buf[lane]);
+    __syncwarp();
+    uint2 mv = make_uint2(0, 0);
+    if (lane + 32 < nb) mv = buf[32 + lane];
+    __syncwarp();
+    if (lane + 32 < nb) buf[lane] = mv;
+    __syncwarp();
+    nb -= 32;
+  };
+  auto append = [&](bool has, uint2 e) {  // warp-uniform call; nb < 32 on entry
+    const uint32_t bal = __ballot_sync(0xffffffffu, has);
+    if (has) buf[nb + __popc(bal & lt)] = e;
+    nb += __popc(bal);
+    taken += __popc(bal);
+    __syncwarp();
+    if (nb >= 32) drain();
+  };
+  volatile uint32_t* seq = rg->seq;
+  volatile unsigned* vdone = &rg->done;
+  volatile unsigned* vtail = &rg->tail;
+  while (true) {
+    uint32_t id = kRingEmpty;
+    if (lane == 0) {
+      const unsigned t = atomicAdd(&rg->head, 1u);
+      while (true) {
+        if (seq[t % kRing] == t + 1) {
+          id = reinterpret_cast<volatile uint32_t*>(rg->ids)[t % kRing];
+          __threadfence_block();
+          seq[t % kRing] = t + kRing;  // free for ticket t + kRing
+          break;
+        }
+        if (*vdone == producers && t >= *vtail) break;  // every chunk published and taken
+        __nanosleep(128);
+      }
+    }
+    id = __shfl_sync(0xffffffffu, id, 0);
+    if (id == kRingEmpty) break;
+    __syncwarp();
+    __threadfence_block();
+    if (id & kChunkEntries) {
+      const uint32_t pos = (id & ~kChunkEntries) + lane;
+      uint2 e = make_uint2(kSentinel, kSentinel);
+      if (pos < ecap) e = __ldcg(elist + pos);
+      append(e.x != kSentinel, e);
+    } else {
+      // the chunk's 16 headers (lanes 0-15) and every record's mask byte of this lane, all
+      // loaded up front (one L2 round trip), then the records in order from registers
+      uint2 hq = make_uint2(kSentinel, 0);
+      if (lane < kRecChunk && id + lane < rcap) hq = __ldcg(reinterpret_cast<const uint2*>(recs + id + lane));
+      uint32_t mk[kRecChunk];
+#pragma unroll
+      for (uint32_t q = 0; q < kRecChunk; ++q) mk[q] = id + q < rcap ? (uint32_t)__ldcg(recs[id + q].m + lane) : 0u;
+#pragma unroll 1
+      for (uint32_t q = 0; q < kRecChunk; ++q) {
+        uint2 h;
+        h.x = __shfl_sync(0xffffffffu, hq.x, q);
+        h.y = __shfl_sync(0xffffffffu, hq.y, q);
+        if (h.x == kSentinel) continue;
+        uint32_t m = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < kRecChunk; ++k)
+          if (k == q) m = mk[k];
+        while (__any_sync(0xffffffffu, m != 0)) {
+          const bool has = m != 0;
+          const uint32_t b = has ? (uint32_t)(__ffs(m) - 1) : 0u;
+          m &= m - 1;
+          append(has, make_uint2(h.x + b, h.y + lane));
+        }
+      }
+    }
+  }
+  if (nb > 0) eval_entry<NN>(g, c, lane < nb ? buf[lane] : make_uint2(kSentinel, kSentinel));
+  if (lane == 0) atomicAdd(&rg->entries, taken);
+}
 
 __device__ __forceinline__ float absmax8(const uint32_t* v) {
   const float* f = reinterpret_cast<const float*>(v);
@@ -853,18 +1073,21 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 // keeping each lane's best per range over the whole segment (lv.select == 3: short levels of
 // small pools, one segment per m-tile); 5, 6 and 7: modes 0, 1 and 2 with an fp16
 // accumulator (full level: scan_f16acc; sparse level: scan_f16sel).  One instantiation per mode keeps each epilogue's registers to its own path.
-template <int MODE>
-__global__ void __launch_bounds__(kScanThreads, 1)
+// EV: 0 = survivors to the global list (expand / eval / residual / winner kernels follow);
+// NN (4, 16, 64) = fused: kEvalWarps consumer warps evaluate them in this kernel (EvalCtx).
+template <int MODE, int EV>
+__global__ void __launch_bounds__(EV ? kFusedThreads : kScanThreads, 1)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
             const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
             const float* __restrict__ thr, MaskRec* __restrict__ recs_all,
             unsigned long long* __restrict__ rcounts, unsigned long long rcap,
             SurvEntry* __restrict__ list_all, unsigned long long cap,
-            unsigned long long* __restrict__ counts) {
+            unsigned long long* __restrict__ counts, EvalCtx ev) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr bool F16 = MODE >= 5;            // fp16 accumulator (full level only)
   constexpr int MB = F16 ? MODE - 5 : MODE;  // the epilogue mode proper
-  const ScanSmem L = scan_smem_layout(g.K);
+  constexpr bool FUSED = EV != 0;
+  const ScanSmem L = scan_smem_layout(g.K, FUSED);
   const int K = g.K;
   unsigned char* sR = smem + L.r_off;
   unsigned char* sP = smem + L.p_off;
@@ -878,6 +1101,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   unsigned* count = reinterpret_cast<unsigned*>(smem + L.bar_off + 448);  // CTA's reserved record slots
   unsigned* ecount = count + 1;  // CTA's reserved entry slots (sparse levels)
   MaskRec* recs = recs_all + (unsigned long long)blockIdx.x * rcap;  // this CTA's partition of `rcap` records
+  EvalRing* ring = FUSED ? reinterpret_cast<EvalRing*>(smem + L.wbuf_off) : nullptr;
+  uint2* ebufs = FUSED ? reinterpret_cast<uint2*>(smem + L.wbuf_off + sizeof(EvalRing)) : nullptr;
+  SurvEntry* elist_cta = list_all + (unsigned long long)blockIdx.x * cap;  // sparse levels: direct entries
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -898,6 +1124,10 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     ptx::fence_mbar_init();
     *count = 0;
     *ecount = 0;
+  }
+  if constexpr (FUSED) {
+    for (uint32_t k = threadIdx.x; k < kRing; k += blockDim.x) ring->seq[k] = k;
+    if (threadIdx.x == 0) ring->head = ring->tail = ring->done = ring->entries = 0;
   }
   if (warp == 1) ptx::tmem_alloc<kScanTmemCols>(tmem_base_smem);
   ptx::tc_fence_before();
@@ -934,6 +1164,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           }
         }
       }
+    }
+    if constexpr (FUSED) {  // the producer warp joins the consumers once every tile is issued
+      __syncwarp();
+      consume<EV>(g, ev, ring, ebufs + (warp * kEvalBuf), recs, (uint32_t)rcap, elist_cta, (uint32_t)cap,
+                  kScanEpiWarps);
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
@@ -984,16 +1219,20 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         __syncwarp();
       }
     }
-  } else {
+    if constexpr (FUSED) {  // the MMA warp joins the consumers once every MMA is issued
+      consume<EV>(g, ev, ring, ebufs + (warp * kEvalBuf), recs, (uint32_t)rcap, elist_cta, (uint32_t)cap,
+                  kScanEpiWarps);
+    }
+  } else if (warp < 2 + kScanEpiWarps) {
     // ================= epilogue =================
     const int e = warp - 2;
     const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
-    WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u};
+    WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u, kSentinel, ring};
     constexpr bool sel = MB >= 2;
-    SurvEntry* elist = list_all + (unsigned long long)blockIdx.x * cap;  // sparse levels: direct entries
+    SurvEntry* elist = elist_cta;
     const uint32_t ecap = (uint32_t)cap;
-    uint32_t ebase = 0, eleft = 0;
+    EntryChunks ech{elist, ecount, ecap, 0u, 0u, kSentinel, ring};
     const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + part * kEpiCols;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
@@ -1081,16 +1320,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
                 if (wmax == 0u) continue;
                 const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
-                if (eleft == 0) {  // warp-level chunk of entry slots
-                  uint32_t nb = 0;
-                  if (lane == 0) nb = atomicAdd(ecount, 32u);
-                  ebase = __shfl_sync(0xffffffffu, nb, 0);
-                  eleft = 32;
-                }
-                if ((uint32_t)lane == win && ebase < ecap)
-                  elist[ebase] = make_uint2(rowbase + 8u * (uint32_t)k + (7u - (wmax & 7u)), d);
-                ++ebase;
-                --eleft;
+                ech.reserve(1);  // warp-level chunk of entry slots
+                if ((uint32_t)lane == win && ech.base < ecap)
+                  elist[ech.base] = make_uint2(rowbase + 8u * (uint32_t)k + (7u - (wmax & 7u)), d);
+                ++ech.base;
+                --ech.left;
               }
             }
             continue;
@@ -1188,21 +1422,14 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           }
           if (!hits) continue;
           const uint32_t nh = (uint32_t)__popc(hits);
-          if (eleft < nh) {  // pad the rest of the chunk, take a new one
-            for (uint32_t q = (uint32_t)lane; q < eleft; q += 32)
-              if (ebase + q < ecap) elist[ebase + q] = make_uint2(kSentinel, kSentinel);
-            uint32_t nb = 0;
-            if (lane == 0) nb = atomicAdd(ecount, 32u);
-            ebase = __shfl_sync(0xffffffffu, nb, 0);
-            eleft = 32;
-          }
+          ech.reserve(nh);  // pads the rest of the chunk and takes a new one when it is short
           if (mine != 0u) {
-            const uint32_t pos = ebase + (uint32_t)__popc(hits & ((1u << lane) - 1u));
+            const uint32_t pos = ech.base + (uint32_t)__popc(hits & ((1u << lane) - 1u));
             const uint32_t wl = 31u - (mine & 31u), ws = 7u - ((mine >> 5) & 7u);
             if (pos < ecap) elist[pos] = make_uint2(rowbase + 8u * (uint32_t)lane + ws, d - (uint32_t)lane + wl);
           }
-          ebase += nh;
-          eleft -= nh;
+          ech.base += nh;
+          ech.left -= nh;
           continue;
         }
         if (MB == 1 && !allpass) {
@@ -1257,36 +1484,48 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           const bool keep = b != 0u && (__uint_as_float(b) > 1.0f || ((allpass >> k) & 1u));
           const uint32_t bal = __ballot_sync(0xffffffffu, keep);
           if (!bal) continue;
-          if (eleft < (uint32_t)__popc(bal)) {  // pad the rest of the chunk, take a new one
-            for (uint32_t q = (uint32_t)lane; q < eleft; q += 32)
-              if (ebase + q < ecap) elist[ebase + q] = make_uint2(kSentinel, kSentinel);
-            uint32_t nb = 0;
-            if (lane == 0) nb = atomicAdd(ecount, 32u);
-            ebase = __shfl_sync(0xffffffffu, nb, 0);
-            eleft = 32;
-          }
-          const uint32_t pos = ebase + __popc(bal & ((1u << lane) - 1u));
+          ech.reserve((uint32_t)__popc(bal));
+          const uint32_t pos = ech.base + __popc(bal & ((1u << lane) - 1u));
           if (keep && pos < ecap) {
             const uint32_t jt = b & 0x1FFFu, s_iso = 7u - ((b >> 13) & 7u);
             const uint32_t dd = dslice + (uint32_t)(jt * lv.stride * kScanTileDom + quarter * 32 + lane);
             elist[pos] = make_uint2(rowbase + 8u * (uint32_t)k + s_iso, dd);
           }
-          ebase += __popc(bal);
-          eleft -= __popc(bal);
+          ech.base += __popc(bal);
+          ech.left -= __popc(bal);
         }
       }
     }
-    // pad the warp's unused entry slots (sparse levels)
-    for (uint32_t k = (uint32_t)lane; k < eleft; k += 32)
-      if (ebase + k < ecap) elist[ebase + k] = make_uint2(kSentinel, kSentinel);
+    // pad the warp's unused entry slots (sparse levels), publish the last chunks
+    ech.close();
     app.close();
+    if constexpr (FUSED) {
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(&ring->done, 1u);
+      }
+      consume<EV>(g, ev, ring, ebufs + (warp * kEvalBuf), recs, (uint32_t)rcap, elist, ecap, kScanEpiWarps);
+    }
+  } else if constexpr (FUSED) {
+    // ================= consumers (evaluation warps) =================
+    consume<EV>(g, ev, ring, ebufs + (warp * kEvalBuf), recs, (uint32_t)rcap, elist_cta, (uint32_t)cap,
+                kScanEpiWarps);
   }
 
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) {
     rcounts[blockIdx.x] = *count;
-    counts[blockIdx.x] = *ecount;  // direct entries (sparse levels); expand_kernel adds the records' entries
+    if (FUSED && MB <= 1) {
+      // full level, fused: the entries were evaluated here (none are stored); a record partition
+      // that overflowed reports at least twice its record count so that the host re-runs the
+      // level with a larger partition (as expand_kernel does)
+      const unsigned long long ent = ring->entries;
+      counts[blockIdx.x] = *count > rcap ? 2ull * *count : (ent < cap ? ent : cap);
+    } else {
+      counts[blockIdx.x] = *ecount;  // direct entries (sparse levels); expand_kernel adds the records' entries
+    }
   }
   if (warp == 1) {
     ptx::tc_fence_after();
@@ -1383,7 +1622,11 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
             const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
             const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
             unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab,
-            uint2* __restrict__ pend, unsigned* __restrict__ pend_counts, unsigned long long seg) {
+            uint2* __restrict__ pend, unsigned* __restrict__ pend_counts, unsigned long long seg,
+            unsigned __int128* __restrict__ win) {
+  // pend == nullptr: every candidate's residual is computed here from the operands in registers
+  // and the (residual, domain * 8 + isometry) minimum is kept per range in `win` (no residual
+  // and winner passes); else the candidates that pass every screen go to the pending list
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const bool screens = !(g.flags & 2);
   const int lane = threadIdx.x & 31;
@@ -1423,12 +1666,16 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
         load_range_words<NN>(img, g, x0, y0, bpk);
         if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
           R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar, screens, false, tab,
-                            qpool, img, d, s, x0, y0, qs, qo, &pending);
-          if (R < inf) publish_best(gbest, r, R);
+                            qpool, img, d, s, x0, y0, qs, qo, pend ? &pending : nullptr);
+          if (R < inf) {
+            publish_best(gbest, r, R);
+            if (!pend) win_min(win + r, R, (uint32_t)d * 8u + (uint32_t)s);
+          }
         }
       }
-      res[i] = R;
+      if (pend) res[i] = R;
     }
+    if (!pend) continue;
     // candidates that passed every screen: (entry, codes) to the residual pass
     const unsigned bal = __ballot_sync(0xffffffffu, pending);
     if (bal) {
@@ -1438,6 +1685,7 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
       if (pending) my_pend[b + __popc(bal & ((1u << lane) - 1u))] = make_uint2((uint32_t)i, qs | (qo << 16));
     }
   }
+  if (!pend) return;
   __syncthreads();
   if (threadIdx.x == 0) pend_counts[blockIdx.x] = s_pend;
 }
@@ -1480,7 +1728,7 @@ residual_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigne
 // smallest (domain, isometry): the reference's first strict minimum (encoder.cpp:281).
 __global__ void winner_kernel(const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts,
                               int parts, unsigned long long part, const double* __restrict__ res,
-                              const unsigned long long* __restrict__ gbest, unsigned* __restrict__ win) {
+                              const unsigned long long* __restrict__ gbest, unsigned __int128* __restrict__ win) {
   const int per = gridDim.x / parts;
   const int c = blockIdx.x / per, sub = blockIdx.x % per;
   const unsigned long long n = min(counts[c], part);
@@ -1491,7 +1739,7 @@ __global__ void winner_kernel(const SurvEntry* __restrict__ list, const unsigned
     if (!(R < __longlong_as_double(0x7ff0000000000000ll))) continue;
     const SurvEntry en = list[i];
     const int r = (int)(en.x >> 3);
-    if ((unsigned long long)__double_as_longlong(R) == gbest[r]) atomicMin(win + r, en.y * 8u + (en.x & 7u));
+    if ((unsigned long long)__double_as_longlong(R) == gbest[r]) win_min(win + r, R, en.y * 8u + (en.x & 7u));
   }
 }
 
@@ -1503,7 +1751,7 @@ template <int NN>
 __global__ void __launch_bounds__(128)
 record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
               const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
-              const unsigned* __restrict__ win, const unsigned long long* __restrict__ gbest,
+              const unsigned __int128* __restrict__ win, const unsigned long long* __restrict__ gbest,
               fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= g.R) return;
@@ -1514,7 +1762,9 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
   load_range_words<NN>(img, g, x0, y0, bpk);
   fic_mapping o;
   o.reserved = 0;
-  const unsigned w = m.shadow ? 0xFFFFFFFFu : win[r];
+  // the (residual, domain * 8 + isometry) minimum; all ones: no non-flat candidate
+  const unsigned __int128 wk = win[r];
+  const unsigned w = (m.shadow || (unsigned long long)(wk >> 64) == ~0ull) ? 0xFFFFFFFFu : (unsigned)wk;
   if (w != 0xFFFFFFFFu) {
     const int d = (int)(w >> 3), s = (int)(w & 7);
     const DomainMetaI mi = meta_i[d];
@@ -1687,32 +1937,55 @@ bool scan_f16sel() {
   return e && e[0] == '1';
 }
 
+typedef void (*ScanKern)(const unsigned char*, Geometry, ScanLevel, const __half*, const RangeMeta*,
+                         const unsigned char*, const float*, MaskRec*, unsigned long long*, unsigned long long,
+                         SurvEntry*, unsigned long long, unsigned long long*, EvalCtx);
+
+template <int EV>
+ScanKern scan_fn(int mode) {
+  switch (mode) {
+    case 0: return scan_kernel<0, EV>;
+    case 1: return scan_kernel<1, EV>;
+    case 2: return scan_kernel<2, EV>;
+    case 3: return scan_kernel<3, EV>;
+    case 4: return scan_kernel<4, EV>;
+    case 5: return scan_kernel<5, EV>;
+    case 6: return scan_kernel<6, EV>;
+    default: return scan_kernel<7, EV>;
+  }
+}
+
+// The fused scan (survivors evaluated inside the scan kernel): opt-in, FIC_FUSED=1 (measured
+// slower than the separate evaluation pass on every configuration).
+bool scan_fused() {
+  const char* e = std::getenv("FIC_FUSED");
+  return e && e[0] == '1';
+}
+
 cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride, int sms, const __half* upool,
                         const RangeMeta* rmeta, const unsigned char* ropnd, const float* thr, SurvEntry* list,
                         unsigned long long* counts, unsigned long long part, void* recs, unsigned long long* rcounts,
-                        cudaStream_t st) {
+                        const unsigned short* qpool, const DomainMetaI* meta_i, unsigned long long* gbest,
+                        void* win, const double* deq, bool fused, cudaStream_t st) {
   const int grid = scan_grid(g, stride, sms);
   const ScanLevel lv = make_level(g, stride, grid);
-  const ScanSmem L = scan_smem_layout(g.K);
+  const ScanSmem L = scan_smem_layout(g.K, fused);
   int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
   // fp16 accumulator: the full level only (its thresholds carry the fp16 bound, range_op_kernel)
   if (scan_f16acc(g) && stride == 1 && mode <= 1) mode += 5;
   if (mode == 2 && scan_f16sel()) mode = 7;
-  auto kern = mode == 7   ? scan_kernel<7>
-              : mode == 6 ? scan_kernel<6>
-              : mode == 5 ? scan_kernel<5>
-              : mode == 4 ? scan_kernel<4>
-              : mode == 3 ? scan_kernel<3>
-              : mode == 2 ? scan_kernel<2>
-              : mode == 1 ? scan_kernel<1>
-                          : scan_kernel<0>;
+  const ScanKern kern = !fused ? scan_fn<0>(mode)
+                        : g.N == 4 ? scan_fn<4>(mode) : (g.N == 16 ? scan_fn<16>(mode) : scan_fn<64>(mode));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   const unsigned long long rcap = scan_rec_part(part);
   MaskRec* R = static_cast<MaskRec*>(recs);
-  kern<<<grid, kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts, rcap, list, part, counts);
+  const EvalCtx ev{img, qpool, meta_i, rmeta, gbest, static_cast<unsigned __int128*>(win),
+                   DeqTables{deq, deq + (1 << g.s_bits)}};
+  kern<<<grid, fused ? kFusedThreads : kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts,
+                                                                    rcap, list, part, counts, ev);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || fused) return e;
   expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
   return cudaGetLastError();
 }
@@ -1746,9 +2019,10 @@ size_t range_op_bytes(const Geometry& g) {
 // range operands.
 void launch_level_ops(const unsigned char* img, const Geometry& g, const RangeMeta* rmeta,
                       const unsigned long long* gbest, float* thr, unsigned char* ropnd,
-                      unsigned long long* pend_count, unsigned* win, unsigned long long* selfcheck, cudaStream_t st) {
+                      unsigned long long* pend_count, bool full_level, unsigned long long* selfcheck,
+                      cudaStream_t st) {
   range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(
-      img, g, rmeta, gbest, thr, ropnd, pend_count, win, selfcheck);
+      img, g, rmeta, gbest, thr, ropnd, pend_count, full_level ? 1 : 0, selfcheck);
 }
 
 // Pending-list segment per eval block: the most entries one block can take (eval_kernel's
@@ -1759,38 +2033,50 @@ unsigned long long eval_pend_seg(unsigned long long part) {
   return (part + stride - 1) / stride * 256;
 }
 
+// inline_res: residuals and the per-range winner key in eval_kernel itself (no residual pass;
+// the final level needs no winner pass either); else eval + residual kernels (pending list).
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
                  const RangeMeta* rmeta, const SurvEntry* list, const unsigned long long* counts, int parts,
                  unsigned long long part, double* res, unsigned long long* gbest, const double* deq, uint2* pend,
-                 unsigned* pend_counts, int sms, cudaStream_t st) {
+                 unsigned* pend_counts, void* win_, bool inline_res, int sms, cudaStream_t st) {
   (void)sms;
   const int blocks = parts * kEvalPer;
   const unsigned long long seg = eval_pend_seg(part);
   const DeqTables tab{deq, deq + (1 << g.s_bits)};
+  unsigned __int128* win = static_cast<unsigned __int128*>(win_);
+  uint2* pd = inline_res ? nullptr : pend;
+#define FIC_EVAL(NN)                                                                                                 \
+  eval_kernel<NN><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab, \
+                                          pd, pend_counts, seg, win);                                                \
+  if (!inline_res)                                                                                                   \
+    residual_kernel<NN><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
   if (g.N == 4) {
-    eval_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
-                                           pend, pend_counts, seg);
-    residual_kernel<4><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
+    FIC_EVAL(4)
   } else if (g.N == 16) {
-    eval_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
-                                            pend, pend_counts, seg);
-    residual_kernel<16><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
+    FIC_EVAL(16)
   } else {
-    eval_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab,
-                                            pend, pend_counts, seg);
-    residual_kernel<64><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
+    FIC_EVAL(64)
   }
+#undef FIC_EVAL
+}
+
+// Inline residuals in eval_kernel (FIC_EVAL_SPLIT=1: separate pending-list residual pass).
+bool eval_inline() {
+  const char* e = std::getenv("FIC_EVAL_SPLIT");
+  return !(e && e[0] == '1');
 }
 
 void launch_winner(const SurvEntry* list, const unsigned long long* counts, int parts, unsigned long long part,
-                   const double* res, const unsigned long long* gbest, unsigned* win, int sms, cudaStream_t st) {
-  winner_kernel<<<parts * 16, 256, 0, st>>>(list, counts, parts, part, res, gbest, win);
+                   const double* res, const unsigned long long* gbest, void* win, int sms, cudaStream_t st) {
+  winner_kernel<<<parts * 16, 256, 0, st>>>(list, counts, parts, part, res, gbest,
+                                            static_cast<unsigned __int128*>(win));
 }
 
 void launch_record(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
-                   const DomainMetaI* meta_i, const RangeMeta* rmeta, const unsigned* win,
+                   const DomainMetaI* meta_i, const RangeMeta* rmeta, const void* win_,
                    const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck, cudaStream_t st) {
   const int blocks = (g.R + 127) / 128;
+  const unsigned __int128* win = static_cast<const unsigned __int128*>(win_);
   if (g.N == 4) record_kernel<4><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
   else if (g.N == 16) record_kernel<16><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
   else record_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);

@@ -436,3 +436,20 @@ def test_sparse_selection_modes_output_neutral(oracle, select):
             enc = fic.encode(img, fic.CodecParams(**pv))
         assert_same(enc.mappings, want, f"select={select} {pv}")
         assert enc.stats == st
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_fused_and_separate_evaluation(oracle, fused):
+    """Survivors evaluated inside the scan kernel (default: consumer warps fed by the epilogue's
+    chunks) or by the separate expand / eval / residual / winner kernels (FIC_FUSED=0): both give
+    the reference's records, including with a survivor list small enough to overflow (the full
+    level re-runs) and with every candidate surviving (exhaustive)."""
+    cases = [(oracle.noise_image(64, 9), dict(n=4, step=2)), (oracle.smooth_image(64, 5), dict(n=8, step=2)),
+             (images.ct_slice(256, 1404002, 0.3), dict(n=8, step=4)), (oracle.noise_image(64, 11), dict(n=2, step=1))]
+    for img, pv in cases:
+        want, st = oracle.encode(img, pv)
+        for extra in (dict(), dict(FIC_LIST_CAP=3000), dict(FIC_DEBUG=1)):
+            with env(FIC_FUSED=fused, **extra):
+                enc = fic.encode(img, fic.CodecParams(**pv))
+            assert_same(enc.mappings, want, f"fused={fused} {extra} {pv}")
+            assert enc.stats == st
