@@ -54,7 +54,7 @@ bool scan_supported(const Geometry&);
 int scan_tiles(const Geometry&);
 long long scan_pool_domains(const Geometry&);
 void launch_pool_v3(const unsigned char*, const Geometry&, __half*, unsigned short*, DomainMetaI*,
-                    unsigned long long*, cudaStream_t);
+                    unsigned long long*, RangeMeta*, unsigned long long*, void*, double*, cudaStream_t);
 void launch_fill_u64(unsigned long long*, long long, unsigned long long, cudaStream_t);
 void launch_seed_v3(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
                     const RangeMeta*, unsigned long long*, const double*, cudaStream_t);
@@ -450,22 +450,20 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   // self-check slots, the host reads only the partitions a level used
   const bool time_pool = g_timing.load() != 0;
   if (time_pool) CK(cudaEventRecord(ws.ev4, st));
-  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, st);  // flat domains per slice
+  // K1 pool + range pass + bar / winner init + dequantised tables in one launch
+  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, b.rm, b.gbest, b.win, b.deq, st);
   if (time_pool) {
     CK(cudaEventRecord(ws.ev5, st));
     // algorithmic bytes: the image read once, the pool written once (fp16 operand 2K, exact
-    // cells 8 x N u16, meta 16 B per padded domain)
+    // cells 8 x N u16, meta 16 B per padded domain), and the preparations riding in the same
+    // launch: per range its N pixels read, RangeMeta (16 B), bar (8 B) and winner key (16 B)
     const double Dt = (double)g.Dt * g.batch;
-    ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0);
+    ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0) + (double)g.R * (g.N + 40.0);
   }
-  launch_range_pass(d_img, g, b.rm, d_counters + g.batch, st);       // shadow ranges per slice
-  launch_fill_u64(b.gbest, g.R, 0x7ff0000000000000ull, st);
-  launch_fill_u64(static_cast<unsigned long long*>(b.win), 2ll * g.R, ~0ull, st);  // no winner yet
-  launch_deq_tables(g, b.deq, st);
   const char* seed_env = std::getenv("FIC_SEED");  // "0": no local seed (A/B)
   const bool seed = !(seed_env && std::strcmp(seed_env, "0") == 0);
   if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
-  g_launches += seed ? 6 : 5;
+  g_launches += seed ? 2 : 1;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
   const std::vector<int> lv = scan_levels(g);
   for (size_t l = 0; l + 1 < lv.size(); ++l) enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st);
@@ -1044,7 +1042,7 @@ int32_t fic_debug_pool(const uint8_t* image, int32_t width, int32_t height, cons
     auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * sizeof(unsigned long long)));
     CK(cudaMemcpyAsync(d_img, image, img_bytes, cudaMemcpyHostToDevice, ws.stream));
     CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), ws.stream));
-    launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_cnt, ws.stream);
+    launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_cnt, nullptr, nullptr, nullptr, nullptr, ws.stream);
     g_launches += 1;
     std::vector<DomainMetaI> mi(g.D);
     CK(cudaMemcpyAsync(mi.data(), b.mi, (size_t)g.D * sizeof(DomainMetaI), cudaMemcpyDeviceToHost, ws.stream));

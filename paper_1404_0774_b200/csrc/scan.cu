@@ -68,42 +68,102 @@ typedef uint2 SurvEntry;
 constexpr int kPoolThreads = 512;
 static_assert(kPoolThreads == 4 * kPoolBlock, "pool moments: four threads per domain");
 
+// The encode's other per-range / per-code preparations ride in the same launch (blocks past
+// the pool's): the range pass (sums, variance, shadow test; encoder.cpp:165-181), the bar and
+// winner-key initialisation and the dequantised code tables (one launch instead of five).
+struct PrepAux {
+  RangeMeta* rmeta;
+  unsigned long long* shadow_count;
+  unsigned long long* gbest;
+  unsigned long long* win;  // 2 words per range
+  double* deq;              // 2^s_bits s values, then 2^o_bits o values
+  int pool_blocks;
+};
+
+__device__ void prep_aux(const unsigned char* __restrict__ img, const Geometry& g, const PrepAux& a) {
+  const int tid = (blockIdx.x - a.pool_blocks) * blockDim.x + threadIdx.x;
+  const int nthreads = (gridDim.x - a.pool_blocks) * blockDim.x;
+  for (int r = tid; r < g.R; r += nthreads) {
+    int x0, y0;
+    range_origin(g, r, x0, y0);
+    long long sb = 0, sbb = 0;
+    for (int i = 0; i < g.n; ++i) {
+      const unsigned char* row = img + (long long)(y0 + i) * g.W + x0;
+      for (int j = 0; j < g.n; ++j) {
+        const int v = row[j];
+        sb += v;
+        sbb += v * v;
+      }
+    }
+    const long long var = (long long)g.N * sbb - sb * sb;
+    const int shadow = (double)var <= g.shadow_eps;
+    a.rmeta[r] = RangeMeta{(int)sb, shadow, var};
+    if (shadow) atomicAdd(a.shadow_count + range_slice(g, r), 1ull);  // per slice of a batch
+    a.gbest[r] = 0x7ff0000000000000ull;  // +inf: no bar yet
+    a.win[2 * r] = ~0ull;                // no winner yet
+    a.win[2 * r + 1] = ~0ull;
+  }
+  const int ns = 1 << g.s_bits, no = 1 << g.o_bits;
+  for (int c = tid; c < ns + no; c += nthreads) {  // UniformQuantizer::dequantize (format.hpp:34-40)
+    if (c < ns) a.deq[c] = dequantize((unsigned)c, g.s_max, g.s_bits);
+    else a.deq[c] = dequantize((unsigned)(c - ns), 255.0, g.o_bits);
+  }
+}
+
 __global__ void __launch_bounds__(kPoolThreads)
 pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __restrict__ upool,
                unsigned short* __restrict__ qpool, DomainMetaI* __restrict__ meta_i,
-               unsigned long long* __restrict__ flat_count) {
-  extern __shared__ __align__(16) unsigned short sq_tile[];  // 128 x N contracted cells
+               unsigned long long* __restrict__ flat_count, PrepAux aux) {
+  if ((int)blockIdx.x >= aux.pool_blocks) {
+    prep_aux(img, g, aux);
+    return;
+  }
+  extern __shared__ __align__(16) unsigned short sq_tile[];  // 128 x N contracted cells, then their transposes
+  unsigned short* sq_tileT = sq_tile + kPoolBlock * g.N;      // per domain: TT[c][r] = q[r][c]
   __shared__ double s_inv[kPoolBlock];
   __shared__ long long s_sum[kPoolBlock];
   __shared__ long long s_sqq[kPoolBlock];
+  __shared__ int s_org[kPoolBlock];  // pixel offset of each domain's window (-1: padding)
   __shared__ unsigned char s_perm[kSyms * 64];
   __shared__ unsigned s_flat;
   const int t = threadIdx.x;
   const int N = g.N, n = g.n, K = g.K;
+  // N, n and K / 8 are powers of two: index arithmetic by shifts and masks (the kernel is
+  // issue-bound on large pools otherwise)
+  const int lgN = __ffs(N) - 1, lgn = __ffs(n) - 1, lgkc = __ffs(K >> 3) - 1;
   const long long dbase = (long long)blockIdx.x * kPoolBlock;
   if (t == 0) s_flat = 0;
   for (int k = t; k < kSyms * N; k += kPoolThreads) {  // perm_s(i) (transforms.cpp:13-26)
-    const int s = k / N, i = k % N;
+    const int s = k >> lgN, i = k & (N - 1);
     int sr, sc;
-    symmetry_source(s, i / n, i % n, n, sr, sc);
+    symmetry_source(s, i >> lgn, i & (n - 1), n, sr, sc);
     s_perm[k] = (unsigned char)(sr * n + sc);
   }
   // a block never straddles slices of a batch (Dt is a multiple of the block)
   const int slice = g.batch > 1 ? (int)(dbase / g.Dt) : 0;
   const long long lbase = dbase - (long long)slice * (g.batch > 1 ? g.Dt : 0);  // slice-local index
-  // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step
-  for (int idx = t; idx < kPoolBlock * N; idx += kPoolThreads) {
-    const int dl = idx / N, j = idx % N;
-    const long long d = dbase + dl;
-    int v = 0;
-    if (lbase + dl < g.D) {
+  if (t < kPoolBlock) {  // domain origins once per domain (the divisions by PY and Dt)
+    int o = -1;
+    if (lbase + t < g.D) {
       int x, y;
-      domain_origin_px(g, (int)d, x, y);
-      const unsigned char* row0 = img + (long long)(y + 2 * (j / n)) * g.W + x + 2 * (j % n);
+      domain_origin_px(g, (int)(dbase + t), x, y);
+      o = y * g.W + x;
+    }
+    s_org[t] = o;
+  }
+  __syncthreads();
+  // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step
+  for (int idx = t; idx < (kPoolBlock << lgN); idx += kPoolThreads) {
+    const int dl = idx >> lgN, j = idx & (N - 1);
+    const int o = s_org[dl];
+    int v = 0;
+    if (o >= 0) {
+      const unsigned char* row0 = img + (long long)o + (long long)(2 * (j >> lgn)) * g.W + 2 * (j & (n - 1));
       const unsigned char* row1 = row0 + g.W;
       v = row0[0] + row0[1] + row1[0] + row1[1];
     }
     sq_tile[idx] = (unsigned short)v;
+    sq_tileT[(dl << lgN) + ((j & (n - 1)) << lgn) + (j >> lgn)] = (unsigned short)v;
   }
   __syncthreads();
   // moments of domain t: Sq, Sqq, den = N*Sqq - Sq^2 (exact), flat iff (double)den <= 16*shadow_eps (encoder.cpp:223)
@@ -112,7 +172,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     const int dl = t >> 2, part = t & 3;
     long long s = 0, ss = 0;
     for (int j = part; j < N; j += 4) {
-      const int v = sq_tile[dl * N + ((j + dl) % N)];  // rotated start: fewer bank conflicts
+      const int v = sq_tile[(dl << lgN) + ((j + dl) & (N - 1))];  // rotated start: fewer bank conflicts
       s += v;
       ss += (long long)v * v;
     }
@@ -129,7 +189,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   if (t < kPoolBlock) {
     const long long d = dbase + t;
     const long long s = s_sum[t], ss = s_sqq[t];
-    if (lbase + t < g.D) {
+    if (s_org[t] >= 0) {
       const long long den = (long long)N * ss - s * s;
       const bool flat = (double)den <= 16.0 * g.shadow_eps;
       meta_i[d] = DomainMetaI{s, flat ? -1 : den};
@@ -146,9 +206,8 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
   // phase 2a: fp16 normalised operand u = (N q - Sq) / sqrt(den), UMMA K-major no-swizzle
   // core matrices, chunk c = ((dl/8) * (K/8) + k/8) * 8 + dl%8 (16-byte coalesced stores)
   uint4* out = reinterpret_cast<uint4*>(upool + dbase * K);
-  const int kc_n = K / 8;
-  for (int c = t; c < kPoolBlock * kc_n; c += kPoolThreads) {
-    const int d8 = c & 7, kc = (c >> 3) % kc_n, dg = (c >> 3) / kc_n;
+  for (int c = t; c < (kPoolBlock << lgkc); c += kPoolThreads) {
+    const int d8 = c & 7, kc = (c >> 3) & ((1 << lgkc) - 1), dg = (c >> 3) >> lgkc;
     const int dl = dg * 8 + d8;
     const double inv = s_inv[dl];
     const double sN = (double)s_sum[dl];
@@ -160,7 +219,7 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
       for (int u = 0; u < 2; ++u) {
         const int k = kc * 8 + 2 * h + u;
         float v = 0.f;
-        if (k < N) v = (float)(((double)N * (double)sq_tile[dl * N + k] - sN) * inv);
+        if (k < N) v = (float)(((double)N * (double)sq_tile[(dl << lgN) + k] - sN) * inv);
         pair |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * u);
       }
       w[h] = pair;
@@ -168,18 +227,30 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     out[c] = make_uint4(w[0], w[1], w[2], w[3]);
   }
   // phase 2b: exact contracted cells per isometry, row (d, s)[i] = q[perm_s(i)] (u16): the
-  // survivor evaluation reads one contiguous row instead of gathering through the isometry
-  if (N >= 8) {
-    const int wpr = N / 8;  // 16-byte words per row
-    uint4* qdst = reinterpret_cast<uint4*>(qpool + dbase * kSyms * N);
-    for (int c = t; c < kPoolBlock * kSyms * wpr; c += kPoolThreads) {
-      const int w = c % wpr, row = c / wpr, sym = row & 7, dl = row >> 3;
-      const unsigned char* pr = s_perm + sym * N + w * 8;
-      const unsigned short* qs = sq_tile + dl * N;
-      uint32_t v[4];
-#pragma unroll
-      for (int h = 0; h < 4; ++h) v[h] = (uint32_t)qs[pr[2 * h]] | ((uint32_t)qs[pr[2 * h + 1]] << 16);
-      qdst[c] = make_uint4(v[0], v[1], v[2], v[3]);
+  // survivor evaluation reads one contiguous row instead of gathering through the isometry.
+  // Pixel row r of isometry s is one source row or column of the block, forward or reversed
+  // (symmetry_source): s 0 row r, 1 column r reversed, 2 row m-r reversed, 3 column m-r,
+  // 4 row r reversed, 5 row m-r, 6 column r, 7 column m-r reversed (m = n - 1) — one aligned
+  // shared-memory vector load from the tile or its transpose plus a half-word reversal.
+  if (n == 8) {
+    uint4* qdst = reinterpret_cast<uint4*>(qpool + dbase * kSyms * 64);
+    for (int c = t; c < kPoolBlock * kSyms * 8; c += kPoolThreads) {
+      const int r = c & 7, sym = (c >> 3) & 7, dl = c >> 6;
+      const bool col = (0xCAu >> sym) & 1u, rev = (0x96u >> sym) & 1u, mir = (0xACu >> sym) & 1u;
+      const int idx = mir ? 7 - r : r;
+      const uint4 v = reinterpret_cast<const uint4*>((col ? sq_tileT : sq_tile) + (dl << 6))[idx];
+      qdst[c] = rev ? make_uint4(__byte_perm(v.w, 0, 0x1032), __byte_perm(v.z, 0, 0x1032), __byte_perm(v.y, 0, 0x1032),
+                                 __byte_perm(v.x, 0, 0x1032))
+                    : v;
+    }
+  } else if (n == 4) {
+    uint2* qdst = reinterpret_cast<uint2*>(qpool + dbase * kSyms * 16);
+    for (int c = t; c < kPoolBlock * kSyms * 4; c += kPoolThreads) {
+      const int r = c & 3, sym = (c >> 2) & 7, dl = c >> 5;
+      const bool col = (0xCAu >> sym) & 1u, rev = (0x96u >> sym) & 1u, mir = (0xACu >> sym) & 1u;
+      const int idx = mir ? 3 - r : r;
+      const uint2 v = reinterpret_cast<const uint2*>((col ? sq_tileT : sq_tile) + (dl << 4))[idx];
+      qdst[c] = rev ? make_uint2(__byte_perm(v.y, 0, 0x1032), __byte_perm(v.x, 0, 0x1032)) : v;
     }
   } else {  // N == 4: one 8-byte row per (domain, isometry)
     uint2* qdst = reinterpret_cast<uint2*>(qpool + dbase * kSyms * N);
@@ -623,10 +694,11 @@ struct Segment {
   int m, j0, j1;  // m-tile, level tiles [j0, j1)
 };
 
+// (32-bit arithmetic: rem < G <= 256 CTAs, k <= 16, level tiles < 2^20, so every product fits)
 __host__ __device__ inline int seg_count(const ScanLevel& lv, int c, int G) {
   if (lv.rem == 0) return lv.rounds;
-  const long long U = (long long)lv.rem * lv.k;
-  return lv.rounds + (int)(U * (c + 1) / G - U * c / G);
+  const unsigned U = (unsigned)lv.rem * (unsigned)lv.k;
+  return lv.rounds + (int)(U * (unsigned)(c + 1) / (unsigned)G - U * (unsigned)c / (unsigned)G);
 }
 
 __host__ __device__ inline Segment seg_at(const ScanLevel& lv, int c, int G, int s) {
@@ -637,12 +709,12 @@ __host__ __device__ inline Segment seg_at(const ScanLevel& lv, int c, int G, int
     sg.j1 = lv.n_lvl;
     return sg;
   }
-  const long long U = (long long)lv.rem * lv.k;
-  const long long u = U * c / G + (s - lv.rounds);
-  const int chunk = (int)(u / lv.rem), mr = (int)(u % lv.rem);
-  sg.m = lv.rounds * G + mr;
-  sg.j0 = (int)((long long)lv.n_lvl * chunk / lv.k);
-  sg.j1 = (int)((long long)lv.n_lvl * (chunk + 1) / lv.k);
+  const unsigned U = (unsigned)lv.rem * (unsigned)lv.k;
+  const unsigned u = U * (unsigned)c / (unsigned)G + (unsigned)(s - lv.rounds);
+  const unsigned chunk = u / (unsigned)lv.rem, mr = u % (unsigned)lv.rem;
+  sg.m = lv.rounds * G + (int)mr;
+  sg.j0 = (int)((unsigned)lv.n_lvl * chunk / (unsigned)lv.k);
+  sg.j1 = (int)((unsigned)lv.n_lvl * (chunk + 1) / (unsigned)lv.k);
   return sg;
 }
 
@@ -1847,11 +1919,17 @@ long long scan_pool_domains(const Geometry& g) {
 
 int scan_rows_per_cta() { return kScanRanges; }
 
+// K1 plus the encode's preparations (PrepAux): counters[b] = flat domains, counters[batch + b]
+// = shadow ranges of slice b (zeroed by the caller).  rmeta / gbest / win / deq may be null
+// (pool only: the read-back probe).
 void launch_pool_v3(const unsigned char* img, const Geometry& g, __half* upool, unsigned short* qpool,
-                    DomainMetaI* meta_i, unsigned long long* flat_count, cudaStream_t st) {
+                    DomainMetaI* meta_i, unsigned long long* counters, RangeMeta* rmeta, unsigned long long* gbest,
+                    void* win, double* deq, cudaStream_t st) {
   const int blocks = (int)((long long)g.Dt * g.batch / kPoolBlock);
-  pool_v3_kernel<<<blocks, kPoolThreads, kPoolBlock * g.N * sizeof(unsigned short), st>>>(img, g, upool, qpool,
-                                                                                           meta_i, flat_count);
+  const int aux_blocks = rmeta ? (g.R + kPoolThreads - 1) / kPoolThreads : 0;
+  const PrepAux aux{rmeta, counters + g.batch, gbest, static_cast<unsigned long long*>(win), deq, blocks};
+  pool_v3_kernel<<<blocks + aux_blocks, kPoolThreads, 2 * kPoolBlock * g.N * sizeof(unsigned short), st>>>(
+      img, g, upool, qpool, meta_i, counters, aux);
 }
 
 void launch_fill_u64(unsigned long long* p, long long n, unsigned long long v, cudaStream_t st) {
