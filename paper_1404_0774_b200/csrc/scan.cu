@@ -152,7 +152,10 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     s_org[t] = o;
   }
   __syncthreads();
-  // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step
+  // phase 1: 2x2 group sums (encoder.cpp:213-215), one (domain, cell) per thread and step; with
+  // an even step (and row stride) every cell's pixel pairs are 2-byte aligned: two 16-bit loads
+  // per cell instead of four byte loads (the kernel is L1-bound on large pools)
+  const bool pairs = ((g.step | g.W) & 1) == 0 && ((uintptr_t)img & 1) == 0;
   for (int idx = t; idx < (kPoolBlock << lgN); idx += kPoolThreads) {
     const int dl = idx >> lgN, j = idx & (N - 1);
     const int o = s_org[dl];
@@ -160,7 +163,13 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
     if (o >= 0) {
       const unsigned char* row0 = img + (long long)o + (long long)(2 * (j >> lgn)) * g.W + 2 * (j & (n - 1));
       const unsigned char* row1 = row0 + g.W;
-      v = row0[0] + row0[1] + row1[0] + row1[1];
+      if (pairs) {
+        const unsigned a0 = *reinterpret_cast<const unsigned short*>(row0);
+        const unsigned a1 = *reinterpret_cast<const unsigned short*>(row1);
+        v = (int)((a0 & 0xFFu) + (a0 >> 8) + (a1 & 0xFFu) + (a1 >> 8));
+      } else {
+        v = row0[0] + row0[1] + row1[0] + row1[1];
+      }
     }
     sq_tile[idx] = (unsigned short)v;
     sq_tileT[(dl << lgN) + ((j & (n - 1)) << lgn) + (j >> lgn)] = (unsigned short)v;
@@ -1740,8 +1749,15 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
           R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar, screens, false, tab,
                             qpool, img, d, s, x0, y0, qs, qo, pend ? &pending : nullptr);
           if (R < inf) {
-            publish_best(gbest, r, R);
-            if (!pend) win_min(win + r, R, (uint32_t)d * 8u + (uint32_t)s);
+            if (pend) {
+              publish_best(gbest, r, R);
+            } else if (R <= bar) {
+              // only a residual at or below the bar read above can lower it or be the final
+              // (residual, index) minimum: the bar never drops below the final minimum (seed
+              // values are upper bounds of candidates the full level evaluates exactly)
+              const unsigned long long rb = (unsigned long long)__double_as_longlong(R);
+              if (rb <= atomicMin(gbest + r, rb)) win_min(win + r, R, (uint32_t)d * 8u + (uint32_t)s);
+            }
           }
         }
       }
