@@ -467,7 +467,9 @@ def run_ours(args):
         if dec:
             dec_scale, dec_ms, dec_bytes = dec
             line["decoder"] = {
-                "kernel": "decode_mean_kernel (+ fused step-RMSE partials and next 2x2 means)", "bound": "hbm",
+                "kernel": "decode_means_kernel (mean-raster iterations: step RMSE from the previous means, next 2x2 "
+                          "means, quantised image in the last iteration; the fp64 raster never round-trips HBM)",
+                "bound": "hbm (algorithmic: the reference's raster read + write per pixel and iteration)",
                 "scale": dec_scale, "iterations": 10, "output": f"{side * dec_scale}^2 fp64",
                 "ms": dec_ms, "achieved": dec_bytes / (dec_ms / 1e3) / 1e9 if dec_ms > 0 else None,
                 "peak": hbm, "unit": "GB/s",

@@ -197,37 +197,54 @@ decode_tile_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
 // ------------------------------------------------------------------ mean-raster decoder
 // Every 2x2 mean the decoder reads, z = ((p00 + p01) + p10 + p11) / 4 at (dy + 2 sr, dx + 2 sc),
 // lies on the even grid whenever every magnified domain origin (dx, dy) is even (checked on
-// the host against the actual mappings: scale even, or every x and y even).  Then an iteration needs only the half-resolution MEAN raster m(i, j) = z at
-// (2i, 2j) of the current raster (a quarter of its size, L2-resident up to 8192^2 outputs),
-// and each output tile, being 32 x 32 at even coordinates, yields the next iteration's means
-// of its own outputs.  Per iteration the full raster is written once and read once (the
-// step RMSE's current values), instead of gathering four doubles per output pixel.  Same
-// per-value arithmetic in the same order, so every raster value is bit-identical.
+// the host against the actual mappings: scale even, or every x and y even).  Then iteration i
+// needs only the half-resolution MEAN raster m_i (m_i(a, b) = z at (2a, 2b) of raster i): output
+// pixel P of iteration i + 1 is v_{i+1}(P) = s_P * m_i(src(P)) + o_P, with src and (s, o) fixed
+// by P's range.  So the full-resolution raster never has to exist between iterations:
+//   * the step RMSE's current value v_i(P) = s_P * m_{i-1}(src(P)) + o_P is recomputed from the
+//     previous mean raster (the same operations on the same operands, so the same bits as the
+//     stored raster value), the initial raster being read only in iteration 0;
+//   * each 32 x 32 output tile forms its own 2 x 2 means m_{i+1} (quarter size);
+//   * the last iteration writes the quantised output image directly (decoder.cpp:99-109).
+// Per iteration and output pixel that is 8 B of m_i + 8 B of m_{i-1} read and 2 B of m_{i+1}
+// written — three quarter-size rasters, L2-resident up to 4096^2 outputs (3 x 33.5 MB) — instead
+// of an 8 B raster write and an 8 B raster read in HBM.  Every raster value, the output image
+// and each step's sum of squared differences are those of the per-pixel kernel.
 bool decode_mean_ok(int out_w, int out_h, int kn, bool even_origins) {
   return decode_tiled(out_w, out_h, kn) && even_origins;
 }
 
-__global__ void mean_raster_kernel(const double* __restrict__ r, double* __restrict__ m, int out_w, int out_h) {
+// m_0: the initial raster's 2 x 2 means (constant kinds: the constant).
+__global__ void mean_init_kernel(double* __restrict__ m, int out_w, int out_h, int kind,
+                                 const unsigned char* __restrict__ sup) {
   const int hw = out_w / 2;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)hw * (out_h / 2)) return;
+  if (kind != FIC_INITIAL_SUPPLIED) {
+    m[i] = kind == FIC_INITIAL_MID_GRAY ? 128.0 : 0.0;  // (c + c + c + c) / 4 == c exactly
+    return;
+  }
   const int y = (int)(i / hw), x = (int)(i % hw);
-  const double* p = r + (long long)(2 * y) * out_w + 2 * x;
-  m[i] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(p[0], p[1]), p[out_w]), p[out_w + 1]), 0.25);
+  const unsigned char* p = sup + (long long)(2 * y) * out_w + 2 * x;
+  m[i] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn((double)p[0], (double)p[1]), (double)p[out_w]), (double)p[out_w + 1]),
+                   0.25);
 }
 
 // LT = log2 of the block side T: 5 = the tile lies inside one range (kn a multiple of 32), else
 // T = kn = 2^LT < 32 and the tile holds (32/T)^2 whole ranges.  Index arithmetic is shifts and
-// masks (the kernel is issue-bound otherwise: per-pixel divisions by kn).
+// masks.  mprev == nullptr: iteration 0, the current values come from the initial raster
+// (init_kind, sup); out_u8 != nullptr: also write the quantised image of this iteration's output.
 template <int LT>
 __global__ void __launch_bounds__(kTileThreads)
-decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mcur, double* __restrict__ nxt,
-                   double* __restrict__ mnxt, const RangeXform* __restrict__ xf, int out_w, int kn, int ranges_x,
-                   double* __restrict__ partial) {
+decode_means_kernel(const double* __restrict__ mcur, const double* __restrict__ mprev, int init_kind,
+                    const unsigned char* __restrict__ sup, double* __restrict__ mnxt,
+                    const RangeXform* __restrict__ xf, int out_w, int kn, int ranges_x,
+                    double* __restrict__ partial, unsigned char* __restrict__ out_u8) {
   constexpr bool kWhole = LT == 5;
   constexpr int T = 1 << LT, bpr = kTile / T, nb = bpr * bpr;
-  __shared__ double zs[kTile][kTile + 1];
-  __shared__ double vs[kTile][kTile + 1];
+  __shared__ double zs[kTile][kTile + 1];  // m_i at the tile's sources
+  __shared__ double ps[kTile][kTile + 1];  // m_{i-1} at the same places (i >= 1)
+  __shared__ double vs[kTile][kTile + 1];  // the tile's new values (its 2 x 2 means)
   struct Blk {
     double s, o;
     int mrow0, mcol0;  // mean-raster origin of the block's source sub-square (T x T)
@@ -236,21 +253,12 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
   __shared__ Blk blk[kWhole ? 1 : nb];
   const int hw = out_w / 2;
   const int Y0 = blockIdx.y * kTile, X0 = blockIdx.x * kTile;  // 2-D grid of tiles
-  // 32-bit element offsets (rasters up to 2^31 doubles) from per-tile base pointers
-  const double* cur_t = cur + (long long)Y0 * out_w + X0;
-  double* nxt_t = nxt + (long long)Y0 * out_w + X0;
   const int lane_c = threadIdx.x & (kTile - 1), row0 = threadIdx.x >> 5;  // element e = threadIdx.x + 256 k
   constexpr int kPer = kTile * kTile / kTileThreads;
   constexpr int kRowStep = kTileThreads / kTile;
-  double zv[kPer], cv[kPer];
-  // the tile's current values (step RMSE) first: they depend on nothing, so their DRAM reads
-  // overlap the code-record load and the block setup
-  if (partial) {
-#pragma unroll
-    for (int k = 0; k < kPer; ++k)
-      cv[k] = __ldcs(cur_t + (row0 + k * kRowStep) * out_w + lane_c);
-  }
-  Blk B;     // kWhole: the tile's one block, computed by every thread (broadcast load, no sync)
+  const bool first = mprev == nullptr;
+  double zv[kPer], pv[kPer];
+  Blk B;
   int a0 = 0, c0 = 0;  // kWhole: the tile's offset inside its range
   if (kWhole) {
     const int ry = Y0 / kn, rx = X0 / kn;
@@ -268,8 +276,11 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     B.mrow0 = t.dy / 2 + B.sr0;
     B.mcol0 = t.dx / 2 + B.sc0;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k)
-      zv[k] = __ldg(mcur + (B.mrow0 + row0 + k * kRowStep) * hw + B.mcol0 + lane_c);
+    for (int k = 0; k < kPer; ++k) {
+      const long long off = (long long)(B.mrow0 + row0 + k * kRowStep) * hw + B.mcol0 + lane_c;
+      zv[k] = __ldg(mcur + off);
+      pv[k] = first ? 0.0 : __ldg(mprev + off);
+    }
   } else {
     for (int b = threadIdx.x; b < nb; b += kTileThreads) {
       const int ry = (Y0 >> LT) + b / bpr, rx = (X0 >> LT) + b % bpr;
@@ -288,32 +299,44 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     for (int k = 0; k < kPer; ++k) {
       const int zr = row0 + k * kRowStep, zc = lane_c;
       const Blk& Q = blk[(zr >> LT) * bpr + (zc >> LT)];
-      zv[k] = __ldg(mcur + (Q.mrow0 + (zr & (T - 1))) * hw + Q.mcol0 + (zc & (T - 1)));
+      const long long off = (long long)(Q.mrow0 + (zr & (T - 1))) * hw + Q.mcol0 + (zc & (T - 1));
+      zv[k] = __ldg(mcur + off);
+      pv[k] = first ? 0.0 : __ldg(mprev + off);
     }
   }
+  // iteration 0: the tile's initial values (constant, or the supplied image at the output pixel)
+  double cv[kPer];
+  if (first) {
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) zs[row0 + k * kRowStep][lane_c] = zv[k];
+    for (int k = 0; k < kPer; ++k)
+      cv[k] = init_kind == FIC_INITIAL_MID_GRAY ? 128.0
+              : init_kind == FIC_INITIAL_BLACK  ? 0.0
+                                                : (double)sup[(long long)(Y0 + row0 + k * kRowStep) * out_w + X0 + lane_c];
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    zs[row0 + k * kRowStep][lane_c] = zv[k];
+    ps[row0 + k * kRowStep][lane_c] = pv[k];
+  }
   __syncthreads();
   double sq = 0.0;
-  // kWhole: the isometry is affine in (row, col), so the thread's z offsets form an
-  // arithmetic sequence over its rows: one base and one stride instead of a per-pixel switch
   int zoff0 = 0, zstep = 0;
-  if (kWhole) {
-    int r00, c00, r10, c10, r01, c01;
+  if (kWhole) {  // the isometry is affine in (row, col): one base and one stride per thread
+    int r00, c00, r10, c10;
     symmetry_source(B.sym, a0 + row0, c0 + lane_c, kn, r00, c00);
     symmetry_source(B.sym, a0 + row0 + 1, c0 + lane_c, kn, r10, c10);
-    (void)r01;
-    (void)c01;
     zoff0 = (r00 - B.sr0) * (kTile + 1) + (c00 - B.sc0);
     zstep = kRowStep * ((r10 - r00) * (kTile + 1) + (c10 - c00));
   }
   const double* zflat = &zs[0][0];
+  const double* pflat = &ps[0][0];
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int orow = row0 + k * kRowStep, ocol = lane_c;
-    double z, s, o;
+    double z, p, s, o;
     if (kWhole) {
       z = zflat[zoff0 + k * zstep];
+      p = pflat[zoff0 + k * zstep];
       s = B.s;
       o = B.o;
     } else {
@@ -322,16 +345,16 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
       int sr, sc;
       symmetry_source(Q.sym, orow & (T - 1), ocol & (T - 1), T, sr, sc);
       z = zs[(bi << LT) + sr][(bj << LT) + sc];
+      p = ps[(bi << LT) + sr][(bj << LT) + sc];
       s = Q.s;
       o = Q.o;
     }
-    const double v = __dadd_rn(__dmul_rn(s, z), o);
-    __stcs(nxt_t + orow * out_w + ocol, v);
+    const double v = __dadd_rn(__dmul_rn(s, z), o);  // decoder.cpp:71-75
+    const double c = first ? cv[k] : __dadd_rn(__dmul_rn(s, p), o);
     vs[orow][ocol] = v;
-    if (partial) {
-      const double dlt = __dsub_rn(cv[k], v);
-      sq = __dadd_rn(sq, __dmul_rn(dlt, dlt));
-    }
+    if (out_u8) out_u8[(long long)(Y0 + orow) * out_w + X0 + ocol] = (unsigned char)lround(clampd(v, 0.0, 255.0));
+    const double dlt = __dsub_rn(c, v);
+    sq = __dadd_rn(sq, __dmul_rn(dlt, dlt));
   }
   __syncthreads();
   {  // the next iteration's means of this tile's outputs: 16 x 16, one per thread
@@ -339,39 +362,40 @@ decode_mean_kernel(const double* __restrict__ cur, const double* __restrict__ mc
     const double m = __dmul_rn(
         __dadd_rn(__dadd_rn(__dadd_rn(vs[2 * i][2 * j], vs[2 * i][2 * j + 1]), vs[2 * i + 1][2 * j]), vs[2 * i + 1][2 * j + 1]),
         0.25);
-    mnxt[(Y0 / 2 + i) * hw + X0 / 2 + j] = m;
+    mnxt[(long long)(Y0 / 2 + i) * hw + X0 / 2 + j] = m;
   }
-  if (partial) {
-    __shared__ double red[kTileThreads / 32];
-    for (int off = 16; off > 0; off >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kTileThreads / 32; ++w) t = __dadd_rn(t, red[w]);
-      partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
-    }
+  __shared__ double red[kTileThreads / 32];
+  for (int off = 16; off > 0; off >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kTileThreads / 32; ++w) t = __dadd_rn(t, red[w]);
+    partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
 }
 
-void launch_mean_raster(const double* r, double* m, int out_w, int out_h, cudaStream_t st) {
+void launch_mean_init(double* m, int out_w, int out_h, int kind, const unsigned char* sup, cudaStream_t st) {
   const long long n = (long long)(out_w / 2) * (out_h / 2);
-  mean_raster_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(r, m, out_w, out_h);
+  mean_init_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(m, out_w, out_h, kind, sup);
 }
 
-// One iteration on the mean raster (decode_mean_ok); partials as decode_partials.
-void launch_decode_mean(const double* cur, const double* mcur, double* nxt, double* mnxt, const RangeXform* xf,
-                        int out_w, int out_h, int kn, int ranges_x, double* partial, cudaStream_t st) {
+// One iteration on the mean rasters (decode_mean_ok); partials as decode_partials.
+void launch_decode_means(const double* mcur, const double* mprev, int init_kind, const unsigned char* sup,
+                         double* mnxt, const RangeXform* xf, int out_w, int out_h, int kn, int ranges_x,
+                         double* partial, unsigned char* out_u8, cudaStream_t st) {
   const dim3 grid(out_w / kTile, out_h / kTile);
-#define FIC_MEAN(LT) decode_mean_kernel<LT><<<grid, kTileThreads, 0, st>>>(cur, mcur, nxt, mnxt, xf, out_w, kn, ranges_x, partial)
+#define FIC_MEANS(LT)                                                                                   \
+  decode_means_kernel<LT><<<grid, kTileThreads, 0, st>>>(mcur, mprev, init_kind, sup, mnxt, xf, out_w, kn, \
+                                                         ranges_x, partial, out_u8)
   switch (kn >= kTile ? 5 : __builtin_ctz((unsigned)kn)) {
-    case 1: FIC_MEAN(1); break;
-    case 2: FIC_MEAN(2); break;
-    case 3: FIC_MEAN(3); break;
-    case 4: FIC_MEAN(4); break;
-    default: FIC_MEAN(5); break;
+    case 1: FIC_MEANS(1); break;
+    case 2: FIC_MEANS(2); break;
+    case 3: FIC_MEANS(3); break;
+    case 4: FIC_MEANS(4); break;
+    default: FIC_MEANS(5); break;
   }
-#undef FIC_MEAN
+#undef FIC_MEANS
 }
 
 // Sums the per-block partials in index order and writes rmse = sqrt(sum / count); block k

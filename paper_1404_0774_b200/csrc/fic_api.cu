@@ -44,9 +44,9 @@ void launch_xform(const fic_mapping*, int, int, const Geometry&, RangeXform*, cu
 void launch_decode_step(const double*, double*, const RangeXform*, int, int, int, int, int, double*, cudaStream_t);
 void launch_rmse_finish(const double*, int, long long, double*, int, cudaStream_t);
 bool decode_mean_ok(int, int, int, bool);
-void launch_mean_raster(const double*, double*, int, int, cudaStream_t);
-void launch_decode_mean(const double*, const double*, double*, double*, const RangeXform*, int, int, int, int,
-                        double*, cudaStream_t);
+void launch_mean_init(double*, int, int, int, const unsigned char*, cudaStream_t);
+void launch_decode_means(const double*, const double*, int, const unsigned char*, double*, const RangeXform*, int,
+                         int, int, int, double*, unsigned char*, cudaStream_t);
 void launch_raster_init(double*, long long, int, const unsigned char*, cudaStream_t);
 void launch_quantize_raster(const double*, long long, unsigned char*, cudaStream_t);
 // scan.cu (tcgen05 path, n in {2, 4, 8})
@@ -237,7 +237,7 @@ struct Workspace {
   bool scan_timed = false;
   double pool_bytes = 0.0;  // > 0: ev4/ev5 bracket a pool build of this many algorithmic bytes
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
-      diag, scratch, mra, mrb, recs, rcounts, pendc, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
+      diag, scratch, mra, mrb, mrc, recs, rcounts, pendc, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
   unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
   unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
@@ -1150,8 +1150,10 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
     const size_t cnt_b = (size_t)std::max<long long>(cnt, 1);
     auto* d_maps = static_cast<fic_mapping*>(ws.out.get((size_t)std::max(1, rx * ry) * sizeof(fic_mapping)));
     auto* xf = static_cast<RangeXform*>(ws.xf.get((size_t)std::max(1, rx * ry) * sizeof(RangeXform)));
-    auto* a = static_cast<double*>(ws.ra.get(cnt_b * 8));
-    auto* b = static_cast<double*>(ws.rb.get(cnt_b * 8));
+    // full-resolution rasters: the per-pixel / tiled paths only (the mean-raster path never
+    // materialises them, decoder.cu)
+    double* a = mean ? nullptr : static_cast<double*>(ws.ra.get(cnt_b * 8));
+    double* b = mean ? nullptr : static_cast<double*>(ws.rb.get(cnt_b * 8));
     // step-RMSE partials of every iteration (reduced once at the end without a convergence test)
     const int slots = has_eps ? 1 : iterations;
     auto* part = static_cast<double*>(ws.partial_sums.get((size_t)nparts * slots * 8));
@@ -1168,12 +1170,15 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
     if (rx * ry > 0)
       CK(cudaMemcpyAsync(d_maps, maps, (size_t)rx * ry * sizeof(fic_mapping), cudaMemcpyHostToDevice, ws.stream));
     const unsigned char* d_sup = nullptr;
-    if (initial_kind == FIC_INITIAL_SUPPLIED) {
-      CK(cudaMemcpyAsync(d_u8, supplied, (size_t)cnt, cudaMemcpyHostToDevice, ws.stream));
-      d_sup = d_u8;
+    if (initial_kind == FIC_INITIAL_SUPPLIED) {  // (its own buffer: the output image is written while it is read)
+      auto* su = static_cast<unsigned char*>(ws.img.get(cnt_b));
+      CK(cudaMemcpyAsync(su, supplied, (size_t)cnt, cudaMemcpyHostToDevice, ws.stream));
+      d_sup = su;
     }
-    launch_raster_init(a, cnt, initial_kind, d_sup, ws.stream);
-    g_launches += 1;
+    if (!mean) {
+      launch_raster_init(a, cnt, initial_kind, d_sup, ws.stream);
+      g_launches += 1;
+    }
     if (rx * ry > 0) {
       launch_xform(d_maps, rx * ry, scale, g, xf, ws.stream);
       g_launches += 1;
@@ -1181,18 +1186,25 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
     const bool timed = g_timing.load() != 0 && !has_eps;
     if (timed) CK(cudaEventRecord(ws.ev0, ws.stream));
     int runs = 0;
-    double *ma = nullptr, *mb = nullptr;
-    if (mean) {
-      ma = static_cast<double*>(ws.mra.get((size_t)cnt / 4 * 8));
-      mb = static_cast<double*>(ws.mrb.get((size_t)cnt / 4 * 8));
-      launch_mean_raster(a, ma, out_w, out_h, ws.stream);
+    double *mprev = nullptr, *mcur = nullptr, *mnxt = nullptr;
+    if (mean) {  // three quarter-size mean rasters: m_{i-1}, m_i, m_{i+1}
+      mcur = static_cast<double*>(ws.mra.get((size_t)cnt / 4 * 8));
+      mnxt = static_cast<double*>(ws.mrb.get((size_t)cnt / 4 * 8));
+      mprev = static_cast<double*>(ws.mrc.get((size_t)cnt / 4 * 8));
+      launch_mean_init(mcur, out_w, out_h, initial_kind, d_sup, ws.stream);
       g_launches += 1;
     }
     for (int it = 0; it < iterations; ++it) {
       double* pt = part + (has_eps ? 0 : (size_t)it * nparts);
       if (mean) {
-        launch_decode_mean(a, ma, b, mb, xf, out_w, out_h, kn, rx, pt, ws.stream);
-        std::swap(ma, mb);
+        // the output image comes from the last iteration run: every one when it may stop early
+        const bool write_u8 = has_eps || it == iterations - 1;
+        launch_decode_means(mcur, it == 0 ? nullptr : mprev, initial_kind, d_sup, mnxt, xf, out_w, out_h, kn, rx, pt,
+                            write_u8 ? d_u8 : nullptr, ws.stream);
+        double* t = mprev;
+        mprev = mcur;
+        mcur = mnxt;
+        mnxt = t;
       } else {
         launch_decode_step(a, b, xf, out_w, out_h, kn, rx, ry, pt, ws.stream);
       }
@@ -1212,8 +1224,10 @@ int32_t fic_decode(const fic_mapping* maps, int32_t width, int32_t height, const
       g_launches += 1;
     }
     if (timed) CK(cudaEventRecord(ws.ev1, ws.stream));
-    launch_quantize_raster(a, cnt, d_u8, ws.stream);
-    g_launches += 1;
+    if (!mean) {  // (the mean-raster path wrote the quantised image in its last iteration)
+      launch_quantize_raster(a, cnt, d_u8, ws.stream);
+      g_launches += 1;
+    }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h_rmse, d_rmse, (size_t)runs * 8, cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaMemcpyAsync(out, d_u8, (size_t)cnt, cudaMemcpyDeviceToHost, ws.stream));
