@@ -66,6 +66,7 @@ cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const _
                         unsigned long long*, const unsigned short*, const DomainMetaI*, unsigned long long*, void*,
                         const double*, bool, cudaStream_t);
 bool scan_fused();
+int scan_level_launches(const Geometry&, int, int, bool);
 size_t scan_rec_bytes(unsigned long long, int);
 int scan_trace_copy(long long*, int);
 int scan_padded_ranges(const Geometry&);
@@ -409,14 +410,12 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
     CK(cudaEventRecord(ws.ev3, st));
     ws.scan_timed = true;
   }
-  if (fused) {  // the scan evaluated its survivors itself
-    g_launches += 2;  // level ops, scan
-    return;
-  }
+  g_launches += 1 + scan_level_launches(g, stride, ws.sms, fused);  // level ops, scan (+ expand)
+  if (fused) return;  // the scan evaluated its survivors itself
   const bool inl = eval_inline();
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
               pendc, b.win, inl, ws.sms, st);
-  g_launches += inl ? 4 : 5;  // level ops, scan, expand, evaluation (+ residuals)
+  g_launches += inl ? 1 : 2;  // evaluation (+ residuals)
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a
@@ -460,8 +459,12 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
     const double Dt = (double)g.Dt * g.batch;
     ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0) + (double)g.R * (g.N + 40.0);
   }
-  const char* seed_env = std::getenv("FIC_SEED");  // "0": no local seed (A/B)
-  const bool seed = !(seed_env && std::strcmp(seed_env, "0") == 0);
+  // The local seed gives the first scan level a bar.  Small pools (<= 1024 tiles) start with a
+  // per-lane-best sparse level that keeps nearly every lane's best column whatever the bar, so
+  // the seed is skipped there (cfg2 0.341 vs 0.347 ms, cfg3 2.455 vs 2.468 ms); large pools keep
+  // it (cfg4 63.7 vs 64.3 ms).  FIC_SEED=0 / 1 forces it off / on.
+  const char* seed_env = std::getenv("FIC_SEED");
+  const bool seed = seed_env ? std::strcmp(seed_env, "0") != 0 : scan_tiles(g) > 1024;
   if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
   g_launches += seed ? 2 : 1;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));

@@ -2079,9 +2079,16 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   kern<<<grid, fused ? kFusedThreads : kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts,
                                                                     rcap, list, part, counts, ev);
   e = cudaGetLastError();
-  if (e != cudaSuccess || fused) return e;
+  // sparse levels append their selected entries directly (no mask records to expand)
+  if (e != cudaSuccess || fused || lv.select != 0) return e;
   expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
   return cudaGetLastError();
+}
+
+// Kernels launch_scan enqueues for a level: the scan, plus expand_kernel where the level writes
+// mask records (full level, separate evaluation).
+int scan_level_launches(const Geometry& g, int stride, int sms, bool fused) {
+  return 1 + (!fused && make_level(g, stride, scan_grid(g, stride, sms)).select == 0 ? 1 : 0);
 }
 
 // Full level with an fp16 accumulator: large pools (the whole-tile vote mode, where the
