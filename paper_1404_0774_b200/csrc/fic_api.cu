@@ -57,7 +57,7 @@ void launch_pool_v3(const unsigned char*, const Geometry&, __half*, unsigned sho
                     unsigned long long*, RangeMeta*, unsigned long long*, void*, double*, cudaStream_t);
 void launch_fill_u64(unsigned long long*, long long, unsigned long long, cudaStream_t);
 void launch_seed_v3(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
-                    const RangeMeta*, unsigned long long*, const double*, cudaStream_t);
+                    const RangeMeta*, unsigned long long*, const double*, int, cudaStream_t);
 size_t deq_table_entries(const Geometry&);
 void launch_deq_tables(const Geometry&, double*, cudaStream_t);
 int scan_grid(const Geometry&, int, int);
@@ -83,7 +83,7 @@ void launch_winner(const uint2*, const unsigned long long*, int, unsigned long l
                    const unsigned long long*, void*, int, cudaStream_t);
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
                    const RangeMeta*, const void*, const unsigned long long*, fic_mapping*, unsigned long long*,
-                   cudaStream_t);
+                   const unsigned long long*, int, unsigned long long*, cudaStream_t);
 void launch_probe_corr(const unsigned char*, const Geometry&, const unsigned short*, int, const int*, const int*,
                        const int*, long long*, cudaStream_t);
 }  // namespace ficb
@@ -307,9 +307,14 @@ int matcher_mode(const Geometry& g) {
 
 constexpr int kMaxLevels = 6;
 constexpr int kPartSlots = 256;      // per-level survivor counters, one per scan CTA (<= SMs)
-constexpr int kScanCountSlots = kMaxLevels * kPartSlots + 2;  // + record self-check failures, pending count
+// per-level survivor counters, then one status block the host reads back after every encode:
+// record self-check failures, the pending count, the largest full-level partition (computed on
+// the device) and the flat / shadow counters of each slice (up to 64 slices per pass)
 constexpr int kSelfcheckSlot = kMaxLevels * kPartSlots;
 constexpr int kPendSlot = kSelfcheckSlot + 1;
+constexpr int kNeedSlot = kPendSlot + 1;
+constexpr int kCounterSlot = kNeedSlot + 1;
+constexpr int kScanCountSlots = kCounterSlot + 2 * 64;
 
 // Scan levels: sparse passes over every 8^k-th (or 4 * 8^k-th) 128-domain tile seed the
 // pruning bar, then the full scan.  Each level prunes with the bar the previous
@@ -432,7 +437,8 @@ void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g,
                   static_cast<double*>(ws.res.p), b.gbest, b.win, ws.sms, st);
     g_launches += 1;
   }
-  launch_record(d_img, g, b.qpool, b.mi, b.rm, b.win, b.gbest, d_out, b.cnt + kSelfcheckSlot, st);
+  launch_record(d_img, g, b.qpool, b.mi, b.rm, b.win, b.gbest, d_out, b.cnt + kSelfcheckSlot, cnt, parts,
+                b.cnt + kNeedSlot, st);
   g_launches += 1;
   CK(cudaGetLastError());
 }
@@ -459,13 +465,16 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
     const double Dt = (double)g.Dt * g.batch;
     ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0) + (double)g.R * (g.N + 40.0);
   }
-  // The local seed gives the first scan level a bar.  Small pools (<= 1024 tiles) start with a
-  // per-lane-best sparse level that keeps nearly every lane's best column whatever the bar, so
-  // the seed is skipped there (cfg2 0.341 vs 0.347 ms, cfg3 2.455 vs 2.468 ms); large pools keep
-  // it (cfg4 63.7 vs 64.3 ms).  FIC_SEED=0 / 1 forces it off / on.
+  // The local seed gives the first scan level a bar (upper bounds of the range's 3 x 3 local
+  // self-similar candidates) for large pools.  Small pools (<= 1024 tiles) start with a
+  // per-lane-best selection level that keeps nearly every lane's best column whatever the bar,
+  // so they skip it: cfg2 0.335 / 0.337 / 0.344 ms without / with a 1 x 1 / 3 x 3 seed, cfg3
+  // 2.456 / 2.447 / 2.462 ms (within noise), one launch fewer.  FIC_SEED=0 / 1 / 3 forces none /
+  // 1 x 1 / 3 x 3.
   const char* seed_env = std::getenv("FIC_SEED");
-  const bool seed = seed_env ? std::strcmp(seed_env, "0") != 0 : scan_tiles(g) > 1024;
-  if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, st);
+  const int seed_side = seed_env ? std::atoi(seed_env) : (scan_tiles(g) > 1024 ? 3 : 0);
+  const bool seed = seed_side > 0;
+  if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, seed_side >= 3 ? 1 : 0, st);
   g_launches += seed ? 2 : 1;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
   const std::vector<int> lv = scan_levels(g);
@@ -612,7 +621,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
   // h_out: the records are also copied to this (pinned) host buffer before the one synchronisation
   // (again after an overflow re-run), so a host-API encode waits for the device once
   Geometry g = g_in;
-  if (g.Dt == 0) g.Dt = (int)scan_pool_domains(g);  // per-slice pool stride (a multiple of 896)
+  if (g.Dt == 0) g.Dt = (int)scan_pool_domains(g);  // per-slice pool stride (a multiple of the pool block)
   if (matcher_mode(g) == 0) {
     if (g.batch != 1) throw InternalFail{"batched encode needs the tcgen05 scan path"};
     enqueue_encode_simt(ws, d_img, g, d_out, d_counters, st);
@@ -625,18 +634,25 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
   const ScanBufs b = scan_bufs(ws, g);
   const size_t nl = scan_levels(g).size();
   auto* hc = static_cast<unsigned long long*>(ws.h_scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
+  if (g.batch > 64) throw InternalFail{"more than 64 slices in one encode pass"};
+  d_counters = b.cnt + kCounterSlot;  // flat / shadow counters live in the status block
   enqueue_encode_graph(ws, d_img, g, b, d_out, d_counters, st);
+  // every level's partition counters only for the survivor statistics (timed / diagnostic encodes)
+  const bool all_counts = g_timing.load() != 0 || (g.flags & 4);
   for (int attempt = 0;; ++attempt) {
-    CK(cudaMemcpyAsync(hc, b.cnt, kScanCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    if (h_counters)
-      CK(cudaMemcpyAsync(h_counters, d_counters, 2 * g.batch * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                         st));
+    // one read-back of the status block (and the records of a host-API encode), one synchronisation
+    if (all_counts)
+      CK(cudaMemcpyAsync(hc, b.cnt, kScanCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    else
+      CK(cudaMemcpyAsync(hc + kSelfcheckSlot, b.cnt + kSelfcheckSlot,
+                         (kCounterSlot - kSelfcheckSlot + 2 * g.batch) * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, st));
     if (h_out) CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (h_counters) std::memcpy(h_counters, hc + kCounterSlot, 2 * g.batch * sizeof(unsigned long long));
     const std::vector<int> lv = scan_levels(g);
     const int fparts = scan_grid(g, 1, ws.sms);
-    unsigned long long need = 0;  // largest partition of the full level
-    for (int c = 0; c < fparts; ++c) need = std::max(need, hc[(nl - 1) * kPartSlots + c]);
+    const unsigned long long need = hc[kNeedSlot];  // largest partition of the full level (record_kernel)
     if (g.flags & 4) {
       std::fprintf(stderr, "[fic diag] scan R=%d D=%d tiles=%d levels", g.R, g.D, scan_tiles(g));
       for (size_t l = 0; l < nl; ++l) {
@@ -650,7 +666,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
       }
       std::fprintf(stderr, " part %llu selfcheck %llu\n", ws.list_cap / fparts, hc[kSelfcheckSlot]);
     }
-    {
+    if (all_counts) {
       std::vector<unsigned long long> surv(nl, 0);
       for (size_t l = 0; l < nl; ++l) {
         const int parts = scan_grid(g, lv[l], ws.sms);

@@ -560,15 +560,16 @@ __device__ __forceinline__ double load_bar(const unsigned long long* gbest, int 
 // Exact evaluation of the 8 isometries of the (2h+1)^2 grid domains around each range's own
 // 2x-scaled neighbourhood (self-similar candidates that usually fit well) to give the
 // first scan level a bar.  One thread per (range, local domain, isometry).
-constexpr int kSeedHalf = 1;
-constexpr int kSeedSide = 2 * kSeedHalf + 1;
-constexpr int kSeedPerRange = kSeedSide * kSeedSide * kSyms;
 
-template <int NN>
+
+// HALF: the (2 HALF + 1)^2 local domains (small pools: HALF = 0, only the range's own 2x-scaled
+// neighbourhood; large pools: HALF = 1).
+template <int NN, int HALF>
 __global__ void __launch_bounds__(128)
 seed_v3_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
                const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
                unsigned long long* __restrict__ gbest, DeqTables tab) {
+  constexpr int kSeedHalf = HALF, kSeedSide = 2 * HALF + 1, kSeedPerRange = kSeedSide * kSeedSide * kSyms;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = tid < (long long)g.R * kSeedPerRange && g.D > 0;
   const int r = in ? (int)(tid / kSeedPerRange) : -1, k = (int)(tid % kSeedPerRange);
@@ -1840,7 +1841,14 @@ __global__ void __launch_bounds__(128)
 record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
               const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
               const unsigned __int128* __restrict__ win, const unsigned long long* __restrict__ gbest,
-              fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck) {
+              fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck,
+              const unsigned long long* __restrict__ full_counts, int parts, unsigned long long* __restrict__ need) {
+  // the largest full-level list partition, for the host's overflow check (one status read-back)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long m = 0;
+    for (int c = 0; c < parts; ++c) m = max(m, full_counts[c]);
+    *need = m;
+  }
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= g.R) return;
   const RangeMeta m = rmeta[r];
@@ -1961,13 +1969,20 @@ void launch_deq_tables(const Geometry& g, double* deq, cudaStream_t st) {
 
 void launch_seed_v3(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
                     const DomainMetaI* meta_i, const RangeMeta* rmeta, unsigned long long* gbest, const double* deq,
-                    cudaStream_t st) {
-  const long long threads = (long long)g.R * kSeedPerRange;
+                    int half, cudaStream_t st) {
+  const int per = (2 * half + 1) * (2 * half + 1) * kSyms;
+  const long long threads = (long long)g.R * per;
   const int blocks = (int)((threads + 127) / 128);
   const DeqTables tab{deq, deq + (1 << g.s_bits)};
-  if (g.N == 4) seed_v3_kernel<4><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
-  else if (g.N == 16) seed_v3_kernel<16><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
-  else seed_v3_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab);
+#define FIC_SEED(NN, H) seed_v3_kernel<NN, H><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, gbest, tab)
+  if (g.N == 4) {
+    if (half) FIC_SEED(4, 1); else FIC_SEED(4, 0);
+  } else if (g.N == 16) {
+    if (half) FIC_SEED(16, 1); else FIC_SEED(16, 0);
+  } else {
+    if (half) FIC_SEED(64, 1); else FIC_SEED(64, 0);
+  }
+#undef FIC_SEED
 }
 
 // Scan CTAs (= list partitions) of a level: one per SM.
@@ -2175,12 +2190,16 @@ void launch_winner(const SurvEntry* list, const unsigned long long* counts, int 
 
 void launch_record(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
                    const DomainMetaI* meta_i, const RangeMeta* rmeta, const void* win_,
-                   const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck, cudaStream_t st) {
+                   const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck,
+                   const unsigned long long* full_counts, int parts, unsigned long long* need, cudaStream_t st) {
   const int blocks = (g.R + 127) / 128;
   const unsigned __int128* win = static_cast<const unsigned __int128*>(win_);
-  if (g.N == 4) record_kernel<4><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
-  else if (g.N == 16) record_kernel<16><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
-  else record_kernel<64><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck);
+#define FIC_REC(NN) \
+  record_kernel<NN><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, need)
+  if (g.N == 4) FIC_REC(4);
+  else if (g.N == 16) FIC_REC(16);
+  else FIC_REC(64);
+#undef FIC_REC
 }
 
 }  // namespace ficb
