@@ -77,7 +77,7 @@ void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, c
                       unsigned char*, unsigned long long*, bool, unsigned long long*, cudaStream_t);
 void launch_eval(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*, const RangeMeta*,
                  const uint2*, const unsigned long long*, int, unsigned long long, double*, unsigned long long*,
-                 const double*, uint2*, unsigned*, void*, bool, int, cudaStream_t);
+                 const double*, uint2*, unsigned*, void*, bool, bool, int, cudaStream_t);
 bool eval_inline();
 void launch_winner(const uint2*, const unsigned long long*, int, unsigned long long, const double*,
                    const unsigned long long*, void*, int, cudaStream_t);
@@ -418,9 +418,12 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   g_launches += 1 + scan_level_launches(g, stride, ws.sms, fused);  // level ops, scan (+ expand)
   if (fused) return;  // the scan evaluated its survivors itself
   const bool inl = eval_inline();
+  // sparse levels only lower the bar: closed-form upper bounds (FIC_SPARSE_EXACT=1: exact residuals)
+  const char* se = std::getenv("FIC_SPARSE_EXACT");
+  const bool bar_only = !final_level && !(se && se[0] == '1');
   launch_eval(d_img, g, b.qpool, b.mi, b.rm, list, cnt, parts, part, res, b.gbest, b.deq, pend,
-              pendc, b.win, inl, ws.sms, st);
-  g_launches += inl ? 1 : 2;  // evaluation (+ residuals)
+              pendc, b.win, inl, bar_only, ws.sms, st);
+  g_launches += inl || bar_only ? 1 : 2;  // evaluation (+ residuals)
 }
 
 // The full level plus winner selection and records.  Its list must be complete; a
@@ -548,7 +551,8 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
   for (const void* q : ptrs) k.push_back((unsigned long long)(uintptr_t)q);
   k.push_back(ws.list_cap);
   for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED",
-                           "FIC_LANEBEST_MAX", "FIC_F16ACC", "FIC_F16SEL", "FIC_FUSED", "FIC_EVAL_SPLIT"}) {
+                           "FIC_LANEBEST_MAX", "FIC_F16ACC", "FIC_F16SEL", "FIC_FUSED", "FIC_EVAL_SPLIT",
+                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;

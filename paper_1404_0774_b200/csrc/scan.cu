@@ -487,10 +487,13 @@ __device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* q
     const double var_a = den_d * 0.0625 * inv_count;
     const double parabola = ssb - 2.0 * s_deq * cov + s_deq * s_deq * var_a;
     if (screens && parabola >= thr + (1e-3 - 1e-9)) return inf;
+    // o = clamp((Sb - s Sa) / N): the same rounded operations as the reference (the division by
+    // N = 2^k is exact), so the clamp decides identically; a clamped o = +-255 quantises to the
+    // top code / code 1 away from any rounding boundary (safe_code checks every other case)
     const double o = fmin(fmax((sb_d - sc * sa_d) * inv_count, -255.0), 255.0);
     if (fabs(o) < 1e-9) goto exact;  // quantize(0) is the special code 0
     const int c = safe_code((o + 255.0) * (1.0 / 510.0) * (double)mo);
-    if (c < 0 || fabs(fabs(o) - 255.0) < 1e-9) goto exact;
+    if (c < 0) goto exact;
     const unsigned qo = c < 1 ? 1u : (c > (int)mo ? mo : (unsigned)c);
     const double o_deq = tab.o[qo];
     const double o_gap = o_deq - (sb_d - s_deq * sa_d) * inv_count;
@@ -698,6 +701,7 @@ struct ScanLevel {
   int k;          // chunks per leftover m-tile
   int select;     // sparse levels: 1, 2 each range's best column per warp and tile (2: small pools), 3 per lane and segment
   int coarse;     // 1: whole-tile |max| vote before the per-range test (large pools: rare hits)
+  int lanes_per_best;  // select == 3: lanes sharing one best entry per range (1, 2 or 4)
 };
 
 struct Segment {
@@ -1559,11 +1563,19 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           }
         }
       }
-      if constexpr (MB == 4) {  // flush the segment's per-lane bests: one entry per lane and range
+      if constexpr (MB == 4) {  // flush the segment's per-lane bests: one entry per lane group and range
+        // lv.lanes_per_best consecutive lanes (1, 2, 4) share one entry: the group's largest key
+        // (ties: the lowest lane) — fewer exact evaluations for a slightly weaker bar
 #pragma unroll
         for (int k = 0; k < kEpiRanges; ++k) {
           const uint32_t b = lbest[k];
-          const bool keep = b != 0u && (__uint_as_float(b) > 1.0f || ((allpass >> k) & 1u));
+          bool win_lane = true;
+          for (int o = 1; o < lv.lanes_per_best; o <<= 1) {
+            const uint32_t ob = __shfl_xor_sync(0xffffffffu, b, o);
+            const bool lower = (lane & o) == 0;
+            if (ob > b || (ob == b && !lower)) win_lane = false;
+          }
+          const bool keep = win_lane && b != 0u && (__uint_as_float(b) > 1.0f || ((allpass >> k) & 1u));
           const uint32_t bal = __ballot_sync(0xffffffffu, keep);
           if (!bal) continue;
           ech.reserve((uint32_t)__popc(bal));
@@ -1705,10 +1717,13 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
             const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
             unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab,
             uint2* __restrict__ pend, unsigned* __restrict__ pend_counts, unsigned long long seg,
-            unsigned __int128* __restrict__ win) {
+            unsigned __int128* __restrict__ win, int bar_only) {
   // pend == nullptr: every candidate's residual is computed here from the operands in registers
   // and the (residual, domain * 8 + isometry) minimum is kept per range in `win` (no residual
-  // and winner passes); else the candidates that pass every screen go to the pending list
+  // and winner passes); else the candidates that pass every screen go to the pending list.
+  // bar_only (sparse levels, which only have to lower the bar): a rigorous closed-form upper
+  // bound of each candidate's exact residual is published instead of the residual itself (no
+  // residual loop); the full level evaluates every candidate below that bar exactly
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const bool screens = !(g.flags & 2);
   const int lane = threadIdx.x & 31;
@@ -1747,10 +1762,10 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
         load_q8_row<NN>(qpool, d, s, qw);
         load_range_words<NN>(img, g, x0, y0, bpk);
         if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
-          R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar, screens, false, tab,
-                            qpool, img, d, s, x0, y0, qs, qo, pend ? &pending : nullptr);
+          R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar, screens,
+                            bar_only != 0, tab, qpool, img, d, s, x0, y0, qs, qo, pend ? &pending : nullptr);
           if (R < inf) {
-            if (pend) {
+            if (pend || bar_only) {
               publish_best(gbest, r, R);
             } else if (R <= bar) {
               // only a residual at or below the bar read above can lower it or be the final
@@ -2011,6 +2026,11 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
     const char* e = std::getenv("FIC_COARSE");  // "0" / "1": force the whole-tile vote off / on (A/B)
     lv.coarse = e ? (std::strcmp(e, "0") != 0) : (n_tiles > 1024 ? 1 : 0);
   }
+  {
+    const char* e = std::getenv("FIC_LANE_GROUP");  // lanes per best entry at per-lane-best levels
+    const int lg = e ? std::atoi(e) : 1;
+    lv.lanes_per_best = lg >= 4 ? 4 : (lg >= 2 ? 2 : 1);
+  }
   lv.n_lvl = (n_tiles + stride - 1) / stride;
   lv.m_tiles = (g.R + kScanRanges - 1) / kScanRanges;
   lv.rounds = lv.m_tiles / G;
@@ -2154,17 +2174,17 @@ unsigned long long eval_pend_seg(unsigned long long part) {
 void launch_eval(const unsigned char* img, const Geometry& g, const unsigned short* qpool, const DomainMetaI* meta_i,
                  const RangeMeta* rmeta, const SurvEntry* list, const unsigned long long* counts, int parts,
                  unsigned long long part, double* res, unsigned long long* gbest, const double* deq, uint2* pend,
-                 unsigned* pend_counts, void* win_, bool inline_res, int sms, cudaStream_t st) {
+                 unsigned* pend_counts, void* win_, bool inline_res, bool bar_only, int sms, cudaStream_t st) {
   (void)sms;
   const int blocks = parts * kEvalPer;
   const unsigned long long seg = eval_pend_seg(part);
   const DeqTables tab{deq, deq + (1 << g.s_bits)};
   unsigned __int128* win = static_cast<unsigned __int128*>(win_);
-  uint2* pd = inline_res ? nullptr : pend;
+  uint2* pd = inline_res || bar_only ? nullptr : pend;
 #define FIC_EVAL(NN)                                                                                                 \
   eval_kernel<NN><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab, \
-                                          pd, pend_counts, seg, win);                                                \
-  if (!inline_res)                                                                                                   \
+                                          pd, pend_counts, seg, win, bar_only ? 1 : 0);                              \
+  if (pd)                                                                                                            \
     residual_kernel<NN><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
   if (g.N == 4) {
     FIC_EVAL(4)

@@ -448,7 +448,8 @@ def test_fused_and_separate_evaluation(oracle, fused):
              (images.ct_slice(256, 1404002, 0.3), dict(n=8, step=4)), (oracle.noise_image(64, 11), dict(n=2, step=1))]
     for img, pv in cases:
         want, st = oracle.encode(img, pv)
-        for extra in (dict(), dict(FIC_LIST_CAP=3000), dict(FIC_DEBUG=1), dict(FIC_SEED=1), dict(FIC_EVAL_SPLIT=1)):
+        for extra in (dict(), dict(FIC_LIST_CAP=3000), dict(FIC_DEBUG=1), dict(FIC_SEED=1), dict(FIC_EVAL_SPLIT=1),
+                      dict(FIC_SPARSE_EXACT=1)):
             with env(FIC_FUSED=fused, **extra):
                 enc = fic.encode(img, fic.CodecParams(**pv))
             assert_same(enc.mappings, want, f"fused={fused} {extra} {pv}")
