@@ -745,24 +745,33 @@ __host__ __device__ __forceinline__ bool scan_f16acc(const Geometry& g) { return
 // Range operand of m-tile `mt` into `sR` (threads [tid, tid + nthreads)): row
 // rl * 8 + s holds the centred range rl permuted by isometry s's inverse and scaled,
 // R[row][j] = (b[i] - Sb/N) / T_r with perm_s(i) = j, so sum_j u_j R[row][j] = X / T_r.
-// (chunk c of the m-tile's operand: row = c / (K/8), k-chunk kc = c % (K/8); s_pix holds the
-// m-tile's 32 ranges' pixels, s_perm[s][j] the pixel index i with perm_s(i) = j)
-__device__ __forceinline__ void build_range_chunks(unsigned char* sR, const Geometry& g, const unsigned char* s_pix,
-                                                   const unsigned char* s_perm, const float* s_mean,
-                                                   const float* s_scale, int tid, int nthreads, int c0, int c1) {
-  const int K = g.K, N = g.N;
-  for (int c = c0 + tid; c < c1; c += nthreads) {
+__device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict__ img, const Geometry& g,
+                             const RangeMeta* __restrict__ rmeta, const float* __restrict__ thr, int mt, int tid,
+                             int nthreads, int chunks) {
+  const int K = g.K, N = g.N, n = g.n;
+  for (int c = tid; c < chunks; c += nthreads) {
     const int row = c / (K / 8), kc = c % (K / 8);
     const int rl = row >> 3, s = row & 7;
+    const int r = mt * kScanRanges + rl;
     const int sinv = s == 1 ? 3 : (s == 3 ? 1 : s);  // inverse isometries: 1 <-> 3, the others are involutions
-    const float mean = s_mean[rl], scale = s_scale[rl];
     uint32_t w[4] = {0, 0, 0, 0};
+    if (r < g.R) {
+      int x0, y0;
+      range_origin(g, r, x0, y0);
+      const float mean = (float)rmeta[r].sb / (float)N;  // exact: N is a power of two
+      float scale = range_scale(thr[r]);
+      // a range without a usable bar keeps every column at the full level; at sparse levels its
+      // columns are the normalised correlations, so the selection there still picks the best
+      if (range_allpass(thr[r])) scale = rsqrtf((float)rmeta[r].var / (float)N + 1.0f);
 #pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      const int j = kc * 8 + h;
-      if (j < N) {
-        const float v = ((float)s_pix[rl * N + s_perm[sinv * N + j]] - mean) * scale;
-        w[h >> 1] |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * (h & 1));
+      for (int h = 0; h < 8; ++h) {
+        const int j = kc * 8 + h;
+        if (j < N) {
+          int ir, ic;
+          symmetry_source(sinv, j / n, j % n, n, ir, ic);  // i with perm_s(i) = j
+          const float v = ((float)img[(long long)(y0 + ir) * g.W + x0 + ic] - mean) * scale;
+          w[h >> 1] |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * (h & 1));
+        }
       }
     }
     *reinterpret_cast<uint4*>(sR + (row >> 3) * K * 16 + kc * 128 + (row & 7) * 16) =
@@ -804,53 +813,22 @@ range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMe
                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr,
                 unsigned char* __restrict__ ropnd, unsigned long long* __restrict__ pend_count, int full_level,
                 unsigned long long* __restrict__ selfcheck) {
-  __shared__ float s_mean[kScanRanges], s_scale[kScanRanges];
-  __shared__ __align__(16) unsigned char s_pix[kScanRanges * 64];  // the m-tile's range pixels
-  __shared__ unsigned char s_perm[kSyms * 64];
-  const int N = g.N, n = g.n;
+  __shared__ float s_thr[kScanRanges];
   if (threadIdx.x < kScanRanges) {
     const int r = blockIdx.x * kScanRanges + threadIdx.x;
     const float t = range_threshold(g, rmeta, gbest, r, full_level && scan_f16acc(g));
+    s_thr[threadIdx.x] = t;
     if (blockIdx.y == 0) thr[r] = t;
-    float mean = 0.f, scale = 0.f;
-    if (r < g.R) {
-      const RangeMeta m = rmeta[r];
-      mean = (float)m.sb / (float)N;  // exact: N is a power of two
-      scale = range_scale(t);
-      // a range without a usable bar keeps every column at the full level; at sparse levels its
-      // columns are the normalised correlations, so the selection there still picks the best
-      if (range_allpass(t)) scale = rsqrtf((float)m.var / (float)N + 1.0f);
-    }
-    s_mean[threadIdx.x] = mean;
-    s_scale[threadIdx.x] = scale;
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     *pend_count = 0;
     if (selfcheck) *selfcheck = 0;
   }
-  // the m-tile's pixels, range-major (row-contiguous loads), and the isometry index tables
-  for (int k = threadIdx.x; k < kScanRanges * N; k += blockDim.x) {
-    const int rl = k / N, i = k % N;
-    const int r = blockIdx.x * kScanRanges + rl;
-    unsigned char v = 0;
-    if (r < g.R) {
-      int x0, y0;
-      range_origin(g, r, x0, y0);
-      v = img[(long long)(y0 + i / n) * g.W + x0 + i % n];
-    }
-    s_pix[k] = v;
-  }
-  for (int k = threadIdx.x; k < kSyms * N; k += blockDim.x) {
-    const int s = k / N, j = k % N;
-    int ir, ic;
-    symmetry_source(s, j / n, j % n, n, ir, ic);  // with the inverse isometry: i with perm_s(i) = j
-    s_perm[k] = (unsigned char)(ir * n + ic);
-  }
   __syncthreads();
   // blockIdx.y splits the m-tile's 256 x K/8 chunks over several CTAs
   const int per = kScanRows * (g.K / 8) / gridDim.y;
-  build_range_chunks(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, g, s_pix, s_perm, s_mean, s_scale,
-                     threadIdx.x, blockDim.x, blockIdx.y * per, blockIdx.y * per + per);
+  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, s_thr - blockIdx.x * kScanRanges,
+               blockIdx.x, blockIdx.y * per + threadIdx.x, blockDim.x, blockIdx.y * per + per);
 }
 
 // Survivor appender of one warp: entries go straight to the CTA's list partition, into
