@@ -2016,8 +2016,11 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
     const int n_lvl = (n_tiles + stride - 1) / stride;
     const char* lb = std::getenv("FIC_LANEBEST_MAX");  // longest level (tiles) using per-lane bests
     const int lane_best_max = lb ? std::atoi(lb) : 48;
+    // per-lane bests only for a short last sparse level of a small pool (cfg2: stride 4, 31
+    // tiles); every other sparse level selects hit-first (cfg3, levels {32, 4}: 2.343 ms vs
+    // 2.411 with per-lane bests at stride 32 and the all-packed selection at stride 4)
     lv.select = stride > 1 && !(e && std::strcmp(e, "0") == 0)
-                    ? (n_tiles <= 1024 ? (n_lvl <= lane_best_max ? 3 : 2) : 1)
+                    ? (n_tiles <= 1024 && stride <= 4 && n_lvl <= lane_best_max ? 3 : 1)
                     : 0;
     if (stride > 1 && e && e[0] >= '1' && e[0] <= '3' && (e[0] != '3' || n_lvl < 8192))
       lv.select = e[0] - '0';  // "1" / "2" / "3": force a selection mode (A/B)

@@ -1,0 +1,15 @@
+mkdir -p gpurun_out
+run() { c=$1; shift; env "$@" timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/v2_sc.json 2>&1
+  python -c "import json; d=json.loads(open('gpurun_out/v2_sc.json').read().strip().splitlines()[-1]); print('$c $*', round(d['ms_per_step'],4), d['survivors_per_level'])"; }
+run cfg3 FIC_X=0
+run cfg3 FIC_LANEBEST_MAX=128
+run cfg3 FIC_LEVELS=32,8
+run cfg3 FIC_LEVELS=64,8
+run cfg3 FIC_LEVELS=16
+run cfg3 FIC_LEVELS=8
+run cfg3 FIC_LEVELS=32,4 FIC_SELECT=1
+run cfg3 FIC_LEVELS=16,2 FIC_LANEBEST_MAX=256
+run cfg2 FIC_X=0
+run cfg2 FIC_LEVELS=8
+run cfg2 FIC_LEVELS=2 FIC_LANEBEST_MAX=128
+run cfg2 FIC_LEVELS=16,4
