@@ -149,6 +149,26 @@ __host__ __device__ __forceinline__ void symmetry_source(int s, int r, int c, in
   }
 }
 
+// symmetry_source as an affine map: sr = R_r r + R_c c + R_m m, sc = C_r r + C_c c + C_m m with
+// m = side - 1 and coefficients in {-1, 0, 1} packed 2 bits each (value + 1) per isometry:
+// bits [0,2) R_r, [2,4) R_c, [4,6) R_m, [6,8) C_r, [8,10) C_c, [10,12) C_m.  No branches: one
+// table word per isometry (warp-uniform in the decoder's whole-tile blocks).
+__host__ __device__ __forceinline__ unsigned symmetry_affine_word(int s) {
+  // (R_r, R_c, R_m; C_r, C_c, C_m) of transforms.cpp:13-26
+  constexpr unsigned k[8] = {
+      (2u << 0) | (1u << 2) | (1u << 4) | (1u << 6) | (2u << 8) | (1u << 10),  // 0 (r, c)
+      (1u << 0) | (0u << 2) | (2u << 4) | (2u << 6) | (1u << 8) | (1u << 10),  // 1 (m - c, r)
+      (0u << 0) | (1u << 2) | (2u << 4) | (1u << 6) | (0u << 8) | (2u << 10),  // 2 (m - r, m - c)
+      (1u << 0) | (2u << 2) | (1u << 4) | (0u << 6) | (1u << 8) | (2u << 10),  // 3 (c, m - r)
+      (2u << 0) | (1u << 2) | (1u << 4) | (1u << 6) | (0u << 8) | (2u << 10),  // 4 (r, m - c)
+      (0u << 0) | (1u << 2) | (2u << 4) | (1u << 6) | (2u << 8) | (1u << 10),  // 5 (m - r, c)
+      (1u << 0) | (2u << 2) | (1u << 4) | (2u << 6) | (1u << 8) | (1u << 10),  // 6 (c, r)
+      (1u << 0) | (0u << 2) | (2u << 4) | (0u << 6) | (1u << 8) | (2u << 10),  // 7 (m - c, m - r)
+  };
+  return k[s & 7];
+}
+__host__ __device__ __forceinline__ int affine_coef(unsigned w, int field) { return (int)((w >> (2 * field)) & 3u) - 1; }
+
 // Byte offset of element (sym s, k) of domain d inside the fp16 operand pool.  Each
 // domain is one K-major, no-swizzle UMMA block of 8 rows (its isometries) by K
 // columns: [K/8 core matrices][8 rows][8 fp16] = K*16 bytes, so a tile of

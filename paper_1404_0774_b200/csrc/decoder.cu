@@ -210,6 +210,8 @@ decode_tile_kernel(const double* __restrict__ cur, double* __restrict__ nxt, con
 // written — three quarter-size rasters, L2-resident up to 4096^2 outputs (3 x 33.5 MB) — instead
 // of an 8 B raster write and an 8 B raster read in HBM.  Every raster value, the output image
 // and each step's sum of squared differences are those of the per-pixel kernel.
+constexpr int kMeanThreads = 128;  // 8 output pixels per thread: the per-tile setup amortised over more work
+
 bool decode_mean_ok(int out_w, int out_h, int kn, bool even_origins) {
   return decode_tiled(out_w, out_h, kn) && even_origins;
 }
@@ -235,7 +237,7 @@ __global__ void mean_init_kernel(double* __restrict__ m, int out_w, int out_h, i
 // masks.  mprev == nullptr: iteration 0, the current values come from the initial raster
 // (init_kind, sup); out_u8 != nullptr: also write the quantised image of this iteration's output.
 template <int LT>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kMeanThreads)
 decode_means_kernel(const double* __restrict__ mcur, const double* __restrict__ mprev, int init_kind,
                     const unsigned char* __restrict__ sup, double* __restrict__ mnxt,
                     const RangeXform* __restrict__ xf, int out_w, int kn, int ranges_x,
@@ -254,27 +256,47 @@ decode_means_kernel(const double* __restrict__ mcur, const double* __restrict__ 
   const int hw = out_w / 2;
   const int Y0 = blockIdx.y * kTile, X0 = blockIdx.x * kTile;  // 2-D grid of tiles
   const int lane_c = threadIdx.x & (kTile - 1), row0 = threadIdx.x >> 5;  // element e = threadIdx.x + 256 k
-  constexpr int kPer = kTile * kTile / kTileThreads;
-  constexpr int kRowStep = kTileThreads / kTile;
+  constexpr int kPer = kTile * kTile / kMeanThreads;
+  constexpr int kRowStep = kMeanThreads / kTile;
   const bool first = mprev == nullptr;
   double zv[kPer], pv[kPer];
   Blk B;
+  unsigned aw = 0;     // kWhole: the isometry as an affine map (symmetry_affine_word)
   int a0 = 0, c0 = 0;  // kWhole: the tile's offset inside its range
   if (kWhole) {
-    const int ry = Y0 / kn, rx = X0 / kn;
-    a0 = Y0 - ry * kn;
-    c0 = X0 - rx * kn;
-    const RangeXform t = xf[ry * ranges_x + rx];
-    int r0, cc0, r1, c1;
-    symmetry_source(t.sym, a0, c0, kn, r0, cc0);
-    symmetry_source(t.sym, a0 + T - 1, c0 + T - 1, kn, r1, c1);
-    B.s = t.s;
-    B.o = t.o;
-    B.sym = t.sym;
-    B.sr0 = min(r0, r1);
-    B.sc0 = min(cc0, c1);
-    B.mrow0 = t.dy / 2 + B.sr0;
-    B.mcol0 = t.dx / 2 + B.sc0;
+    // the tile's block (one range): thread 0 does the divisions, the code load and the corner
+    // sources once, every thread reads them from shared memory
+    __shared__ int s_blk[6];
+    __shared__ double s_so[2];
+    if (threadIdx.x == 0) {
+      const int ry = Y0 / kn, rx = X0 / kn;
+      const int ta0 = Y0 - ry * kn, tc0 = X0 - rx * kn;
+      const RangeXform t = xf[ry * ranges_x + rx];
+      int r0, cc0, r1, c1;
+      symmetry_source(t.sym, ta0, tc0, kn, r0, cc0);
+      symmetry_source(t.sym, ta0 + T - 1, tc0 + T - 1, kn, r1, c1);
+      s_blk[0] = ta0;
+      s_blk[1] = tc0;
+      s_blk[2] = t.sym;
+      s_blk[3] = min(r0, r1);
+      s_blk[4] = min(cc0, c1);
+      s_blk[5] = 0;
+      s_so[0] = t.s;
+      s_so[1] = t.o;
+      blk[0].mrow0 = t.dy / 2 + min(r0, r1);
+      blk[0].mcol0 = t.dx / 2 + min(cc0, c1);
+    }
+    __syncthreads();
+    a0 = s_blk[0];
+    c0 = s_blk[1];
+    B.sym = s_blk[2];
+    B.sr0 = s_blk[3];
+    B.sc0 = s_blk[4];
+    B.s = s_so[0];
+    B.o = s_so[1];
+    B.mrow0 = blk[0].mrow0;
+    B.mcol0 = blk[0].mcol0;
+    aw = symmetry_affine_word(B.sym);
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const long long off = (long long)(B.mrow0 + row0 + k * kRowStep) * hw + B.mcol0 + lane_c;
@@ -282,7 +304,7 @@ decode_means_kernel(const double* __restrict__ mcur, const double* __restrict__ 
       pv[k] = first ? 0.0 : __ldg(mprev + off);
     }
   } else {
-    for (int b = threadIdx.x; b < nb; b += kTileThreads) {
+    for (int b = threadIdx.x; b < nb; b += kMeanThreads) {
       const int ry = (Y0 >> LT) + b / bpr, rx = (X0 >> LT) + b % bpr;
       const RangeXform t = xf[ry * ranges_x + rx];
       Blk Q;
@@ -322,11 +344,11 @@ decode_means_kernel(const double* __restrict__ mcur, const double* __restrict__ 
   double sq = 0.0;
   int zoff0 = 0, zstep = 0;
   if (kWhole) {  // the isometry is affine in (row, col): one base and one stride per thread
-    int r00, c00, r10, c10;
-    symmetry_source(B.sym, a0 + row0, c0 + lane_c, kn, r00, c00);
-    symmetry_source(B.sym, a0 + row0 + 1, c0 + lane_c, kn, r10, c10);
-    zoff0 = (r00 - B.sr0) * (kTile + 1) + (c00 - B.sc0);
-    zstep = kRowStep * ((r10 - r00) * (kTile + 1) + (c10 - c00));
+    const int m = kn - 1, r = a0 + row0, c = c0 + lane_c;
+    const int sr = affine_coef(aw, 0) * r + affine_coef(aw, 1) * c + affine_coef(aw, 2) * m;
+    const int sc = affine_coef(aw, 3) * r + affine_coef(aw, 4) * c + affine_coef(aw, 5) * m;
+    zoff0 = (sr - B.sr0) * (kTile + 1) + (sc - B.sc0);
+    zstep = kRowStep * (affine_coef(aw, 0) * (kTile + 1) + affine_coef(aw, 3));
   }
   const double* zflat = &zs[0][0];
   const double* pflat = &ps[0][0];
@@ -357,20 +379,20 @@ decode_means_kernel(const double* __restrict__ mcur, const double* __restrict__ 
     sq = __dadd_rn(sq, __dmul_rn(dlt, dlt));
   }
   __syncthreads();
-  {  // the next iteration's means of this tile's outputs: 16 x 16, one per thread
-    const int i = threadIdx.x >> 4, j = threadIdx.x & 15;
+  for (int e = threadIdx.x; e < 256; e += kMeanThreads) {  // the next iteration's 16 x 16 means of the tile
+    const int i = e >> 4, j = e & 15;
     const double m = __dmul_rn(
         __dadd_rn(__dadd_rn(__dadd_rn(vs[2 * i][2 * j], vs[2 * i][2 * j + 1]), vs[2 * i + 1][2 * j]), vs[2 * i + 1][2 * j + 1]),
         0.25);
     mnxt[(long long)(Y0 / 2 + i) * hw + X0 / 2 + j] = m;
   }
-  __shared__ double red[kTileThreads / 32];
+  __shared__ double red[kMeanThreads / 32];
   for (int off = 16; off > 0; off >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, off));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < kTileThreads / 32; ++w) t = __dadd_rn(t, red[w]);
+    for (int w = 0; w < kMeanThreads / 32; ++w) t = __dadd_rn(t, red[w]);
     partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
 }
@@ -386,7 +408,7 @@ void launch_decode_means(const double* mcur, const double* mprev, int init_kind,
                          double* partial, unsigned char* out_u8, cudaStream_t st) {
   const dim3 grid(out_w / kTile, out_h / kTile);
 #define FIC_MEANS(LT)                                                                                   \
-  decode_means_kernel<LT><<<grid, kTileThreads, 0, st>>>(mcur, mprev, init_kind, sup, mnxt, xf, out_w, kn, \
+  decode_means_kernel<LT><<<grid, kMeanThreads, 0, st>>>(mcur, mprev, init_kind, sup, mnxt, xf, out_w, kn, \
                                                          ranges_x, partial, out_u8)
   switch (kn >= kTile ? 5 : __builtin_ctz((unsigned)kn)) {
     case 1: FIC_MEANS(1); break;

@@ -552,7 +552,7 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
   k.push_back(ws.list_cap);
   for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED",
                            "FIC_LANEBEST_MAX", "FIC_F16ACC", "FIC_F16SEL", "FIC_FUSED", "FIC_EVAL_SPLIT",
-                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP"}) {
+                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP", "FIC_EVAL_PER"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;

@@ -2179,7 +2179,9 @@ void launch_eval(const unsigned char* img, const Geometry& g, const unsigned sho
                  unsigned long long part, double* res, unsigned long long* gbest, const double* deq, uint2* pend,
                  unsigned* pend_counts, void* win_, bool inline_res, bool bar_only, int sms, cudaStream_t st) {
   (void)sms;
-  const int blocks = parts * kEvalPer;
+  int per = kEvalPer;  // blocks per list partition (the pending-list path needs kEvalPer)
+  if (const char* e = std::getenv("FIC_EVAL_PER"); e && (inline_res || bar_only)) per = std::max(1, std::atoi(e));
+  const int blocks = parts * per;
   const unsigned long long seg = eval_pend_seg(part);
   const DeqTables tab{deq, deq + (1 << g.s_bits)};
   unsigned __int128* win = static_cast<unsigned __int128*>(win_);
