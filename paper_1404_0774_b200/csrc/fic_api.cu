@@ -474,8 +474,10 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   // so they skip it: cfg2 0.335 / 0.337 / 0.344 ms without / with a 1 x 1 / 3 x 3 seed, cfg3
   // 2.456 / 2.447 / 2.462 ms (within noise), one launch fewer.  FIC_SEED=0 / 1 / 3 forces none /
   // 1 x 1 / 3 x 3.
+  // Without any sparse level (pools under 32 tiles, cfg1) the seed is the full level's only bar.
   const char* seed_env = std::getenv("FIC_SEED");
-  const int seed_side = seed_env ? std::atoi(seed_env) : (scan_tiles(g) > 1024 ? 3 : 0);
+  const int seed_side =
+      seed_env ? std::atoi(seed_env) : (scan_tiles(g) > 1024 || scan_levels(g).size() == 1 ? 3 : 0);
   const bool seed = seed_side > 0;
   if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, seed_side >= 3 ? 1 : 0, st);
   g_launches += seed ? 2 : 1;
