@@ -454,3 +454,34 @@ def test_fused_and_separate_evaluation(oracle, fused):
                 enc = fic.encode(img, fic.CodecParams(**pv))
             assert_same(enc.mappings, want, f"fused={fused} {extra} {pv}")
             assert enc.stats == st
+
+
+def test_random_parameter_sweep(oracle):
+    """Seeded random sweep over the parameter space the reference accepts (range size, domain
+    step, quantiser widths, s_max, shadow_eps) and image kinds (noise, smooth, binary, piecewise
+    flat, the CT phantom) against the oracle: codes, residual bits and stats, through the
+    default path (levels, selection, bars chosen per geometry)."""
+    rng = np.random.default_rng(14040774)
+    for trial in range(120):
+        n = int(rng.choice([2, 4, 8]))
+        side = int(rng.choice([s for s in (16, 32, 64, 128) if s >= 2 * n]))
+        step = int(rng.integers(1, 2 * n + 1))
+        pv = dict(n=n, step=step, s_bits=int(rng.integers(2, 9)), o_bits=int(rng.integers(3, 10)),
+                  s_max=float(rng.choice([0.5, 0.75, 1.0, 1.5])),
+                  shadow_eps=float(rng.choice([0.0, 0.0, 10.0, 300.0])))
+        kind = trial % 5
+        if kind == 0:
+            img = oracle.noise_image(side, 1000 + trial)
+        elif kind == 1:
+            img = oracle.smooth_image(side, 1000 + trial)
+        elif kind == 2:
+            img = (rng.random((side, side)) > 0.5).astype(np.uint8) * 255
+        elif kind == 3:
+            img = oracle.smooth_image(side, 1000 + trial)
+            img[: side // 2, : side // 3] = int(rng.integers(0, 256))
+        else:
+            img = images.ct_slice(side, 1404002 + trial, 0.2)
+        want, st = oracle.encode(img, pv)
+        enc = fic.encode(img, fic.CodecParams(**pv))
+        assert_same(enc.mappings, want, f"trial {trial} {pv} kind {kind}")
+        assert enc.stats == st, (trial, pv)
