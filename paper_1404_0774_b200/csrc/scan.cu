@@ -2129,17 +2129,16 @@ int scan_level_launches(const Geometry& g, int stride, int sms, bool fused) {
   return 1 + (!fused && make_level(g, stride, scan_grid(g, stride, sms)).select == 0 ? 1 : 0);
 }
 
-// Full level with an fp16 accumulator: large pools (the whole-tile vote mode, where the
-// epilogue's TMEM read and |max| test pace the MMAs: cfg4 scan 56.5 -> 51.6 ms) and K = 16
-// (one fp16 rounding: +0.4% survivors; cfg3 2.518 vs 2.525 ms); other small pools keep fp32
-// (the wider bound adds survivors that cost more than the halved read: cfg2 0.375 vs 0.372 ms,
-// cfg5 13.51 vs 13.31 ms).  FIC_F16ACC=1 / 0 forces it on / off for the full level.
+// Full level with an fp16 accumulator: large pools only (the whole-tile vote mode, where the
+// epilogue's TMEM read and |max| test pace the MMAs: cfg4 scan 56.5 -> 51.6 ms); small pools
+// keep fp32 (the wider bound adds survivors that cost more than the halved read: cfg2 0.319 vs
+// 0.326 ms, cfg3 (K = 16) 2.305 vs 2.342 ms, round 2).  FIC_F16ACC=1 / 0 forces it on / off.
 bool scan_use_f16acc(const Geometry& g, int stride, int sms) {
   if (stride != 1) return false;
   const char* e = std::getenv("FIC_F16ACC");
   if (e) return e[0] == '1';
   const ScanLevel lv = make_level(g, 1, scan_grid(g, 1, sms));
-  return lv.select == 0 && (lv.coarse || g.K <= 16);
+  return lv.select == 0 && lv.coarse;
 }
 
 int scan_padded_ranges(const Geometry& g) { return ((g.R + kScanRanges - 1) / kScanRanges) * kScanRanges; }

@@ -396,9 +396,9 @@ def test_coarse_vote_output_neutral(oracle, coarse):
 
 @pytest.mark.parametrize("coarse", ["0", "1"])
 def test_f16_accumulator_output_neutral(oracle, coarse):
-    """The full level with an fp16 accumulator (scan modes 5/6, default for large pools and
-    K = 16) forced on small images of every range size (n = 2, 4, 8), with and without the
-    whole-tile vote: identical codes and residual bits.
+    """The full level with an fp16 accumulator (scan modes 5/6, default for large pools) forced
+    on small images of every range size (n = 2, 4, 8), with and without the whole-tile vote:
+    identical codes and residual bits.
     The binary 0/255 image drives the operand/partial-sum overflow guard (ranges with a tiny
     bar relative to their norm get no bar)."""
     rng = np.random.default_rng(1404)
