@@ -747,7 +747,7 @@ void fill_stats_batch(fic_stats* stats, const Geometry& g, const unsigned long l
 // holds whole 32-range scan tiles (so no tile straddles two slices' domain pools), else 1.
 int batch_chunk(const Geometry& g) {
   if (matcher_mode(g) != 1 || g.R % 32 != 0) return 1;
-  if (const char* e = std::getenv("FIC_BATCH_CHUNK")) return std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("FIC_BATCH_CHUNK")) return std::min(64, std::max(1, std::atoi(e)));
   return 64;
 }
 
