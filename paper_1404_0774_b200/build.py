@@ -18,6 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
          "-Xptxas", "-warn-spills"] + (["-DFIC_TRACE"] if os.environ.get("FIC_TRACE") else [])  # pipeline trace build
+FLAGS += os.environ.get("FIC_NVCC_DEFINES", "").split()  # experiments, e.g. "-DFIC_EVAL_MINB_FULL=3"
 
 
 def _stale():

@@ -1710,14 +1710,21 @@ __device__ __forceinline__ bool list_slot(unsigned long long i, unsigned long lo
 // One thread per list entry: exact correlation from the q8 row and the range pixels, then
 // the reference's fp64 arithmetic (eval_exact) against the range's current bar; an achieved
 // residual lowers the bar.  res[i] = residual (+inf when pruned or flat).
-template <int NN>
-__global__ void __launch_bounds__(256, 4)
+#ifndef FIC_EVAL_MINB_FULL
+#define FIC_EVAL_MINB_FULL 3  // blocks per SM the register budget targets (full level: 85 registers, no spills)
+#endif
+#ifndef FIC_EVAL_MINB_BAR
+#define FIC_EVAL_MINB_BAR 4  // (sparse levels, bar only: 64 registers)
+#endif
+template <int NN, int BAR_ONLY>
+__global__ void __launch_bounds__(256, BAR_ONLY ? FIC_EVAL_MINB_BAR : FIC_EVAL_MINB_FULL)
 eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned short* __restrict__ qpool,
             const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
             const SurvEntry* __restrict__ list, const unsigned long long* __restrict__ counts, int parts,
             unsigned long long part, double* __restrict__ res, unsigned long long* __restrict__ gbest, DeqTables tab,
             uint2* __restrict__ pend, unsigned* __restrict__ pend_counts, unsigned long long seg,
-            unsigned __int128* __restrict__ win, int bar_only) {
+            unsigned __int128* __restrict__ win) {
+  constexpr bool bar_only = BAR_ONLY != 0;
   // pend == nullptr: every candidate's residual is computed here from the operands in registers
   // and the (residual, domain * 8 + isometry) minimum is kept per range in `win` (no residual
   // and winner passes); else the candidates that pass every screen go to the pending list.
@@ -1763,7 +1770,7 @@ eval_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned sh
         load_range_words<NN>(img, g, x0, y0, bpk);
         if (mi.den >= 0) {  // flat code blocks are never candidates (encoder.cpp:223-229)
           R = eval_fast<NN>(g, qw, bpk, rm.sb, (double)rm.var / (double)NN, mi.sq, mi.den, bar, screens,
-                            bar_only != 0, tab, qpool, img, d, s, x0, y0, qs, qo, pend ? &pending : nullptr);
+                            bar_only, tab, qpool, img, d, s, x0, y0, qs, qo, pend ? &pending : nullptr);
           if (R < inf) {
             if (pend || bar_only) {
               publish_best(gbest, r, R);
@@ -2186,8 +2193,12 @@ void launch_eval(const unsigned char* img, const Geometry& g, const unsigned sho
   unsigned __int128* win = static_cast<unsigned __int128*>(win_);
   uint2* pd = inline_res || bar_only ? nullptr : pend;
 #define FIC_EVAL(NN)                                                                                                 \
-  eval_kernel<NN><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest, tab, \
-                                          pd, pend_counts, seg, win, bar_only ? 1 : 0);                              \
+  if (bar_only)                                                                                                      \
+    eval_kernel<NN, 1><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest,  \
+                                               tab, pd, pend_counts, seg, win);                                      \
+  else                                                                                                               \
+    eval_kernel<NN, 0><<<blocks, 256, 0, st>>>(img, g, qpool, meta_i, rmeta, list, counts, parts, part, res, gbest,  \
+                                               tab, pd, pend_counts, seg, win);                                      \
   if (pd)                                                                                                            \
     residual_kernel<NN><<<blocks, 256, 0, st>>>(img, g, qpool, list, pend, pend_counts, seg, res, gbest, tab);
   if (g.N == 4) {
