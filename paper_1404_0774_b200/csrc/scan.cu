@@ -457,13 +457,15 @@ __device__ __forceinline__ int safe_code(double scaled) {
 // upper_only: return an upper bound of the exact residual from the closed form
 // parabola(s_deq) + N*o_gap^2 (seeding the bar; no residual loop).
 template <int NN>
-__device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* qw, const uint32_t* bpk, int sb,
-                                            double ssb, long long sqv, long long denv, double thr, bool screens,
-                                            bool upper_only, const DeqTables& tab, const unsigned short* qpool,
-                                            const unsigned char* img, int d, int s, int x0, int y0,
-                                            unsigned& qs_out, unsigned& qo_out, bool* pending = nullptr) {
+__device__ __forceinline__ double eval_fast_acc(const Geometry& g, int acc, const uint32_t* qw, const uint32_t* bpk,
+                                                int sb, double ssb, long long sqv, long long denv, double thr,
+                                                bool screens, bool upper_only, const DeqTables& tab,
+                                                const unsigned short* qpool, const unsigned char* img, int d, int s,
+                                                int x0, int y0, unsigned& qs_out, unsigned& qo_out,
+                                                bool* pending = nullptr) {
+  // (acc: the exact correlation sum_i q[perm_s(i)] b_i; qw / bpk are only read by the inline
+  // residual, i.e. never when upper_only)
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  const int acc = dot_q_b<NN>(qw, bpk);
   const long long num_q = (long long)NN * acc - sqv * (long long)sb;
   const double num_d = (double)num_q, den_d = (double)denv, sb_d = (double)sb;
   const double smax = g.s_max;
@@ -527,6 +529,33 @@ exact:
                                screens && !upper_only, &qs_out, &qo_out);
 }
 
+template <int NN>
+__device__ __forceinline__ double eval_fast(const Geometry& g, const uint32_t* qw, const uint32_t* bpk, int sb,
+                                            double ssb, long long sqv, long long denv, double thr, bool screens,
+                                            bool upper_only, const DeqTables& tab, const unsigned short* qpool,
+                                            const unsigned char* img, int d, int s, int x0, int y0,
+                                            unsigned& qs_out, unsigned& qo_out, bool* pending = nullptr) {
+  return eval_fast_acc<NN>(g, dot_q_b<NN>(qw, bpk), qw, bpk, sb, ssb, sqv, denv, thr, screens, upper_only, tab, qpool,
+                           img, d, s, x0, y0, qs_out, qo_out, pending);
+}
+
+__device__ __forceinline__ double load_bar(const unsigned long long* gbest, int r) {
+  return __longlong_as_double((long long)__ldcg(gbest + r));
+}
+
+// Operands of the survivor evaluation (scan epilogue bounds, fused consumers).
+struct EvalCtx {
+  const unsigned char* img;
+  const unsigned short* qpool;
+  const DomainMetaI* meta_i;
+  const RangeMeta* rmeta;
+  unsigned long long* gbest;
+  unsigned __int128* win;
+  DeqTables tab;
+};
+
+
+
 __global__ void deq_tables_kernel(Geometry g, double* ts, double* to) {
   const int ns = 1 << g.s_bits, no = 1 << g.o_bits;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ns + no; c += gridDim.x * blockDim.x) {
@@ -555,9 +584,6 @@ __device__ __forceinline__ void load_q8_row(const unsigned short* __restrict__ q
   }
 }
 
-__device__ __forceinline__ double load_bar(const unsigned long long* gbest, int r) {
-  return __longlong_as_double((long long)__ldcg(gbest + r));
-}
 
 // ------------------------------------------------------------------ seed
 // Exact evaluation of the 8 isometries of the (2h+1)^2 grid domains around each range's own
@@ -1017,15 +1043,6 @@ struct EntryChunks {
 };
 
 // ---- fused evaluation: consumer side ----
-struct EvalCtx {
-  const unsigned char* img;
-  const unsigned short* qpool;
-  const DomainMetaI* meta_i;
-  const RangeMeta* rmeta;
-  unsigned long long* gbest;
-  unsigned __int128* win;
-  DeqTables tab;
-};
 
 // One lane's survivor, evaluated exactly (eval_kernel's body with the residual inline).
 template <int NN>
