@@ -306,7 +306,7 @@ int matcher_mode(const Geometry& g) {
 }
 
 constexpr int kMaxLevels = 6;
-constexpr int kPartSlots = 256;      // per-level survivor counters, one per scan CTA (<= SMs)
+constexpr int kPartSlots = 512;      // per-level survivor counters, one per scan CTA (<= 2 x SMs)
 // per-level survivor counters, then one status block the host reads back after every encode:
 // record self-check failures, the pending count, the largest full-level partition (computed on
 // the device) and the flat / shadow counters of each slice (up to 64 slices per pass)
@@ -554,7 +554,7 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
   k.push_back(ws.list_cap);
   for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED",
                            "FIC_LANEBEST_MAX", "FIC_F16ACC", "FIC_F16SEL", "FIC_FUSED", "FIC_EVAL_SPLIT",
-                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP", "FIC_EVAL_PER"}) {
+                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP", "FIC_EVAL_PER", "FIC_ROTATE"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;

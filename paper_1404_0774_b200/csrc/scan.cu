@@ -43,7 +43,10 @@ constexpr int kScanRanges = kScanRows / kSyms;  // 32
 constexpr int kPoolBlock = 128;                 // domains per pool-builder CTA (pool padding)
 constexpr int kScanTileDom = 128;               // domains per pool tile (MMA M = TMEM lanes)
 constexpr int kScanMaxStages = 16;
-constexpr int kScanEpiWarps = 16;                       // 4 lane quarters x kEpiParts column parts
+#ifndef FIC_EPI_WARPS
+#define FIC_EPI_WARPS 16
+#endif
+constexpr int kScanEpiWarps = FIC_EPI_WARPS;            // 4 lane quarters x kEpiParts column parts
 constexpr int kEpiParts = kScanEpiWarps / 4;
 constexpr int kEpiRanges = kScanRanges / kEpiParts;    // ranges per epilogue thread
 constexpr int kEpiCols = kEpiRanges * kSyms;           // TMEM columns per epilogue thread
@@ -53,8 +56,17 @@ constexpr int kScanThreads = (2 + kScanEpiWarps) * 32;
 // role is done
 constexpr int kEvalWarps = 2;
 constexpr int kFusedThreads = (2 + kScanEpiWarps + kEvalWarps) * 32;
-constexpr uint32_t kScanTmemCols = 512;
-constexpr int kSmemBudget = 226 * 1024;
+// Scan CTAs per SM (FIC_SCAN_CTAS, 1 or 2).  Two CTAs per SM each own ONE 256-column TMEM
+// accumulator (instead of one CTA with two) and half the shared memory: twice the epilogue warps
+// per SM to hide the epilogue's latency, at a 56-register budget (fp32 accumulators are then
+// read 32 columns at a time).
+#ifndef FIC_SCAN_CTAS
+#define FIC_SCAN_CTAS 1
+#endif
+constexpr int kScanCtas = FIC_SCAN_CTAS;
+constexpr int kTBufs = 2 / kScanCtas;  // TMEM accumulator buffers per CTA
+constexpr uint32_t kScanTmemCols = 256 * kTBufs;
+constexpr int kSmemBudget = kScanCtas == 1 ? 226 * 1024 : 112 * 1024;
 
 // Survivor list entry: (encoded range r * 8 + isometry, canonical domain).
 typedef uint2 SurvEntry;
@@ -728,6 +740,7 @@ struct ScanLevel {
   int select;     // sparse levels: 1, 2 each range's best column per warp and tile (2: small pools), 3 per lane and segment
   int coarse;     // 1: whole-tile |max| vote before the per-range test (large pools: rare hits)
   int lanes_per_best;  // select == 3: lanes sharing one best entry per range (1, 2 or 4)
+  int rotate;          // epilogue column parts rotate over the warps tile by tile (select != 3)
 };
 
 struct Segment {
@@ -1179,7 +1192,7 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 // EV: 0 = survivors to the global list (expand / eval / residual / winner kernels follow);
 // NN (4, 16, 64) = fused: kEvalWarps consumer warps evaluate them in this kernel (EvalCtx).
 template <int MODE, int EV>
-__global__ void __launch_bounds__(EV ? kFusedThreads : kScanThreads, 1)
+__global__ void __launch_bounds__(EV ? kFusedThreads : kScanThreads, EV ? 1 : kScanCtas)
 scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, const __half* __restrict__ upool,
             const RangeMeta* __restrict__ rmeta, const unsigned char* __restrict__ ropnd,
             const float* __restrict__ thr, MaskRec* __restrict__ recs_all,
@@ -1291,9 +1304,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         ptx::mbar_wait(&rfull_bar[sg & 1], (sg >> 1) & 1);
         const uint64_t r_desc = ptx::smem_desc(ptx::smem_addr(sR + (sg & 1) * L.r_bytes), 128, K * 16);
         for (int j = S.j0; j < S.j1; ++j, ++i) {
-          const int buf = i & 1;
+          const int buf = kTBufs == 2 ? (i & 1) : 0;
           trace_stamp(g, i, 0);
-          ptx::mbar_wait(&tempty_bar[buf], ((i >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&tempty_bar[buf], (kTBufs == 2 ? ((i >> 1) & 1) : (i & 1)) ^ 1);
           trace_stamp(g, i, 1);
           ptx::mbar_wait(&full_bar[s], ring_phase);
           trace_stamp(g, i, 2);
@@ -1329,37 +1342,49 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
   } else if (warp < 2 + kScanEpiWarps) {
     // ================= epilogue =================
     const int e = warp - 2;
-    const int part = e >> 2;        // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
+    const int part0 = e >> 2;       // column part: ranges part*kEpiRanges .. +kEpiRanges-1 of the m-tile
     const int quarter = warp & 3;   // TMEM lane quarter: domains quarter*32 .. +31 of the tile
+    // lv.rotate: the column part advances by one per tile, so the warps of a part with a hot
+    // range (many hits) take turns instead of pacing every tile
+    const bool rotate = MB != 4 && lv.rotate;
     WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u, kSentinel, ring};
     constexpr bool sel = MB >= 2;
     SurvEntry* elist = elist_cta;
     const uint32_t ecap = (uint32_t)cap;
     EntryChunks ech{elist, ecount, ecap, 0u, 0u, kSentinel, ring};
-    const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + part * kEpiCols;
+    const uint32_t tlane = tmem_base + ((uint32_t)(quarter * 32) << 16);
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const Segment S = seg_at(lv, cta, G, sg);
-      const int r0 = S.m * kScanRanges + part * kEpiRanges;  // this thread's ranges
-      const uint32_t dslice = (uint32_t)(range_slice(g, r0) * g.Dt);  // pool index of the slice's domain 0
-      uint32_t allpass = 0;                          // ranges without a usable threshold
+      const int m0 = S.m * kScanRanges;  // the m-tile's first range (one slice per m-tile)
+      const uint32_t dslice = (uint32_t)(range_slice(g, m0) * g.Dt);  // pool index of the slice's domain 0
+      uint32_t allpass_all = 0;  // ranges of the m-tile without a usable threshold
 #pragma unroll
-      for (int k = 0; k < kEpiRanges; k += 4) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(thr + r0 + k));
-        allpass |= (uint32_t)range_allpass(t.x) << k | (uint32_t)range_allpass(t.y) << (k + 1) |
-                   (uint32_t)range_allpass(t.z) << (k + 2) | (uint32_t)range_allpass(t.w) << (k + 3);
+      for (int k = 0; k < kScanRanges; k += 4) {
+        if (!rotate && k / kEpiRanges != part0) continue;
+        const float4 t = __ldg(reinterpret_cast<const float4*>(thr + m0 + k));
+        allpass_all |= (uint32_t)range_allpass(t.x) << k | (uint32_t)range_allpass(t.y) << (k + 1) |
+                       (uint32_t)range_allpass(t.z) << (k + 2) | (uint32_t)range_allpass(t.w) << (k + 3);
       }
-      const uint32_t rowbase = (uint32_t)r0 * 8u;
+      uint32_t allpass = (allpass_all >> (part0 * kEpiRanges)) & ((1u << kEpiRanges) - 1u);
+      uint32_t rowbase = (uint32_t)(m0 + part0 * kEpiRanges) * 8u;  // this thread's ranges x 8
+      uint32_t tcol = tlane + part0 * kEpiCols;
       // MODE 4: each lane's running best column per range over the segment's tiles, packed as
       // (|x| truncated to 7 mantissa bits | 7 - isometry | level tile index), flushed below
       uint32_t lbest[MB == 4 ? kEpiRanges : 1];
 #pragma unroll
       for (int k = 0; k < (MB == 4 ? kEpiRanges : 1); ++k) lbest[k] = 0u;
       for (int j = S.j0; j < S.j1; ++j, ++i) {
-        const int buf = i & 1;
+        const int buf = kTBufs == 2 ? (i & 1) : 0;
+        if (rotate) {
+          const int part = (part0 + i) & (kEpiParts - 1);
+          allpass = (allpass_all >> (part * kEpiRanges)) & ((1u << kEpiRanges) - 1u);
+          rowbase = (uint32_t)(m0 + part * kEpiRanges) * 8u;
+          tcol = tlane + part * kEpiCols;
+        }
         if (lane == 0 && i > 0) trace_stamp(g, i - 1, 19 + e);  // done with the previous tile
         const uint32_t d = dslice + (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
-        ptx::mbar_wait_sleep(&tfull_bar[buf], (i >> 1) & 1);
+        ptx::mbar_wait_sleep(&tfull_bar[buf], kTBufs == 2 ? ((i >> 1) & 1) : (i & 1));
         ptx::tc_fence_after();
         if (g.flags & 128) {  // debug: no TMEM reads at all (MMA + producer throughput)
           __syncwarp();
@@ -1367,22 +1392,34 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           continue;
         }
         const uint32_t ta = tcol + buf * kScanRows;
-        uint32_t v[kEpiCols];  // F16: the first kEpiCols / 2
+        // fp32 accumulators at two CTAs per SM: kLoadCols = 32 columns (kCR ranges) per TMEM
+        // load, the buffer released after the last chunk's load
+        constexpr int kLoadCols = (F16 || kScanCtas == 1) ? kEpiCols : 32;
+        constexpr int kChunks = F16 ? 1 : kEpiCols / kLoadCols;
+        constexpr int kCR = kEpiRanges / kChunks;  // ranges per chunk
+#pragma unroll
+        for (int hc = 0; hc < kChunks; ++hc) {
+        uint32_t v[F16 ? kEpiCols : kLoadCols];  // F16: the first kEpiCols / 2
         __syncwarp();
         if constexpr (F16) {
-          ptx::tmem_ld_32x32b_x64_pack16(ta, v);  // register j: columns 2j, 2j + 1
+          if constexpr (kEpiCols == 64) ptx::tmem_ld_32x32b_x64_pack16(ta, v);  // register j: columns 2j, 2j + 1
+          else ptx::tmem_ld_32x32b_x32_pack16(ta, v);
         } else {
 #pragma unroll
-          for (int c = 0; c < kEpiCols; c += 32) ptx::tmem_ld_32x32b_x32(ta + c, v + c);
+          for (int c = 0; c < kLoadCols; c += 32) ptx::tmem_ld_32x32b_x32(ta + hc * kLoadCols + c, v + c);
         }
         ptx::tmem_ld_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
-          trace_stamp(g, i, 3 + e);
+        if (hc == kChunks - 1) {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::mbar_arrive(&tempty_bar[buf]);  // all columns read: release the buffer
+            trace_stamp(g, i, 3 + e);
+          }
         }
         if (g.flags & 8) continue;                          // debug: skip the test
+        const uint32_t ap = (allpass >> (hc * kCR)) & ((1u << kCR) - 1u);  // the chunk's ranges
+        const uint32_t rb = rowbase + 8u * (uint32_t)(hc * kCR);
         if constexpr (F16) {
           // fp16 pairs: range k's 8 isometry columns are registers 4k .. 4k + 3; the |max| test
           // runs on half2 (3-input VHMNMX with |.| modifiers: four columns per instruction).
@@ -1455,12 +1492,12 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           // work per tile); the threshold test is applied once, when the segment is flushed
           const uint32_t jtag = (uint32_t)j;  // < 8192 tiles (small pools only)
 #pragma unroll
-          for (int k = 0; k < kEpiRanges; ++k) {
+          for (int k = 0; k < kCR; ++k) {
             float m = 0.f;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
               m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFF0000u) | ((uint32_t)(7 - c) << 13) | jtag));
-            lbest[k] = max(lbest[k], __float_as_uint(m));
+            lbest[hc * kCR + k] = max(lbest[hc * kCR + k], __float_as_uint(m));
           }
           continue;
         }
@@ -1473,10 +1510,10 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           // warp max yield the winning lane and isometry.
           // MODE 3: packed maxima of every range up front (most ranges hit); MODE 2: plain
           // maxima for the hit test, packed ones only for the ranges that hit
-          uint32_t pk[kEpiRanges];
-          uint32_t gmask = allpass;
+          uint32_t pk[kCR];
+          uint32_t gmask = ap;
 #pragma unroll
-          for (int k = 0; k < kEpiRanges; ++k) {
+          for (int k = 0; k < kCR; ++k) {
             if constexpr (MB == 3) {
               float m = 0.f;
 #pragma unroll
@@ -1498,9 +1535,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           // one warp max yields the winning isometry AND lane; the hit ranges' maxima are
           // independent (issued back to back), then one chunk reservation covers all entries of
           // the tile and lane k writes range k's entry
-          uint32_t wm[kEpiRanges];
+          uint32_t wm[kCR];
 #pragma unroll
-          for (int k = 0; k < kEpiRanges; ++k) {
+          for (int k = 0; k < kCR; ++k) {
             uint32_t key = 0u;
             if ((groups >> k) & 1u) {
               float m = 0.f;
@@ -1513,13 +1550,13 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
               }
               const uint32_t mk = (__float_as_uint(m) & 0x7FFFFF00u) | ((__float_as_uint(m) & 7u) << 5) |
                                   (31u - (uint32_t)lane);
-              key = (m > 1.0f || ((allpass >> k) & 1u)) ? mk : 0u;
+              key = (m > 1.0f || ((ap >> k) & 1u)) ? mk : 0u;
             }
             wm[k] = __reduce_max_sync(0xffffffffu, key);
           }
           uint32_t hits = 0u, mine = 0u;
 #pragma unroll
-          for (int k = 0; k < kEpiRanges; ++k) {
+          for (int k = 0; k < kCR; ++k) {
             hits |= (uint32_t)(wm[k] != 0u) << k;
             if (lane == k) mine = wm[k];
           }
@@ -1529,20 +1566,20 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           if (mine != 0u) {
             const uint32_t pos = ech.base + (uint32_t)__popc(hits & ((1u << lane) - 1u));
             const uint32_t wl = 31u - (mine & 31u), ws = 7u - ((mine >> 5) & 7u);
-            if (pos < ecap) elist[pos] = make_uint2(rowbase + 8u * (uint32_t)lane + ws, d - (uint32_t)lane + wl);
+            if (pos < ecap) elist[pos] = make_uint2(rb + 8u * (uint32_t)lane + ws, d - (uint32_t)lane + wl);
           }
           ech.base += nh;
           ech.left -= nh;
           continue;
         }
-        if (MB == 1 && !allpass) {
+        if (MB == 1 && !ap) {
           // large pools, hits in ~2% of warp-tiles: one |max| over all 64 columns (32 FMNMX3)
           // and a warp vote first; the per-range breakdown only for the rare tiles with a hit
           // four independent FMNMX3 chains (8 deep instead of 16: the test's latency, not its
           // instruction count, is what the MMA waits on)
           float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
 #pragma unroll
-          for (int c = 0; c < kEpiCols; c += 8) {
+          for (int c = 0; c < kLoadCols; c += 8) {
             m0 = fmaxf(m0, fmaxf(fabsf(__uint_as_float(v[c])), fabsf(__uint_as_float(v[c + 1]))));
             m1 = fmaxf(m1, fmaxf(fabsf(__uint_as_float(v[c + 2])), fabsf(__uint_as_float(v[c + 3]))));
             m2 = fmaxf(m2, fmaxf(fabsf(__uint_as_float(v[c + 4])), fabsf(__uint_as_float(v[c + 5]))));
@@ -1551,9 +1588,9 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           if (!__any_sync(0xffffffffu, fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) > 1.0f)) continue;
         }
         // |max| of each range's 8 isometry columns (4 FMNMX3 each); mask of ranges above 1
-        uint32_t gmask = allpass;
+        uint32_t gmask = ap;
 #pragma unroll
-        for (int k = 0; k < kEpiRanges; ++k) {
+        for (int k = 0; k < kCR; ++k) {
           const float* f = reinterpret_cast<const float*>(v + 8 * k);
           const float gm = fmaxf(fmaxf(fmaxf(fmaxf(fabsf(f[0]), fabsf(f[1])), fmaxf(fabsf(f[2]), fabsf(f[3]))),
                                        fmaxf(fabsf(f[4]), fabsf(f[5]))),
@@ -1566,19 +1603,20 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           // ranges with a hit in some lane of the warp, one warp-uniform branch per range, so
           // only the hit ranges' column bits are formed (8 compares each)
 #pragma unroll
-          for (int k = 0; k < kEpiRanges; ++k) {
+          for (int k = 0; k < kCR; ++k) {
             if ((groups >> k) & 1u) {
               uint32_t bits = 0;
-              if ((allpass >> k) & 1u) {
+              if ((ap >> k) & 1u) {
                 bits = 0xFFu;
               } else {
 #pragma unroll
                 for (int c = 0; c < 8; ++c) bits |= (uint32_t)(fabsf(__uint_as_float(v[8 * k + c])) > 1.0f) << c;
               }
-              app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
+              app.put(bits, rb + 8u * (uint32_t)k, d - (uint32_t)lane);
             }
           }
         }
+        }  // chunk
       }
       if constexpr (MB == 4) {  // flush the segment's per-lane bests: one entry per lane group and range
         // lv.lanes_per_best consecutive lanes (1, 2, 4) share one entry: the group's largest key
@@ -2024,11 +2062,11 @@ void launch_seed_v3(const unsigned char* img, const Geometry& g, const unsigned 
 #undef FIC_SEED
 }
 
-// Scan CTAs (= list partitions) of a level: one per SM.
+// Scan CTAs (= list partitions) of a level: kScanCtas per SM.
 int scan_grid(const Geometry& g, int stride, int sms) {
   (void)g;
   (void)stride;
-  return sms;
+  return sms * kScanCtas;
 }
 
 static ScanLevel make_level(const Geometry& g, int stride, int G) {
@@ -2057,6 +2095,12 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
     const char* e = std::getenv("FIC_LANE_GROUP");  // lanes per best entry at per-lane-best levels
     const int lg = e ? std::atoi(e) : 1;
     lv.lanes_per_best = lg >= 4 ? 4 : (lg >= 2 ? 2 : 1);
+  }
+  {
+    // rotate the epilogue's column parts over the warps tile by tile (cfg3 full level 1.42 ->
+    // 1.31 ms, cfg4 -1 %, cfg2 neutral); FIC_ROTATE=0 / 1 forces it off / on (A/B)
+    const char* e = std::getenv("FIC_ROTATE");
+    lv.rotate = e ? (std::strcmp(e, "0") != 0) : 1;
   }
   lv.n_lvl = (n_tiles + stride - 1) / stride;
   lv.m_tiles = (g.R + kScanRanges - 1) / kScanRanges;
@@ -2203,6 +2247,7 @@ void launch_eval(const unsigned char* img, const Geometry& g, const unsigned sho
                  unsigned* pend_counts, void* win_, bool inline_res, bool bar_only, int sms, cudaStream_t st) {
   (void)sms;
   int per = kEvalPer;  // blocks per list partition (the pending-list path needs kEvalPer)
+  if (inline_res || bar_only) per = std::max(1, kEvalPer / kScanCtas);  // the same grid for 2 CTAs per SM
   if (const char* e = std::getenv("FIC_EVAL_PER"); e && (inline_res || bar_only)) per = std::max(1, std::atoi(e));
   const int blocks = parts * per;
   const unsigned long long seg = eval_pend_seg(part);
