@@ -71,7 +71,7 @@ size_t scan_rec_bytes(unsigned long long, int);
 int scan_trace_copy(long long*, int);
 int scan_padded_ranges(const Geometry&);
 void launch_threshold(const Geometry&, const RangeMeta*, const unsigned long long*, float*, cudaStream_t);
-bool scan_use_f16acc(const Geometry&, int stride, int sms);
+bool scan_use_f16acc(const Geometry&, int stride, int sms, bool sparse_levels);
 size_t range_op_bytes(const Geometry&);
 void launch_level_ops(const unsigned char*, const Geometry&, const RangeMeta*, const unsigned long long*, float*,
                       unsigned char*, unsigned long long*, bool, unsigned long long*, cudaStream_t);
@@ -399,9 +399,10 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   auto* pendc = static_cast<unsigned*>(ws.pendc.get((size_t)kPartSlots * 8 * sizeof(unsigned)));
   const unsigned long long part = ws.list_cap / (unsigned long long)parts;
   const bool final_level = stride == 1;  // resets the winner slots and the self-check counter too
-  // the full level of a large pool accumulates in fp16 (flags & 256: its thresholds and its scan)
+  // the full level accumulates in fp16 after sparse levels or for large pools (flags & 256: its
+  // thresholds and its scan)
   Geometry gl = g;
-  gl.flags = scan_use_f16acc(g, stride, ws.sms) ? (g.flags | 256) : (g.flags & ~256);
+  gl.flags = scan_use_f16acc(g, stride, ws.sms, scan_levels(g).size() > 1) ? (g.flags | 256) : (g.flags & ~256);
   launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, b.cnt + kPendSlot, final_level,
                    final_level ? b.cnt + kSelfcheckSlot : nullptr, st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;

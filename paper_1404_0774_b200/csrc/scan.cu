@@ -291,8 +291,11 @@ pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __rest
 // accumulation of K products (2^-21 relative each, generous) and fp16 subnormals.
 // f16acc (the full level with an fp16 accumulator, flags & 256): each of the K/16 MMAs rounds
 // the running sum to fp16, to nearest even (pinned on the B200 by tools/f16acc_probe.cu: ties
-// and quarter points, inside a K=16 step and across steps); every partial sum is bounded by
-// sum |u_i b_i| <= |u| |b|, so the K/16 roundings add at most (K/16) 2^-11 |u| |b|.
+// and quarter points, inside a K=16 step and across steps); every intermediate partial sum is
+// bounded by sum |u_i b_i| <= |u| |b|, so the first K/16 - 1 roundings add at most
+// (K/16 - 1) 2^-11 |u| |b|, while the last one is relative to the result the test compares:
+// |y| <= |fl(y)| / (1 - 2^-11), so a column passing the test at T (1 - 2^-11) has |y| <= T
+// (K = 16: the only rounding is that last one, ~T instead of ~|u| |b| wide).
 // Invariant: no scaled operand (fp16) and no fp16 partial sum may overflow, because the
 // epilogue's tests do not agree on non-finite values (the fp16 bit-pattern test counts inf and
 // NaN as hits, while __hmax2 in the whole-tile vote and the per-range max drops NaN operands).
@@ -304,8 +307,8 @@ __device__ __forceinline__ float scan_threshold(double ssb, double bar, int N, i
   const double sqrtT = sqrt((double)N * t) * (1.0 - 1e-6);
   const double ub = sqrt((double)N * ssb);
   double err = (9.765625e-4 * 1.0005 + (double)K * 4.76837158203125e-7) * 1.05 * ub + 0.01;
-  if (f16acc) err += (double)(K / 16) * 4.8828125e-4 * 1.05 * ub;
-  const double T = sqrtT - err;
+  if (f16acc) err += (double)(K / 16 - 1) * 4.8828125e-4 * 1.05 * ub;
+  const double T = (sqrtT - err) * (f16acc ? 1.0 - 4.8828125e-4 * 1.05 : 1.0);
   if (T * 60000.0 < ub * 1.01) return -1.f;
   return T > 0.0 ? __double2float_rd(T) : -1.f;
 }
@@ -1425,6 +1428,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           // runs on half2 (3-input VHMNMX with |.| modifiers: four columns per instruction).
           // |x| > 1 on the bit patterns: (h & 0x7FFF) > 0x3C00 (no inf / NaN: scan_threshold)
           const __half2* h = reinterpret_cast<const __half2*>(v);
+          const __half2 one2 = __float2half2_rn(1.0f);
           if (MB == 1 && !allpass) {
             __half2 m0 = __habs2(h[0]), m1 = __habs2(h[1]);
 #pragma unroll
@@ -1432,18 +1436,18 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
               m0 = __hmax2(m0, __hmax2(__habs2(h[c]), __habs2(h[c + 1])));
               m1 = __hmax2(m1, __hmax2(__habs2(h[c + 2]), __habs2(h[c + 3])));
             }
-            const __half2 mx = __hmax2(m0, m1);
-            const uint32_t mm = *reinterpret_cast<const uint32_t*>(&mx);
-            if (!__any_sync(0xffffffffu, (mm & 0xFFFFu) > 0x3C00u || (mm >> 16) > 0x3C00u)) continue;
+            if (!__any_sync(0xffffffffu, __hgt2_mask(__hmax2(m0, m1), one2) != 0u)) continue;
           }
-          uint32_t gmask = allpass;
+          // per range: one 3-input and one 2-input half2 |max|, one half2 compare (a 0xFFFF mask
+          // per half) and one masked OR; both halves folded once at the end
+          uint32_t g2 = 0u;
 #pragma unroll
           for (int k = 0; k < kEpiRanges; ++k) {
-            const __half2 mx = __hmax2(__hmax2(__habs2(h[4 * k]), __habs2(h[4 * k + 1])),
-                                       __hmax2(__habs2(h[4 * k + 2]), __habs2(h[4 * k + 3])));
-            const uint32_t mm = *reinterpret_cast<const uint32_t*>(&mx);
-            gmask |= (uint32_t)((mm & 0xFFFFu) > 0x3C00u || (mm >> 16) > 0x3C00u) << k;
+            const __half2 mx = __hmax2(__hmax2(__hmax2(__habs2(h[4 * k]), __habs2(h[4 * k + 1])), __habs2(h[4 * k + 2])),
+                                       __habs2(h[4 * k + 3]));
+            g2 |= __hgt2_mask(mx, one2) & (0x00010001u << k);
           }
+          const uint32_t gmask = ((g2 | (g2 >> 16)) & ((1u << kEpiRanges) - 1u)) | allpass;
           const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
           if constexpr (MB == 2) {
             // sparse level (it only lowers the bar, so fp16 accuracy is enough): per hit range the
@@ -1477,9 +1481,12 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 if ((allpass >> k) & 1u) {
                   bits = 0xFFu;
                 } else {
+                  // column c = 2j + half of register j: half2 compares give 0xFFFF masks, bit
+                  // 2j of the low half and bit 2j + 1 of the high half are kept, then folded
+                  uint32_t x = 0u;
 #pragma unroll
-                  for (int c = 0; c < 8; ++c)
-                    bits |= (uint32_t)(((v[4 * k + (c >> 1)] >> (16 * (c & 1))) & 0x7FFFu) > 0x3C00u) << c;
+                  for (int j = 0; j < 4; ++j) x |= __hgt2_mask(__habs2(h[4 * k + j]), one2) & (0x00020001u << (2 * j));
+                  bits = (x | (x >> 16)) & 0xFFu;
                 }
                 app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
               }
@@ -2197,16 +2204,18 @@ int scan_level_launches(const Geometry& g, int stride, int sms, bool fused) {
   return 1 + (!fused && make_level(g, stride, scan_grid(g, stride, sms)).select == 0 ? 1 : 0);
 }
 
-// Full level with an fp16 accumulator: large pools only (the whole-tile vote mode, where the
-// epilogue's TMEM read and |max| test pace the MMAs: cfg4 scan 56.5 -> 51.6 ms); small pools
-// keep fp32 (the wider bound adds survivors that cost more than the halved read: cfg2 0.319 vs
-// 0.326 ms, cfg3 (K = 16) 2.305 vs 2.342 ms, round 2).  FIC_F16ACC=1 / 0 forces it on / off.
-bool scan_use_f16acc(const Geometry& g, int stride, int sms) {
+// Full level with an fp16 accumulator whenever sparse levels ran before it (their bar keeps the
+// wider fp16 bound's extra survivors few) or the pool is large (whole-tile vote).  The fp16
+// epilogue tests 4 columns per |max| instruction and one half2 compare per range, so it beats
+// fp32 wherever the survivors stay few: cfg2 full level 121 -> 102 us, cfg3 1.31 -> 1.09 ms,
+// cfg4 56.5 -> 51.6 ms; cfg1 (no sparse level: hit-dominated) keeps fp32 (0.226 vs 0.223 ms).
+// FIC_F16ACC=1 / 0 forces it on / off.
+bool scan_use_f16acc(const Geometry& g, int stride, int sms, bool sparse_levels) {
   if (stride != 1) return false;
   const char* e = std::getenv("FIC_F16ACC");
   if (e) return e[0] == '1';
   const ScanLevel lv = make_level(g, 1, scan_grid(g, 1, sms));
-  return lv.select == 0 && lv.coarse;
+  return lv.select == 0 && (lv.coarse || sparse_levels);
 }
 
 int scan_padded_ranges(const Geometry& g) { return ((g.R + kScanRanges - 1) / kScanRanges) * kScanRanges; }

@@ -394,11 +394,13 @@ def test_coarse_vote_output_neutral(oracle, coarse):
         assert enc.stats == st
 
 
+@pytest.mark.parametrize("acc", ["1", "0"])
 @pytest.mark.parametrize("coarse", ["0", "1"])
-def test_f16_accumulator_output_neutral(oracle, coarse):
-    """The full level with an fp16 accumulator (scan modes 5/6, default for large pools) forced
-    on small images of every range size (n = 2, 4, 8), with and without the whole-tile vote:
-    identical codes and residual bits.
+def test_f16_accumulator_output_neutral(oracle, coarse, acc):
+    """The full level with an fp16 accumulator (scan modes 5/6, the default after sparse levels
+    and for large pools) and with an fp32 one (modes 0/1), each forced on small images of every
+    range size (n = 2, 4, 8), with and without the whole-tile vote: identical codes and
+    residual bits.
     The binary 0/255 image drives the operand/partial-sum overflow guard (ranges with a tiny
     bar relative to their norm get no bar)."""
     rng = np.random.default_rng(1404)
@@ -411,9 +413,9 @@ def test_f16_accumulator_output_neutral(oracle, coarse):
              (images.ct_slice(128, 1404003, 0.5), dict(n=2, step=1))]
     for img, pv in cases:
         want, st = oracle.encode(img, pv)
-        with env(FIC_F16ACC="1", FIC_COARSE=coarse):
+        with env(FIC_F16ACC=acc, FIC_COARSE=coarse):
             enc = fic.encode(img, fic.CodecParams(**pv))
-        assert_same(enc.mappings, want, f"f16acc coarse={coarse} {pv}")
+        assert_same(enc.mappings, want, f"f16acc={acc} coarse={coarse} {pv}")
         assert enc.stats == st
 
 
