@@ -821,6 +821,49 @@ __device__ void build_ranges(unsigned char* sR, const unsigned char* __restrict_
   }
 }
 
+// build_ranges for a compile-time range size NN = n * n (4, 16, 64): shifts instead of
+// divisions, and the inverse isometry's source cell from three bitmasks instead of a switch
+// (the rows of one warp carry different isometries): swap (0xCA), first flipped (0xA6),
+// second flipped (0x9C), the same map as symmetry_source (transforms.cpp:13-26).
+template <int NN>
+__device__ void build_ranges_n(unsigned char* sR, const unsigned char* __restrict__ img, const Geometry& g,
+                               const RangeMeta* __restrict__ rmeta, const float* __restrict__ thr, int mt, int tid,
+                               int nthreads, int chunks) {
+  constexpr int n = NN == 4 ? 2 : (NN == 16 ? 4 : 8);
+  constexpr int K = NN < 16 ? 16 : NN;
+  constexpr int KC = K / 8;
+  constexpr int m = n - 1;
+  for (int c = tid; c < chunks; c += nthreads) {
+    const int row = c / KC, kc = c % KC;
+    const int rl = row >> 3, s = row & 7;
+    const int r = mt * kScanRanges + rl;
+    const int sinv = s == 1 ? 3 : (s == 3 ? 1 : s);  // inverse isometries: 1 <-> 3, the others are involutions
+    const bool swap = (0xCAu >> sinv) & 1u, f0 = (0xA6u >> sinv) & 1u, f1 = (0x9Cu >> sinv) & 1u;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (r < g.R) {
+      int x0, y0;
+      range_origin(g, r, x0, y0);
+      const float mean = (float)rmeta[r].sb / (float)NN;  // exact: NN is a power of two
+      float scale = range_scale(thr[r]);
+      if (range_allpass(thr[r])) scale = rsqrtf((float)rmeta[r].var / (float)NN + 1.0f);
+      const unsigned char* base = img + (long long)y0 * g.W + x0;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int j = kc * 8 + h;
+        if (j < NN) {
+          const int jr = j / n, jc = j % n;
+          const int a = swap ? jc : jr, b = swap ? jr : jc;
+          const int ir = f0 ? m - a : a, ic = f1 ? m - b : b;  // i with perm_s(i) = j
+          const float v = ((float)base[(long long)ir * g.W + ic] - mean) * scale;
+          w[h >> 1] |= (uint32_t)__half_as_ushort(__float2half_rn(v)) << (16 * (h & 1));
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(sR + (row >> 3) * K * 16 + kc * 128 + (row & 7) * 16) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 // Per-range scan thresholds of a level (scan_threshold against the range's current bar);
 // padded to whole m-tiles.  Invalid and shadow ranges get +1e30 (never survive), flags & 1
 // (exhaustive debug mode) -1 (everything survives).
@@ -850,6 +893,7 @@ __global__ void threshold_kernel(Geometry g, const RangeMeta* __restrict__ rmeta
 // ranges, the blockIdx.y == 0 CTA writes them out for the scan epilogue), one launch per level.
 // It also resets the level's pending-residual counter and, for the full level, the record
 // self-check counter (instead of separate memsets).
+template <int NN>
 __global__ void __launch_bounds__(256)
 range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMeta* __restrict__ rmeta,
                 const unsigned long long* __restrict__ gbest, float* __restrict__ thr,
@@ -869,8 +913,13 @@ range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMe
   __syncthreads();
   // blockIdx.y splits the m-tile's 256 x K/8 chunks over several CTAs
   const int per = kScanRows * (g.K / 8) / gridDim.y;
-  build_ranges(ropnd + (long long)blockIdx.x * kScanRows * g.K * 2, img, g, rmeta, s_thr - blockIdx.x * kScanRanges,
-               blockIdx.x, blockIdx.y * per + threadIdx.x, blockDim.x, blockIdx.y * per + per);
+  unsigned char* dst = ropnd + (long long)blockIdx.x * kScanRows * g.K * 2;
+  const float* t = s_thr - blockIdx.x * kScanRanges;
+  if constexpr (NN == 0)
+    build_ranges(dst, img, g, rmeta, t, blockIdx.x, blockIdx.y * per + threadIdx.x, blockDim.x, blockIdx.y * per + per);
+  else
+    build_ranges_n<NN>(dst, img, g, rmeta, t, blockIdx.x, blockIdx.y * per + threadIdx.x, blockDim.x,
+                       blockIdx.y * per + per);
 }
 
 // Survivor appender of one warp: entries go straight to the CTA's list partition, into
@@ -2236,8 +2285,16 @@ void launch_level_ops(const unsigned char* img, const Geometry& g, const RangeMe
                       const unsigned long long* gbest, float* thr, unsigned char* ropnd,
                       unsigned long long* pend_count, bool full_level, unsigned long long* selfcheck,
                       cudaStream_t st) {
-  range_op_kernel<<<dim3((g.R + kScanRanges - 1) / kScanRanges, g.K / 8), 256, 0, st>>>(
-      img, g, rmeta, gbest, thr, ropnd, pend_count, full_level ? 1 : 0, selfcheck);
+  const dim3 grid((g.R + kScanRanges - 1) / kScanRanges, g.K / 8);
+  const int fl = full_level ? 1 : 0;
+  if (g.N == 4 && g.K == 16)
+    range_op_kernel<4><<<grid, 256, 0, st>>>(img, g, rmeta, gbest, thr, ropnd, pend_count, fl, selfcheck);
+  else if (g.N == 16 && g.K == 16)
+    range_op_kernel<16><<<grid, 256, 0, st>>>(img, g, rmeta, gbest, thr, ropnd, pend_count, fl, selfcheck);
+  else if (g.N == 64 && g.K == 64)
+    range_op_kernel<64><<<grid, 256, 0, st>>>(img, g, rmeta, gbest, thr, ropnd, pend_count, fl, selfcheck);
+  else
+    range_op_kernel<0><<<grid, 256, 0, st>>>(img, g, rmeta, gbest, thr, ropnd, pend_count, fl, selfcheck);
 }
 
 // Pending-list segment per eval block: the most entries one block can take (eval_kernel's
