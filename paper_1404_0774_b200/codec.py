@@ -118,12 +118,19 @@ def _range_count(h, w, p):
     return (w // p.n) * (h // p.n) if p.n > 0 else 0
 
 
-def encode(image, params=None, workers=1, chunk=(16, 16)):
-    """Full-search PIFS encode (module.cpp:94-107 -> encode_sequential / encode_parallel)."""
+def encode(image, params=None, workers=1, chunk=(16, 16), out=None):
+    """Full-search PIFS encode (module.cpp:94-107 -> encode_sequential / encode_parallel).
+    (extension) `out`: a caller-owned MAPPING_DTYPE array of at least (w/n)*(h/n) records to
+    encode into (page-locked memory, e.g. a pinned torch tensor's numpy view, is filled by DMA
+    directly, as a page-locked `image` is read); the result's mappings are a view of it."""
     params = CodecParams() if params is None else params
     img = _u8_2d(image)
     h, w = img.shape
-    out = np.zeros(max(_range_count(h, w, params), 1), MAPPING_DTYPE)
+    count = _range_count(h, w, params)
+    if out is None:
+        out = np.zeros(max(count, 1), MAPPING_DTYPE)
+    elif out.dtype != MAPPING_DTYPE or out.ndim != 1 or len(out) < count or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a contiguous MAPPING_DTYPE array of at least {count} records")
     st = FicStats()
     L = lib()
     if workers > 1:
@@ -132,7 +139,7 @@ def encode(image, params=None, workers=1, chunk=(16, 16)):
     else:
         rc = L.fic_encode(ptr(img), w, h, ctypes.byref(params.struct), ptr(out), ctypes.byref(st))
     _check(rc)
-    return EncodedImage(w, h, params, out[: _range_count(h, w, params)], st.as_dict())
+    return EncodedImage(w, h, params, out[:count], st.as_dict())
 
 
 def encode_with_stats(image, params=None):

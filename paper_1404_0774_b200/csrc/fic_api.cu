@@ -245,6 +245,9 @@ struct Workspace {
   // CUDA graphs of the scan-path encode, keyed by everything its launches bake in
   struct Graph {
     std::vector<unsigned long long> key;
+    cudaGraph_t graph = nullptr;  // kept for out_node (the records read-back, retargeted per call)
+    cudaGraphNode_t out_node = nullptr;
+    void* out_dst = nullptr;
     cudaGraphExec_t exec = nullptr;
     unsigned long long launches = 0;
     unsigned long long used = 0;
@@ -564,30 +567,59 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
   return k;
 }
 
-void enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b,
-                          fic_mapping* d_out, unsigned long long* d_counters, cudaStream_t st) {
+// The read-back of an encode: the status block from the self-check slot on (self-check,
+// largest partition, flat / shadow counters) into the pinned `hc`, and for a host-API encode the
+// records into the pinned `h_out`.
+struct Readback {
+  unsigned long long* hc;
+  size_t status_bytes;
+  fic_mapping* h_out;  // null: records stay on the device
+  size_t out_bytes;
+};
+
+void enqueue_readback(const Readback& rb, const ScanBufs& b, const fic_mapping* d_out, cudaStream_t st) {
+  CK(cudaMemcpyAsync(rb.hc + kSelfcheckSlot, b.cnt + kSelfcheckSlot, rb.status_bytes, cudaMemcpyDeviceToHost, st));
+  if (rb.h_out) CK(cudaMemcpyAsync(rb.h_out, d_out, rb.out_bytes, cudaMemcpyDeviceToHost, st));
+}
+
+// Returns true when the read-back rode in the replayed graph (its last nodes: no gap between
+// the last kernel and the copies, 2 fewer host calls); false when the caller must enqueue it.
+bool enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b,
+                          fic_mapping* d_out, unsigned long long* d_counters, cudaStream_t st,
+                          const Readback* rb) {
   if (std::getenv("FIC_NO_GRAPH") || g_timing.load()) {  // timed encodes (event records) run eagerly
     enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
-    return;
+    return false;
   }
   // the list capacity this encode will use (as enqueue_encode_scan sets it)
   ws.list_cap_grown = std::max(ws.list_cap_grown, std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128));
   ws.list_cap = ws.list_cap_grown;
   if (const char* lc = std::getenv("FIC_LIST_CAP")) ws.list_cap = std::strtoull(lc, nullptr, 10);
-  const std::vector<unsigned long long> key = encode_key(ws, d_img, g, d_out, d_counters, st);
+  std::vector<unsigned long long> key = encode_key(ws, d_img, g, d_out, d_counters, st);
+  key.push_back(rb ? (unsigned long long)(uintptr_t)rb->hc : 0ull);
+  key.push_back(rb ? rb->status_bytes : 0ull);
+  key.push_back(rb && rb->h_out ? rb->out_bytes : 0ull);
   ++ws.graph_clock;
   for (auto& gr : ws.graphs) {
     if (gr.key == key) {
+      if (gr.out_node && rb->h_out != gr.out_dst) {  // retarget the records copy to this call's buffer
+        CK(cudaGraphExecMemcpyNodeSetParams1D(gr.exec, gr.out_node, rb->h_out, d_out, rb->out_bytes,
+                                              cudaMemcpyDeviceToHost));
+        gr.out_dst = rb->h_out;
+      }
       CK(cudaGraphLaunch(gr.exec, st));
       g_launches += gr.launches;
       gr.used = ws.graph_clock;
-      return;
+      return rb != nullptr;
     }
   }
   if (key != ws.last_key) {  // first sighting: eager (allocates); capture on the next one
     enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
-    ws.last_key = encode_key(ws, d_img, g, d_out, d_counters, st);
-    return;
+    ws.last_key = encode_key(ws, d_img, g, d_out, d_counters, st);  // (the eager run may have grown buffers)
+    ws.last_key.push_back(rb ? (unsigned long long)(uintptr_t)rb->hc : 0ull);
+    ws.last_key.push_back(rb ? rb->status_bytes : 0ull);
+    ws.last_key.push_back(rb && rb->h_out ? rb->out_bytes : 0ull);
+    return false;
   }
   const unsigned long long l0 = g_launches.load();
   cudaGraph_t graph = nullptr;
@@ -596,6 +628,7 @@ void enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geome
   CK(cudaStreamBeginCapture(ws.stream, cudaStreamCaptureModeRelaxed));
   try {
     enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, ws.stream);
+    if (rb) enqueue_readback(*rb, b, d_out, ws.stream);
   } catch (...) {
     cudaStreamEndCapture(ws.stream, &graph);
     if (graph) cudaGraphDestroy(graph);
@@ -606,16 +639,34 @@ void enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geome
   gr.key = key;
   gr.launches = g_launches.load() - l0;
   gr.used = ws.graph_clock;
+  gr.graph = graph;
+  if (rb && rb->h_out) {  // the records copy: the memcpy node writing h_out
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeMemcpy) continue;
+      cudaMemcpy3DParms mp{};
+      CK(cudaGraphMemcpyNodeGetParams(nd, &mp));
+      if (mp.dstPtr.ptr == rb->h_out) gr.out_node = nd;
+    }
+    if (!gr.out_node) throw InternalFail{"graph capture: records read-back node not found"};
+    gr.out_dst = rb->h_out;
+  }
   CK(cudaGraphInstantiate(&gr.exec, graph, 0));
-  CK(cudaGraphDestroy(graph));
   CK(cudaGraphLaunch(gr.exec, st));
   if (ws.graphs.size() >= 16) {  // evict the least recently used
     auto it = std::min_element(ws.graphs.begin(), ws.graphs.end(),
                                [](const Workspace::Graph& a, const Workspace::Graph& c) { return a.used < c.used; });
     CK(cudaGraphExecDestroy(it->exec));
+    CK(cudaGraphDestroy(it->graph));
     ws.graphs.erase(it);
   }
   ws.graphs.push_back(std::move(gr));
+  return rb != nullptr;
 }
 
 // Enqueue the whole encode of the region described by g and wait for it; a survivor list
@@ -643,18 +694,21 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
   auto* hc = static_cast<unsigned long long*>(ws.h_scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
   if (g.batch > 64) throw InternalFail{"more than 64 slices in one encode pass"};
   d_counters = b.cnt + kCounterSlot;  // flat / shadow counters live in the status block
-  enqueue_encode_graph(ws, d_img, g, b, d_out, d_counters, st);
   // every level's partition counters only for the survivor statistics (timed / diagnostic encodes)
   const bool all_counts = g_timing.load() != 0 || (g.flags & 4);
+  const Readback rb{hc, (kCounterSlot - kSelfcheckSlot + 2 * g.batch) * sizeof(unsigned long long), h_out,
+                    (size_t)g.R * sizeof(fic_mapping)};
+  const bool in_graph = enqueue_encode_graph(ws, d_img, g, b, d_out, d_counters, st, all_counts ? nullptr : &rb);
   for (int attempt = 0;; ++attempt) {
     // one read-back of the status block (and the records of a host-API encode), one synchronisation
     if (all_counts)
       CK(cudaMemcpyAsync(hc, b.cnt, kScanCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    else
-      CK(cudaMemcpyAsync(hc + kSelfcheckSlot, b.cnt + kSelfcheckSlot,
-                         (kCounterSlot - kSelfcheckSlot + 2 * g.batch) * sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, st));
-    if (h_out) CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, st));
+    if (all_counts ? h_out != nullptr : !(attempt == 0 && in_graph)) {
+      if (all_counts)
+        CK(cudaMemcpyAsync(h_out, d_out, rb.out_bytes, cudaMemcpyDeviceToHost, st));
+      else
+        enqueue_readback(rb, b, d_out, st);
+    }
     CK(cudaStreamSynchronize(st));
     if (h_counters) std::memcpy(h_counters, hc + kCounterSlot, 2 * g.batch * sizeof(unsigned long long));
     const std::vector<int> lv = scan_levels(g);
@@ -785,23 +839,46 @@ int32_t guarded(F&& f) {
   }
 }
 
+// Page-locked (cudaHostAlloc / cudaHostRegister) host memory: copied by DMA directly.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host image -> device: DMA straight from a pinned image, else staged through the pinned
+// workspace buffer (one host copy, one DMA: splitting it into overlapped chunks measured
+// slower, 317.8 vs 308.9 us per cfg2 encode).
+void upload_image(Workspace& ws, const uint8_t* image, unsigned char* d_img, size_t bytes) {
+  const uint8_t* src = image;
+  if (!host_pinned(image)) {
+    auto* h_img = static_cast<unsigned char*>(ws.h_img.get(bytes));
+    std::memcpy(h_img, image, bytes);
+    src = h_img;
+  }
+  CK(cudaMemcpyAsync(d_img, src, bytes, cudaMemcpyHostToDevice, ws.stream));
+}
+
 // Encode `g` of the host image into host `out` (g.R records).
 int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, fic_stats* stats) {
   return guarded([&]() -> int32_t {
     Workspace& ws = workspace();
     std::lock_guard<std::mutex> lock(ws.mu);
     const size_t img_bytes = (size_t)g.W * g.H;
-    auto* h_img = static_cast<unsigned char*>(ws.h_img.get(img_bytes));
-    std::memcpy(h_img, image, img_bytes);
     auto* d_img = static_cast<unsigned char*>(ws.img.get(img_bytes));
     auto* d_out = static_cast<fic_mapping*>(ws.out.get((size_t)g.R * sizeof(fic_mapping)));
     auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * g.batch * sizeof(unsigned long long)));
-    auto* h_out = static_cast<fic_mapping*>(ws.h_out.get((size_t)g.R * sizeof(fic_mapping)));
+    // records: DMA straight into a pinned `out`, else through the pinned workspace buffer
+    const bool out_pinned = host_pinned(out);
+    auto* h_out = out_pinned ? out : static_cast<fic_mapping*>(ws.h_out.get((size_t)g.R * sizeof(fic_mapping)));
     auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * g.batch * sizeof(unsigned long long)));
-    CK(cudaMemcpyAsync(d_img, h_img, img_bytes, cudaMemcpyHostToDevice, ws.stream));
+    upload_image(ws, image, d_img, img_bytes);
     run_encode(ws, d_img, g, d_out, d_cnt, h_cnt, ws.stream, h_out);  // records copied before its one sync
     collect_timing(ws);
-    std::memcpy(out, h_out, (size_t)g.R * sizeof(fic_mapping));
+    if (!out_pinned) std::memcpy(out, h_out, (size_t)g.R * sizeof(fic_mapping));
     if (g.batch > 1)
       fill_stats_batch(stats, g, h_cnt);
     else

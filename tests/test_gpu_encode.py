@@ -487,3 +487,31 @@ def test_random_parameter_sweep(oracle):
         enc = fic.encode(img, fic.CodecParams(**pv))
         assert_same(enc.mappings, want, f"trial {trial} {pv} kind {kind}")
         assert enc.stats == st, (trial, pv)
+
+
+@pytest.mark.gpu
+def test_encode_into_caller_buffers(oracle):
+    """fic.encode(out=...): page-locked image and records (DMA both ways, the records copy
+    riding in the replayed graph and retargeted to each call's buffer) and pageable ones give
+    the same records as the plain call; a wrong buffer is refused."""
+    import torch
+
+    from paper_1404_0774_b200.abi import MAPPING_DTYPE
+
+    img = images.ct_slice(256, 1404011, 0.4)
+    p = fic.CodecParams(n=8, step=4)
+    want, st = oracle.encode(img, dict(n=8, step=4))
+    R = (256 // 8) ** 2
+    pin_img = torch.empty(img.shape, dtype=torch.uint8, pin_memory=True).numpy()
+    pin_img[:] = img
+    outs = [torch.empty(R * 32, dtype=torch.uint8, pin_memory=True).numpy().view(MAPPING_DTYPE) for _ in range(2)]
+    outs.append(np.zeros(R, MAPPING_DTYPE))
+    for rep in range(3):  # eager, captured, replayed: each call into another buffer
+        for k, o in enumerate(outs):
+            o[:] = np.zeros(1, MAPPING_DTYPE)
+            enc = fic.encode(pin_img if k != 2 else img, p, out=o)
+            assert enc.mappings.base is o or np.shares_memory(enc.mappings, o)
+            assert_same(o, want, f"out buffer {k} pass {rep}")
+            assert enc.stats == st
+    with pytest.raises(ValueError):
+        fic.encode(img, p, out=np.zeros(R - 1, MAPPING_DTYPE))
