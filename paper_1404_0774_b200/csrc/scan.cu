@@ -1500,26 +1500,44 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
           if constexpr (MB == 2) {
             // sparse level (it only lowers the bar, so fp16 accuracy is enough): per hit range the
-            // warp's best column, key = |h| << 3 | (7 - isometry) (exact magnitude order; ties
-            // to the lower isometry, then the lower lane)
+            // warp's best column.  Each half's low 3 mantissa bits are replaced by 7 - isometry
+            // (one LOP3 per register; the magnitude order is kept to 2^-7), so the half2 |max|
+            // tree yields the best column AND its isometry; key = that half << 5 | 31 - lane,
+            // one warp max per range, one chunk reservation per tile, lane k writes range k's
+            // entry (as the fp32 selection)
+            uint32_t wm[kEpiRanges];
 #pragma unroll
             for (int k = 0; k < kEpiRanges; ++k) {
+              uint32_t key = 0u;
               if ((groups >> k) & 1u) {
-                uint32_t m = 0;
+                __half2 t[4];
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                  m = max(m, (((v[4 * k + (c >> 1)] >> (16 * (c & 1))) & 0x7FFFu) << 3) | (uint32_t)(7 - c));
-                const uint32_t key = (m > ((0x3C00u << 3) | 7u) || ((allpass >> k) & 1u)) ? m : 0u;
-                const uint32_t wmax = __reduce_max_sync(0xffffffffu, key);
-                if (wmax == 0u) continue;
-                const uint32_t win = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
-                ech.reserve(1);  // warp-level chunk of entry slots
-                if ((uint32_t)lane == win && ech.base < ecap)
-                  elist[ech.base] = make_uint2(rowbase + 8u * (uint32_t)k + (7u - (wmax & 7u)), d);
-                ++ech.base;
-                --ech.left;
+                for (int j = 0; j < 4; ++j) {
+                  const uint32_t u = (v[4 * k + j] & 0x7FF87FF8u) | ((7u - 2u * j) | ((6u - 2u * j) << 16));
+                  t[j] = *reinterpret_cast<const __half2*>(&u);
+                }
+                const __half2 m2 = __hmax2(__hmax2(__hmax2(t[0], t[1]), t[2]), t[3]);
+                const uint32_t m = __half_as_ushort(__hmax(__low2half(m2), __high2half(m2)));
+                key = (m > 0x3C07u || ((allpass >> k) & 1u)) ? (m << 5) | (31u - (uint32_t)lane) : 0u;
               }
+              wm[k] = __reduce_max_sync(0xffffffffu, key);
             }
+            uint32_t hits = 0u, mine = 0u;
+#pragma unroll
+            for (int k = 0; k < kEpiRanges; ++k) {
+              hits |= (uint32_t)(wm[k] != 0u) << k;
+              if (lane == k) mine = wm[k];
+            }
+            if (!hits) continue;
+            const uint32_t nh = (uint32_t)__popc(hits);
+            ech.reserve(nh);
+            if (mine != 0u) {
+              const uint32_t pos = ech.base + (uint32_t)__popc(hits & ((1u << lane) - 1u));
+              const uint32_t wl = 31u - (mine & 31u), ws = 7u - ((mine >> 5) & 7u);
+              if (pos < ecap) elist[pos] = make_uint2(rowbase + 8u * (uint32_t)lane + ws, d - (uint32_t)lane + wl);
+            }
+            ech.base += nh;
+            ech.left -= nh;
             continue;
           }
           if (groups) {
@@ -2184,13 +2202,16 @@ size_t scan_rec_bytes(unsigned long long list_cap, int parts) {
   return (size_t)scan_rec_part(list_cap / (unsigned long long)parts) * parts * sizeof(MaskRec);
 }
 
-// Hit-first sparse levels (large pools) with an fp16 accumulator (FIC_F16SEL=1, scan mode 7): a
-// sparse level only lowers the bar, so neither its test nor its selection needs a bound.  Off
-// by default: cfg4 measured no gain (stride-16 level 5.36 ms either way; that epilogue is bound
-// by the per-hit-range warp reductions, not by the TMEM read or the |max| test).
-bool scan_f16sel() {
+// Hit-first sparse levels with an fp16 accumulator (scan mode 7): a sparse level only lowers
+// the bar, so neither its test nor its selection needs a bound.  The fp16 selection tags each
+// half with its isometry (one LOP3 per register) and takes the half2 |max| tree: on by default
+// for small pools (cfg3: stride-32 / stride-4 levels 112 -> 88 / 512 -> 421 us, encode 2.04 ->
+// 1.92 ms); large pools keep fp32 (cfg4: its stride-16 level got slower and its 2^-7 magnitude
+// resolution a weaker bar, 63.1 -> 64.9 ms).  FIC_F16SEL=0 / 1 forces it off / on.
+bool scan_f16sel(const Geometry& g) {
   const char* e = std::getenv("FIC_F16SEL");
-  return e && e[0] == '1';
+  if (e) return e[0] == '1';
+  return scan_tiles(g) <= 1024;
 }
 
 typedef void (*ScanKern)(const unsigned char*, Geometry, ScanLevel, const __half*, const RangeMeta*,
@@ -2229,7 +2250,7 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
   // fp16 accumulator: the full level only (its thresholds carry the fp16 bound, range_op_kernel)
   if (scan_f16acc(g) && stride == 1 && mode <= 1) mode += 5;
-  if (mode == 2 && scan_f16sel()) mode = 7;
+  if (mode == 2 && scan_f16sel(g)) mode = 7;
   const ScanKern kern = !fused ? scan_fn<0>(mode)
                         : g.N == 4 ? scan_fn<4>(mode) : (g.N == 16 ? scan_fn<16>(mode) : scan_fn<64>(mode));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
