@@ -1239,7 +1239,7 @@ __device__ __forceinline__ float absmax8(const uint32_t* v) {
 // the per-range test before the selection (lv.select == 1), 3 sparse level selecting from the
 // packed maxima of every range (lv.select == 2: most ranges hit in most tiles), 4 sparse level
 // keeping each lane's best per range over the whole segment (lv.select == 3: short levels of
-// small pools, one segment per m-tile); 5, 6 and 7: modes 0, 1 and 2 with an fp16
+// small pools, one segment per m-tile); 5, 6, 7 and 9: modes 0, 1, 2 and 4 with an fp16
 // accumulator (full level: scan_f16acc; sparse level: scan_f16sel).  One instantiation per mode keeps each epilogue's registers to its own path.
 // EV: 0 = survivors to the global list (expand / eval / residual / winner kernels follow);
 // NN (4, 16, 64) = fused: kEvalWarps consumer warps evaluate them in this kernel (EvalCtx).
@@ -1478,6 +1478,24 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           // |x| > 1 on the bit patterns: (h & 0x7FFF) > 0x3C00 (no inf / NaN: scan_threshold)
           const __half2* h = reinterpret_cast<const __half2*>(v);
           const __half2 one2 = __float2half2_rn(1.0f);
+          if constexpr (MB == 4) {
+            // per-lane best per range over the segment: the isometry-tagged half2 |max| tree
+            // (as the fp16 hit-first selection) and the tile index below it
+            const uint32_t jtag = (uint32_t)j;  // < 8192 tiles (small pools only)
+#pragma unroll
+            for (int k = 0; k < kEpiRanges; ++k) {
+              __half2 t[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t u = (v[4 * k + q] & 0x7FF87FF8u) | ((7u - 2u * q) | ((6u - 2u * q) << 16));
+                t[q] = *reinterpret_cast<const __half2*>(&u);
+              }
+              const __half2 m2 = __hmax2(__hmax2(__hmax2(t[0], t[1]), t[2]), t[3]);
+              const uint32_t m = __half_as_ushort(__hmax(__low2half(m2), __high2half(m2)));
+              lbest[k] = max(lbest[k], (m << 16) | jtag);
+            }
+            continue;
+          }
           if (MB == 1 && !allpass) {
             __half2 m0 = __habs2(h[0]), m1 = __habs2(h[1]);
 #pragma unroll
@@ -1704,13 +1722,16 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             const bool lower = (lane & o) == 0;
             if (ob > b || (ob == b && !lower)) win_lane = false;
           }
-          const bool keep = win_lane && b != 0u && (__uint_as_float(b) > 1.0f || ((allpass >> k) & 1u));
+          // fp32 key: the float bits (|x| to 7 mantissa bits | 7 - isometry | tile); fp16 key:
+          // (half |x| with 7 - isometry in its low 3 bits) << 16 | tile
+          const bool above = F16 ? (b >> 16) > 0x3C07u : __uint_as_float(b) > 1.0f;
+          const bool keep = win_lane && b != 0u && (above || ((allpass >> k) & 1u));
           const uint32_t bal = __ballot_sync(0xffffffffu, keep);
           if (!bal) continue;
           ech.reserve((uint32_t)__popc(bal));
           const uint32_t pos = ech.base + __popc(bal & ((1u << lane) - 1u));
           if (keep && pos < ecap) {
-            const uint32_t jt = b & 0x1FFFu, s_iso = 7u - ((b >> 13) & 7u);
+            const uint32_t jt = b & 0x1FFFu, s_iso = 7u - ((b >> (F16 ? 16 : 13)) & 7u);
             const uint32_t dd = dslice + (uint32_t)(jt * lv.stride * kScanTileDom + quarter * 32 + lane);
             elist[pos] = make_uint2(rowbase + 8u * (uint32_t)k + s_iso, dd);
           }
@@ -2228,7 +2249,8 @@ ScanKern scan_fn(int mode) {
     case 4: return scan_kernel<4, EV>;
     case 5: return scan_kernel<5, EV>;
     case 6: return scan_kernel<6, EV>;
-    default: return scan_kernel<7, EV>;
+    case 7: return scan_kernel<7, EV>;
+    default: return scan_kernel<9, EV>;
   }
 }
 
@@ -2250,7 +2272,7 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   int mode = lv.select == 3 ? 4 : (lv.select == 2 ? 3 : (lv.select == 1 ? 2 : (lv.coarse ? 1 : 0)));
   // fp16 accumulator: the full level only (its thresholds carry the fp16 bound, range_op_kernel)
   if (scan_f16acc(g) && stride == 1 && mode <= 1) mode += 5;
-  if (mode == 2 && scan_f16sel(g)) mode = 7;
+  if ((mode == 2 || mode == 4) && scan_f16sel(g)) mode += 5;  // 7 / 9: fp16 selection
   const ScanKern kern = !fused ? scan_fn<0>(mode)
                         : g.N == 4 ? scan_fn<4>(mode) : (g.N == 16 ? scan_fn<16>(mode) : scan_fn<64>(mode));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
