@@ -382,7 +382,8 @@ ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
   b.gbest = static_cast<unsigned long long*>(ws.gbest.get((size_t)g.R * sizeof(unsigned long long)));
   b.win = ws.win.get((size_t)g.R * 16);
   b.ropnd = static_cast<unsigned char*>(ws.ropnd.get(range_op_bytes(g)));
-  b.thr = static_cast<float*>(ws.thr.get((size_t)scan_padded_ranges(g) * sizeof(float)));
+  // thresholds, then one allpass bit mask per 32-range m-tile
+  b.thr = static_cast<float*>(ws.thr.get((size_t)scan_padded_ranges(g) * sizeof(float) * 33 / 32));
   b.deq = static_cast<double*>(ws.deq.get(deq_table_entries(g) * sizeof(double)));
   b.cnt = static_cast<unsigned long long*>(ws.scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
   return b;

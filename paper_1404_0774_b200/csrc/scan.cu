@@ -864,6 +864,15 @@ __device__ void build_ranges_n(unsigned char* sR, const unsigned char* __restric
   }
 }
 
+// After the level's padded thresholds: one bit mask per 32-range m-tile of its ranges without a
+// usable bar (range_allpass), written by range_op_kernel, read once per scan segment.
+__host__ __device__ __forceinline__ uint32_t* scan_allpass_masks(float* thr, const Geometry& g) {
+  return reinterpret_cast<uint32_t*>(thr + (size_t)((g.R + kScanRanges - 1) / kScanRanges) * kScanRanges);
+}
+__host__ __device__ __forceinline__ const uint32_t* scan_allpass_masks(const float* thr, const Geometry& g) {
+  return reinterpret_cast<const uint32_t*>(thr + (size_t)((g.R + kScanRanges - 1) / kScanRanges) * kScanRanges);
+}
+
 // Per-range scan thresholds of a level (scan_threshold against the range's current bar);
 // padded to whole m-tiles.  Invalid and shadow ranges get +1e30 (never survive), flags & 1
 // (exhaustive debug mode) -1 (everything survives).
@@ -905,6 +914,9 @@ range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMe
     const float t = range_threshold(g, rmeta, gbest, r, full_level && scan_f16acc(g));
     s_thr[threadIdx.x] = t;
     if (blockIdx.y == 0) thr[r] = t;
+    // the m-tile's ranges without a usable bar as one bit mask (the scan epilogue's allpass)
+    const unsigned ap = __ballot_sync(0xffffffffu, range_allpass(t));
+    if (blockIdx.y == 0 && threadIdx.x == 0) scan_allpass_masks(thr, g)[blockIdx.x] = ap;
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     *pend_count = 0;
@@ -1410,14 +1422,8 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
       const Segment S = seg_at(lv, cta, G, sg);
       const int m0 = S.m * kScanRanges;  // the m-tile's first range (one slice per m-tile)
       const uint32_t dslice = (uint32_t)(range_slice(g, m0) * g.Dt);  // pool index of the slice's domain 0
-      uint32_t allpass_all = 0;  // ranges of the m-tile without a usable threshold
-#pragma unroll
-      for (int k = 0; k < kScanRanges; k += 4) {
-        if (!rotate && k / kEpiRanges != part0) continue;
-        const float4 t = __ldg(reinterpret_cast<const float4*>(thr + m0 + k));
-        allpass_all |= (uint32_t)range_allpass(t.x) << k | (uint32_t)range_allpass(t.y) << (k + 1) |
-                       (uint32_t)range_allpass(t.z) << (k + 2) | (uint32_t)range_allpass(t.w) << (k + 3);
-      }
+      // ranges of the m-tile without a usable threshold (range_op_kernel's bit mask)
+      const uint32_t allpass_all = __ldg(scan_allpass_masks(thr, g) + S.m);
       uint32_t allpass = (allpass_all >> (part0 * kEpiRanges)) & ((1u << kEpiRanges) - 1u);
       uint32_t rowbase = (uint32_t)(m0 + part0 * kEpiRanges) * 8u;  // this thread's ranges x 8
       uint32_t tcol = tlane + part0 * kEpiCols;
