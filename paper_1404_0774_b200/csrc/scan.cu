@@ -2021,11 +2021,14 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
               const unsigned __int128* __restrict__ win, const unsigned long long* __restrict__ gbest,
               fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck,
               const unsigned long long* __restrict__ full_counts, int parts, unsigned long long* __restrict__ need) {
-  // the largest full-level list partition, for the host's overflow check (one status read-back)
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  // the largest full-level list partition, for the host's overflow check (one status read-back):
+  // one warp, its loads in flight together
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
     unsigned long long m = 0;
-    for (int c = 0; c < parts; ++c) m = max(m, full_counts[c]);
-    *need = m;
+    for (int c = threadIdx.x; c < parts; c += 32) m = max(m, full_counts[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *need = m;
   }
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= g.R) return;
@@ -2404,10 +2407,10 @@ void launch_record(const unsigned char* img, const Geometry& g, const unsigned s
                    const DomainMetaI* meta_i, const RangeMeta* rmeta, const void* win_,
                    const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck,
                    const unsigned long long* full_counts, int parts, unsigned long long* need, cudaStream_t st) {
-  const int blocks = (g.R + 127) / 128;
+  const int blocks = (g.R + 63) / 64;  // 64-thread blocks: the per-range exact evaluations spread over more SMs
   const unsigned __int128* win = static_cast<const unsigned __int128*>(win_);
 #define FIC_REC(NN) \
-  record_kernel<NN><<<blocks, 128, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, need)
+  record_kernel<NN><<<blocks, 64, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, need)
   if (g.N == 4) FIC_REC(4);
   else if (g.N == 16) FIC_REC(16);
   else FIC_REC(64);

@@ -515,3 +515,27 @@ def test_encode_into_caller_buffers(oracle):
             assert enc.stats == st
     with pytest.raises(ValueError):
         fic.encode(img, p, out=np.zeros(R - 1, MAPPING_DTYPE))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("acc", ["1", "0"])
+def test_near_threshold_candidates(oracle, acc):
+    """Periodic textures with faint noise: whole families of domains are copies of each other
+    up to a few grey levels, so each range has many candidates whose residuals tie or nearly tie
+    with the bar, i.e. correlations that sit right at the scan's pruning threshold (and
+    lexicographic ties the winner key must break by domain index).  Both accumulators, both
+    sparse selections: identical codes and residual bits."""
+    rng = np.random.default_rng(140401)
+    cases = []
+    for period, n, step, amp in [(8, 4, 2, 1), (16, 8, 4, 2), (4, 4, 1, 1), (12, 4, 3, 3), (8, 8, 2, 0)]:
+        base = rng.integers(0, 256, (period, period))
+        img = np.tile(base, (128 // period + 1, 128 // period + 1))[:128, :128]
+        img = np.clip(img + rng.integers(-amp, amp + 1, img.shape), 0, 255).astype(np.uint8)
+        cases.append((img, dict(n=n, step=step)))
+    for img, pv in cases:
+        want, st = oracle.encode(img, pv)
+        for sel in ("0", "1"):
+            with env(FIC_F16ACC=acc, FIC_F16SEL=sel):
+                enc = fic.encode(img, fic.CodecParams(**pv))
+            assert_same(enc.mappings, want, f"near-threshold acc={acc} sel={sel} {pv}")
+            assert enc.stats == st
