@@ -83,7 +83,8 @@ void launch_winner(const uint2*, const unsigned long long*, int, unsigned long l
                    const unsigned long long*, void*, int, cudaStream_t);
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
                    const RangeMeta*, const void*, const unsigned long long*, fic_mapping*, unsigned long long*,
-                   const unsigned long long*, int, unsigned long long*, cudaStream_t);
+                   const unsigned long long*, int, unsigned long long*, unsigned long long*, unsigned long long*,
+                   unsigned long long*, int, bool, cudaStream_t);
 void launch_probe_corr(const unsigned char*, const Geometry&, const unsigned short*, int, const int*, const int*,
                        const int*, long long*, cudaStream_t);
 }  // namespace ficb
@@ -255,6 +256,7 @@ struct Workspace {
   std::vector<Graph> graphs;
   std::vector<unsigned long long> last_key;  // fingerprint of the previous eager encode
   unsigned long long graph_clock = 0;
+  void* counts_zeroed = nullptr;  // the status block whose accumulators were cleared (scan_bufs)
   std::mutex mu;
 };
 
@@ -317,7 +319,9 @@ constexpr int kSelfcheckSlot = kMaxLevels * kPartSlots;
 constexpr int kPendSlot = kSelfcheckSlot + 1;
 constexpr int kNeedSlot = kPendSlot + 1;
 constexpr int kCounterSlot = kNeedSlot + 1;
-constexpr int kScanCountSlots = kCounterSlot + 2 * 64;
+constexpr int kAccumSlot = kCounterSlot + 2 * 64;  // flat / shadow accumulators (pool launch atomics)
+constexpr int kTicketSlot = kAccumSlot + 2 * 64;   // record_kernel's last-block ticket
+constexpr int kScanCountSlots = kTicketSlot + 2;
 
 // Scan levels: sparse passes over every 8^k-th (or 4 * 8^k-th) 128-domain tile seed the
 // pruning bar, then the full scan.  Each level prunes with the bar the previous
@@ -386,6 +390,11 @@ ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
   b.thr = static_cast<float*>(ws.thr.get((size_t)scan_padded_ranges(g) * sizeof(float) * 33 / 32));
   b.deq = static_cast<double*>(ws.deq.get(deq_table_entries(g) * sizeof(double)));
   b.cnt = static_cast<unsigned long long*>(ws.scan_counts.get(kScanCountSlots * sizeof(unsigned long long)));
+  if (ws.scan_counts.p != ws.counts_zeroed) {  // new status block: clear the accumulators and the ticket once
+    CK(cudaMemsetAsync(b.cnt + kAccumSlot, 0, (kScanCountSlots - kAccumSlot) * sizeof(unsigned long long), ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+    ws.counts_zeroed = ws.scan_counts.p;
+  }
   return b;
 }
 
@@ -433,8 +442,10 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
 
 // The full level plus winner selection and records.  Its list must be complete; a
 // truncated one (count > cap) is detected by the caller, which re-runs this part only.
+// snapshot: the record kernel moves the flat / shadow accumulators to the status slots (false
+// on a re-run of the full level after an overflow: the first run's snapshot stands).
 void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, size_t level,
-                   fic_mapping* d_out, cudaStream_t st) {
+                   fic_mapping* d_out, cudaStream_t st, bool snapshot = true) {
   unsigned long long* cnt = b.cnt + level * kPartSlots;
   enqueue_level(ws, d_img, g, b, 1, cnt, st);
   const bool timed = g_timing.load() != 0;
@@ -446,7 +457,8 @@ void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g,
     g_launches += 1;
   }
   launch_record(d_img, g, b.qpool, b.mi, b.rm, b.win, b.gbest, d_out, b.cnt + kSelfcheckSlot, cnt, parts,
-                b.cnt + kNeedSlot, st);
+                b.cnt + kNeedSlot, b.cnt + kAccumSlot, b.cnt + kCounterSlot, b.cnt + kTicketSlot, 2 * g.batch, snapshot,
+                st);
   g_launches += 1;
   CK(cudaGetLastError());
 }
@@ -458,13 +470,15 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   ws.list_cap_grown = std::max(ws.list_cap_grown, std::max<unsigned long long>(1ull << 22, (unsigned long long)g.R * 8 * 128));
   ws.list_cap = ws.list_cap_grown;
   if (const char* lc = std::getenv("FIC_LIST_CAP")) ws.list_cap = std::strtoull(lc, nullptr, 10);  // tests: force overflow
-  CK(cudaMemsetAsync(d_counters, 0, 2 * g.batch * sizeof(unsigned long long), st));
   // b.cnt: the scan kernels write their partitions' counters, range_op resets the pending and
-  // self-check slots, the host reads only the partitions a level used
+  // self-check slots, the host reads only the partitions a level used; the flat / shadow counts
+  // accumulate in the kAccumSlot slots, which record_kernel moves to d_counters (the kCounterSlot
+  // slots) and clears for the next encode (zeroed once when the block is allocated, scan_bufs)
+  (void)d_counters;
   const bool time_pool = g_timing.load() != 0;
   if (time_pool) CK(cudaEventRecord(ws.ev4, st));
   // K1 pool + range pass + bar / winner init + dequantised tables in one launch
-  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, d_counters, b.rm, b.gbest, b.win, b.deq, st);
+  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, b.cnt + kAccumSlot, b.rm, b.gbest, b.win, b.deq, st);
   if (time_pool) {
     CK(cudaEventRecord(ws.ev5, st));
     // algorithmic bytes: the image read once, the pool written once (fp16 operand 2K, exact
@@ -758,7 +772,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
       ws.list_cap = std::max(ws.list_cap, std::min(want, limit));
       if (!std::getenv("FIC_LIST_CAP")) ws.list_cap_grown = ws.list_cap;
     }
-    enqueue_final(ws, d_img, g, b, nl - 1, d_out, st);
+    enqueue_final(ws, d_img, g, b, nl - 1, d_out, st, false);
   }
 }
 

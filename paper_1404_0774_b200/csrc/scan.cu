@@ -2020,7 +2020,9 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
               const DomainMetaI* __restrict__ meta_i, const RangeMeta* __restrict__ rmeta,
               const unsigned __int128* __restrict__ win, const unsigned long long* __restrict__ gbest,
               fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck,
-              const unsigned long long* __restrict__ full_counts, int parts, unsigned long long* __restrict__ need) {
+              const unsigned long long* __restrict__ full_counts, int parts, unsigned long long* __restrict__ need,
+              unsigned long long* __restrict__ accum, unsigned long long* __restrict__ snap,
+              unsigned long long* __restrict__ ticket, int nslots, int snapshot) {
   // the largest full-level list partition, for the host's overflow check (one status read-back):
   // one warp, its loads in flight together
   if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -2031,7 +2033,7 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
     if (threadIdx.x == 0) *need = m;
   }
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= g.R) return;
+  if (r < g.R) {
   const RangeMeta m = rmeta[r];
   int x0, y0;
   range_origin(g, r, x0, y0);
@@ -2076,6 +2078,27 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
     o.residual = rv;
   }
   out[r] = o;
+  }
+  // The encode's flat / shadow counters accumulate (pool launch atomics) in `accum`, zero at
+  // the start of every encode: the last record block moves them to `snap` (the status slots the
+  // host reads; not on a re-run of the full level, which must keep the first snapshot) and
+  // clears them and the ticket, so no memset node has to start the next encode.
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1ull) == (unsigned long long)gridDim.x - 1ull;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int i = threadIdx.x; i < nslots; i += blockDim.x) {
+      const unsigned long long v = accum[i];
+      accum[i] = 0ull;
+      if (snapshot) snap[i] = v;
+    }
+    if (threadIdx.x == 0) *ticket = 0ull;
+  }
 }
 
 // (test support, fic_debug_correlations) the exact integer correlation sum_i q_{perm_s(i)} b_i of
@@ -2406,11 +2429,14 @@ void launch_winner(const SurvEntry* list, const unsigned long long* counts, int 
 void launch_record(const unsigned char* img, const Geometry& g, const unsigned short* qpool,
                    const DomainMetaI* meta_i, const RangeMeta* rmeta, const void* win_,
                    const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck,
-                   const unsigned long long* full_counts, int parts, unsigned long long* need, cudaStream_t st) {
+                   const unsigned long long* full_counts, int parts, unsigned long long* need,
+                   unsigned long long* accum, unsigned long long* snap, unsigned long long* ticket, int nslots,
+                   bool snapshot, cudaStream_t st) {
   const int blocks = (g.R + 63) / 64;  // 64-thread blocks: the per-range exact evaluations spread over more SMs
   const unsigned __int128* win = static_cast<const unsigned __int128*>(win_);
 #define FIC_REC(NN) \
-  record_kernel<NN><<<blocks, 64, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, need)
+  record_kernel<NN><<<blocks, 64, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, \
+                                           need, accum, snap, ticket, nslots, snapshot ? 1 : 0)
   if (g.N == 4) FIC_REC(4);
   else if (g.N == 16) FIC_REC(16);
   else FIC_REC(64);
