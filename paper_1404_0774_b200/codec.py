@@ -174,20 +174,25 @@ def encode_rows(image, row_begin, row_end, params=None):
     return out[:count], st.as_dict()
 
 
-def encode_batch(images, params=None):
-    """(extension) encode a (count, side, side) uint8 volume (up to 64 slices per encode pass;
-    each slice's codes equal its own fic_encode); returns a list of EncodedImage and the
-    summed stats."""
+def encode_batch(images, params=None, out=None):
+    """(extension) encode a (count, side, side) uint8 volume (up to 64 slices per encode pass,
+    pipelined: the next pass uploads while the current one encodes; each slice's codes equal its
+    own fic_encode); returns a list of EncodedImage (views of one record array) and the summed
+    stats.  `out`: a caller-owned MAPPING_DTYPE array of at least count*(w/n)*(h/n) records (a
+    page-locked one, like a page-locked volume, is filled by DMA directly)."""
     params = CodecParams() if params is None else params
     vol = np.ascontiguousarray(np.asarray(images), dtype=np.uint8)
     if vol.ndim != 3:
         raise ValueError("expected a 3D uint8 array (count x height x width)")
     c, h, w = vol.shape
     per = _range_count(h, w, params)
-    out = np.zeros(max(c * per, 1), MAPPING_DTYPE)
+    if out is None:
+        out = np.empty(max(c * per, 1), MAPPING_DTYPE)
+    elif out.dtype != MAPPING_DTYPE or out.ndim != 1 or len(out) < c * per or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a contiguous MAPPING_DTYPE array of at least {c * per} records")
     st = FicStats()
     _check(lib().fic_encode_batch(ptr(vol), c, w, h, ctypes.byref(params.struct), ptr(out), ctypes.byref(st)))
-    return [EncodedImage(w, h, params, out[i * per:(i + 1) * per].copy()) for i in range(c)], st.as_dict()
+    return [EncodedImage(w, h, params, out[i * per:(i + 1) * per]) for i in range(c)], st.as_dict()
 
 
 def _maps(enc):

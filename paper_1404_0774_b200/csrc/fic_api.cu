@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -241,6 +242,12 @@ struct Workspace {
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
       diag, scratch, mra, mrb, mrc, recs, rcounts, pendc, upool, qpool, win, list, res, scan_counts, ropnd, thr, deq, pend;
   HostBuf h_img, h_out, h_counters, h_raster, h_rmse, h_scan_counts;
+  // batched host encodes: the second image / record buffers of the double-buffered pipeline and
+  // the stream that uploads the next pass while the current one encodes
+  DevBuf img2, out2;
+  HostBuf h_img2, h_out2;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_up = nullptr;
   unsigned long long list_cap = 0;        // survivor-list capacity (entries) of the current encode
   unsigned long long list_cap_grown = 0;  // capacity later encodes start from (grown on overflow)
   // CUDA graphs of the scan-path encode, keyed by everything its launches bake in
@@ -254,7 +261,7 @@ struct Workspace {
     unsigned long long used = 0;
   };
   std::vector<Graph> graphs;
-  std::vector<unsigned long long> last_key;  // fingerprint of the previous eager encode
+  std::vector<std::vector<unsigned long long>> seen_keys;  // fingerprints of recent eager encodes
   unsigned long long graph_clock = 0;
   void* counts_zeroed = nullptr;  // the status block whose accumulators were cleared (scan_bufs)
   std::mutex mu;
@@ -279,6 +286,8 @@ Workspace& workspace() {
     CK(cudaEventCreate(&w->ev3));
     CK(cudaEventCreate(&w->ev4));
     CK(cudaEventCreate(&w->ev5));
+    CK(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&w->ev_up, cudaEventDisableTiming));
     g_ws[dev] = w;
   }
   return *g_ws[dev];
@@ -628,12 +637,16 @@ bool enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geome
       return rb != nullptr;
     }
   }
-  if (key != ws.last_key) {  // first sighting: eager (allocates); capture on the next one
+  // first sighting: eager (allocates); capture on the next one.  A few recent keys are kept, so
+  // encodes alternating between buffers (the batched pipeline) are captured too.
+  if (std::find(ws.seen_keys.begin(), ws.seen_keys.end(), key) == ws.seen_keys.end()) {
     enqueue_encode_scan(ws, d_img, g, b, d_out, d_counters, st);
-    ws.last_key = encode_key(ws, d_img, g, d_out, d_counters, st);  // (the eager run may have grown buffers)
-    ws.last_key.push_back(rb ? (unsigned long long)(uintptr_t)rb->hc : 0ull);
-    ws.last_key.push_back(rb ? rb->status_bytes : 0ull);
-    ws.last_key.push_back(rb && rb->h_out ? rb->out_bytes : 0ull);
+    std::vector<unsigned long long> k2 = encode_key(ws, d_img, g, d_out, d_counters, st);  // (buffers may have grown)
+    k2.push_back(rb ? (unsigned long long)(uintptr_t)rb->hc : 0ull);
+    k2.push_back(rb ? rb->status_bytes : 0ull);
+    k2.push_back(rb && rb->h_out ? rb->out_bytes : 0ull);
+    ws.seen_keys.push_back(std::move(k2));
+    if (ws.seen_keys.size() > 4) ws.seen_keys.erase(ws.seen_keys.begin());
     return false;
   }
   const unsigned long long l0 = g_launches.load();
@@ -690,7 +703,8 @@ bool enqueue_encode_graph(Workspace& ws, const unsigned char* d_img, const Geome
 // h_counters; batch == 1 for a single image).
 void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in, fic_mapping* d_out,
                 unsigned long long* d_counters, unsigned long long* h_counters, cudaStream_t st,
-                fic_mapping* h_out = nullptr) {
+                fic_mapping* h_out = nullptr, const std::function<void()>& overlap = {}) {
+  // overlap: host work run once while this encode executes (before its synchronisation)
   // h_out: the records are also copied to this (pinned) host buffer before the one synchronisation
   // (again after an overflow re-run), so a host-API encode waits for the device once
   Geometry g = g_in;
@@ -701,6 +715,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
     if (h_counters)
       CK(cudaMemcpyAsync(h_counters, d_counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     if (h_out) CK(cudaMemcpyAsync(h_out, d_out, (size_t)g.R * sizeof(fic_mapping), cudaMemcpyDeviceToHost, st));
+    if (overlap) overlap();
     CK(cudaStreamSynchronize(st));
     return;
   }
@@ -724,6 +739,7 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
       else
         enqueue_readback(rb, b, d_out, st);
     }
+    if (attempt == 0 && overlap) overlap();
     CK(cudaStreamSynchronize(st));
     if (h_counters) std::memcpy(h_counters, hc + kCounterSlot, 2 * g.batch * sizeof(unsigned long long));
     const std::vector<int> lv = scan_levels(g);
@@ -877,6 +893,74 @@ void upload_image(Workspace& ws, const uint8_t* image, unsigned char* d_img, siz
   CK(cudaMemcpyAsync(d_img, src, bytes, cudaMemcpyHostToDevice, ws.stream));
 }
 
+// Batched host encode, pipelined over its passes (up to batch_chunk slices each): while pass c
+// encodes, the host stages pass c+1's slices into the other pinned buffer and a copy stream
+// uploads them into the other device image buffer, and pass c-1's records are copied out of
+// their pinned buffer.  Records and stats equal per-pass encode_host calls.
+int32_t encode_batch_host(const uint8_t* images, const Geometry& g1, int count, fic_mapping* out, fic_stats* stats) {
+  return guarded([&]() -> int32_t {
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lock(ws.mu);
+    const int chunk = batch_chunk(g1);
+    const int passes = (count + chunk - 1) / chunk;
+    const size_t slice_bytes = (size_t)g1.W * g1.H;
+    const size_t img_bytes = slice_bytes * std::min(chunk, count);
+    const size_t out_recs = (size_t)g1.R * std::min(chunk, count);
+    unsigned char* d_img[2] = {static_cast<unsigned char*>(ws.img.get(img_bytes)),
+                               static_cast<unsigned char*>(passes > 1 ? ws.img2.get(img_bytes) : nullptr)};
+    fic_mapping* d_out[2] = {static_cast<fic_mapping*>(ws.out.get(out_recs * sizeof(fic_mapping))),
+                             static_cast<fic_mapping*>(passes > 1 ? ws.out2.get(out_recs * sizeof(fic_mapping)) : nullptr)};
+    fic_mapping* h_out[2] = {static_cast<fic_mapping*>(ws.h_out.get(out_recs * sizeof(fic_mapping))),
+                             static_cast<fic_mapping*>(passes > 1 ? ws.h_out2.get(out_recs * sizeof(fic_mapping)) : nullptr)};
+    const bool src_pinned = host_pinned(images);
+    const bool out_pinned = host_pinned(out);  // records DMA'd straight into the caller's buffer
+    unsigned char* h_img[2] = {src_pinned ? nullptr : static_cast<unsigned char*>(ws.h_img.get(img_bytes)),
+                               src_pinned || passes < 2 ? nullptr : static_cast<unsigned char*>(ws.h_img2.get(img_bytes))};
+    auto* d_cnt = static_cast<unsigned long long*>(ws.counters.get(2 * 64 * sizeof(unsigned long long)));
+    auto* h_cnt = static_cast<unsigned long long*>(ws.h_counters.get(2 * 64 * sizeof(unsigned long long)));
+    auto slices = [&](int c) { return std::min(chunk, count - c * chunk); };
+    // pass c's slices -> d_img[c % 2] on the copy stream (staged through pinned memory unless the
+    // caller's volume is pinned); the encode stream waits for it
+    auto upload = [&](int c) {
+      const size_t bytes = slice_bytes * slices(c);
+      const uint8_t* src = images + (size_t)c * chunk * slice_bytes;
+      if (!src_pinned) {
+        std::memcpy(h_img[c % 2], src, bytes);
+        src = h_img[c % 2];
+      }
+      CK(cudaMemcpyAsync(d_img[c % 2], src, bytes, cudaMemcpyHostToDevice, ws.copy_stream));
+      CK(cudaEventRecord(ws.ev_up, ws.copy_stream));
+    };
+    auto emit = [&](int c) {  // pass c's records, from its pinned buffer to the caller's
+      if (!out_pinned)
+        std::memcpy(out + (size_t)c * chunk * g1.R, h_out[c % 2], (size_t)slices(c) * g1.R * sizeof(fic_mapping));
+    };
+    fic_stats total{0, 0, 0};
+    upload(0);
+    for (int c = 0; c < passes; ++c) {
+      CK(cudaStreamWaitEvent(ws.stream, ws.ev_up, 0));  // pass c's slices are on the device
+      const Geometry g = batch_geometry(g1, slices(c));
+      fic_mapping* dst = out_pinned ? out + (size_t)c * chunk * g1.R : h_out[c % 2];
+      run_encode(ws, d_img[c % 2], g, d_out[c % 2], d_cnt, h_cnt, ws.stream, dst, [&]() {
+        if (c + 1 < passes) upload(c + 1);  // (pass c-1, which read that buffer, has finished)
+        if (c > 0) emit(c - 1);
+      });
+      collect_timing(ws);
+      fic_stats s{0, 0, 0};
+      if (g.batch > 1)
+        fill_stats_batch(&s, g, h_cnt);
+      else
+        fill_stats(&s, g, h_cnt[0], h_cnt[1]);
+      total.candidates_tested += s.candidates_tested;
+      total.shadow_ranges += s.shadow_ranges;
+      total.shadow_codeblocks += s.shadow_codeblocks;
+    }
+    emit(passes - 1);
+    if (stats) *stats = total;
+    return FIC_OK;
+  });
+}
+
 // Encode `g` of the host image into host `out` (g.R records).
 int32_t encode_host(const uint8_t* image, const Geometry& g, fic_mapping* out, fic_stats* stats) {
   return guarded([&]() -> int32_t {
@@ -1028,19 +1112,11 @@ int32_t fic_encode_batch(const uint8_t* images, int32_t count, int32_t width, in
   if (count < 0) return fail(FIC_ERR_BAD_PARAMS, "negative batch size");
   if (count > 0 && (!images || !out)) return fail(FIC_ERR_BAD_PARAMS, "null buffer");
   const Geometry g = make_geometry(width, height, p);
-  fic_stats total{0, 0, 0};
-  const int chunk = batch_chunk(g);
-  for (int i = 0; i < count; i += chunk) {
-    const int k = std::min(chunk, count - i);
-    fic_stats s{0, 0, 0};
-    e = encode_host(images + (size_t)i * width * height, batch_geometry(g, k), out + (size_t)i * g.R, &s);
-    if (e) return e;
-    total.candidates_tested += s.candidates_tested;
-    total.shadow_ranges += s.shadow_ranges;
-    total.shadow_codeblocks += s.shadow_codeblocks;
+  if (count == 0) {
+    if (stats) *stats = fic_stats{0, 0, 0};
+    return FIC_OK;
   }
-  if (stats) *stats = total;
-  return FIC_OK;
+  return encode_batch_host(images, g, count, out, stats);
 }
 
 // Encode `count` slices already resident on the device (d_images: count x height x width,

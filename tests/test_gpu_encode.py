@@ -539,3 +539,29 @@ def test_near_threshold_candidates(oracle, acc):
                 enc = fic.encode(img, fic.CodecParams(**pv))
             assert_same(enc.mappings, want, f"near-threshold acc={acc} sel={sel} {pv}")
             assert enc.stats == st
+
+
+@pytest.mark.gpu
+def test_batch_pipelined_caller_buffers(oracle):
+    """encode_batch over several passes (FIC_BATCH_CHUNK=2: 5 slices = 3 pipelined passes),
+    with page-locked volume and record buffers and with pageable ones: the same records as
+    per-slice encodes, equal to the oracle on sampled slices."""
+    import torch
+
+    from paper_1404_0774_b200.abi import MAPPING_DTYPE
+
+    vol = np.stack([images.ct_slice(128, 1404100 + i, 0.3) for i in range(5)])
+    p = fic.CodecParams(n=8, step=4)
+    per = (128 // 8) ** 2
+    want = [fic.encode(s, p).mappings for s in vol]
+    pin_vol = torch.empty(vol.shape, dtype=torch.uint8, pin_memory=True).numpy()
+    pin_vol[:] = vol
+    pin_out = torch.empty(5 * per * 32, dtype=torch.uint8, pin_memory=True).numpy().view(MAPPING_DTYPE)
+    with env(FIC_BATCH_CHUNK=2):
+        for src, out in ((vol, None), (pin_vol, pin_out), (pin_vol, None), (vol, pin_out)):
+            encs, st = fic.encode_batch(src, p, out=out)
+            for i, e in enumerate(encs):
+                assert_same(e.mappings, want[i], f"slice {i}")
+    for i in (0, 4):
+        w, _ = oracle.encode(vol[i], dict(n=8, step=4))
+        assert_same(want[i], w, f"oracle slice {i}")
