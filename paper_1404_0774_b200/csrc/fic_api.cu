@@ -363,6 +363,10 @@ std::vector<int> scan_levels(const Geometry& g) {
     // (measured: cfg2 {4} 0.56 ms vs {64, 8} 0.61; cfg3 {32, 4} 3.09 vs {64, 8} 3.65).
     std::vector<int> rev;
     for (int s = 4; tiles >= 8 * s; s *= 8) rev.push_back(s);
+    // a last level short enough for per-lane bests at stride 3 (<= 48 level tiles) gives a
+    // better bar for a few more tiles: cfg2 {3} 0.271 vs {4} 0.278 ms (cfg3's stride-4 level
+    // is hit-first; {32, 3} there measured slower)
+    if (!rev.empty() && (tiles + 2) / 3 <= 48) rev[0] = 3;
     lv.assign(rev.rbegin(), rev.rend());
   }
   // the host keeps kMaxLevels counter partitions (sparse levels + the full one): an override
