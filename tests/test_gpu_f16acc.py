@@ -32,6 +32,9 @@ def test_f16_accumulator_matches_bound_assumptions(tmp_path):
     # fp16 accumulation: (K/16) roundings of at most 2^-11 |u||b| each (the bound adds the first
     # K/16 - 1 this way and the last one relative to the result, which is smaller)
     assert e16 <= (K // 16) * 2.0 ** -11 * 1.05 + K * 2.0 ** -21, out
+    # 16 products inside one step: summed, then rounded once (each within the bound)
+    m = re.search(r"many-term step: exact-then-round (\d+), per-product rounding \d+, within the bound (\d+) of (\d+)", out)
+    assert m and m.group(2) == m.group(3), out
     for k2 in (1, 16):  # round to nearest even, inside a K=16 step and across steps
         m = re.search(rf"rounding probe \(second term at k={k2}\): matches RNE (\d+), RZ \d+, neither (\d+) of (\d+)",
                       out)

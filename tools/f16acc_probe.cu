@@ -201,6 +201,38 @@ int main() {
     }
     std::printf("rounding probe (second term at k=%d): matches RNE %d, RZ %d, neither %d of %d\n", k2, rn, rz, other, M);
   }
+  // many terms inside ONE K=16 step: row m sums 1.0 and 15 copies of c_m = (m+1) 2^-16, each
+  // below half an fp16 ulp of the running sum for small m.  Exact-then-round (what the pruning
+  // bound assumes: one rounding per step, relative to the result, plus a K 2^-21 allowance)
+  // gives fl16(1 + 15 c_m); rounding after every product would leave 1.0.
+  {
+    for (auto& h : hA) h = __float2half(0.f);
+    for (auto& h : hB) h = __float2half(0.f);
+    for (int m = 0; m < M; ++m) {
+      hA[core_off(m, 0)] = __float2half(1.f);
+      for (int k = 1; k < 16; ++k) hA[core_off(m, k)] = __float2half((float)(m + 1) * 0x1p-16f);
+    }
+    for (int k = 0; k < 16; ++k) hB[core_off(0, k)] = __float2half(1.f);
+    cudaMemcpy(dA, hA.data(), M * K * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, hB.data(), N * K * 2, cudaMemcpyHostToDevice);
+    probe<<<1, 128, smem>>>(dA, dB, d32, d16, d16p);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h16.data(), d16, M * N * 4, cudaMemcpyDeviceToHost);
+    int exact_round = 0, per_product = 0, within_bound = 0;
+    for (int m = 0; m < M; ++m) {
+      const double c = (double)(m + 1) * 0x1p-16, ex = 1.0 + 15.0 * c;
+      __half_raw hr;
+      hr.x = (unsigned short)(h16[m * N] & 0xFFFF);
+      const double got = __half2float(__half(hr));
+      exact_round += got == (double)__half2float(__float2half_rn((float)ex));
+      float seq = 1.f;
+      for (int k = 1; k < 16; ++k) seq = __half2float(__float2half_rn(seq + (float)c));
+      per_product += got == (double)seq;
+      within_bound += std::fabs(got - ex) <= std::ldexp(1.0, -11) * std::fabs(ex) + 16 * std::ldexp(1.0, -21) * ex;
+    }
+    std::printf("many-term step: exact-then-round %d, per-product rounding %d, within the bound %d of %d\n",
+                exact_round, per_product, within_bound, M);
+  }
   std::printf("reference: 2^-11 = %.3e, 4 * 2^-11 = %.3e, 64 * 2^-11 = %.3e\n", std::ldexp(1.0, -11),
               4 * std::ldexp(1.0, -11), 64 * std::ldexp(1.0, -11));
   return 0;
