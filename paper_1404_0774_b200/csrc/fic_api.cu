@@ -367,6 +367,10 @@ std::vector<int> scan_levels(const Geometry& g) {
     // better bar for a few more tiles: cfg2 {3} 0.271 vs {4} 0.278 ms (cfg3's stride-4 level
     // is hit-first; {32, 3} there measured slower)
     if (!rev.empty() && (tiles + 2) / 3 <= 48) rev[0] = 3;
+    // pools too small for a stride-4 level with 8 tiles still get one at stride 3 (from 6
+    // tiles): its per-lane bests give the full level a bar the local seed cannot (cfg1, 30
+    // tiles: 0.233 -> 0.101 ms)
+    if (rev.empty() && tiles >= 6) rev.push_back(3);
     lv.assign(rev.rbegin(), rev.rend());
   }
   // the host keeps kMaxLevels counter partitions (sparse levels + the full one): an override
@@ -506,7 +510,7 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   // so they skip it: cfg2 0.335 / 0.337 / 0.344 ms without / with a 1 x 1 / 3 x 3 seed, cfg3
   // 2.456 / 2.447 / 2.462 ms (within noise), one launch fewer.  FIC_SEED=0 / 1 / 3 forces none /
   // 1 x 1 / 3 x 3.
-  // Without any sparse level (pools under 32 tiles, cfg1) the seed is the full level's only bar.
+  // Without any sparse level (pools under 6 tiles) the seed is the full level's only bar.
   const char* seed_env = std::getenv("FIC_SEED");
   const int seed_side =
       seed_env ? std::atoi(seed_env) : (scan_tiles(g) > 1024 || scan_levels(g).size() == 1 ? 3 : 0);
