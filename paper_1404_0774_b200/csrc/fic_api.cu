@@ -85,7 +85,7 @@ void launch_winner(const uint2*, const unsigned long long*, int, unsigned long l
 void launch_record(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
                    const RangeMeta*, const void*, const unsigned long long*, fic_mapping*, unsigned long long*,
                    const unsigned long long*, int, unsigned long long*, unsigned long long*, unsigned long long*,
-                   unsigned long long*, int, bool, cudaStream_t);
+                   unsigned long long*, int, bool, unsigned long long*, int, int, cudaStream_t);
 void launch_probe_corr(const unsigned char*, const Geometry&, const unsigned short*, int, const int*, const int*,
                        const int*, long long*, cudaStream_t);
 }  // namespace ficb
@@ -264,6 +264,9 @@ struct Workspace {
   std::vector<std::vector<unsigned long long>> seen_keys;  // fingerprints of recent eager encodes
   unsigned long long graph_clock = 0;
   void* counts_zeroed = nullptr;  // the status block whose accumulators were cleared (scan_bufs)
+  // device alias of the page-locked status copy (h_scan_counts + kSelfcheckSlot): record_kernel
+  // writes the status there directly (null: the status is read back by a copy)
+  unsigned long long* hstat_dev = nullptr;
   std::mutex mu;
 };
 
@@ -475,7 +478,7 @@ void enqueue_final(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   }
   launch_record(d_img, g, b.qpool, b.mi, b.rm, b.win, b.gbest, d_out, b.cnt + kSelfcheckSlot, cnt, parts,
                 b.cnt + kNeedSlot, b.cnt + kAccumSlot, b.cnt + kCounterSlot, b.cnt + kTicketSlot, 2 * g.batch, snapshot,
-                st);
+                ws.hstat_dev, kNeedSlot - kSelfcheckSlot, kCounterSlot - kSelfcheckSlot, st);
   g_launches += 1;
   CK(cudaGetLastError());
 }
@@ -610,7 +613,8 @@ struct Readback {
 };
 
 void enqueue_readback(const Readback& rb, const ScanBufs& b, const fic_mapping* d_out, cudaStream_t st) {
-  CK(cudaMemcpyAsync(rb.hc + kSelfcheckSlot, b.cnt + kSelfcheckSlot, rb.status_bytes, cudaMemcpyDeviceToHost, st));
+  if (rb.status_bytes)  // (0: record_kernel wrote the status into the page-locked copy itself)
+    CK(cudaMemcpyAsync(rb.hc + kSelfcheckSlot, b.cnt + kSelfcheckSlot, rb.status_bytes, cudaMemcpyDeviceToHost, st));
   if (rb.h_out) CK(cudaMemcpyAsync(rb.h_out, d_out, rb.out_bytes, cudaMemcpyDeviceToHost, st));
 }
 
@@ -734,8 +738,19 @@ void run_encode(Workspace& ws, const unsigned char* d_img, const Geometry& g_in,
   d_counters = b.cnt + kCounterSlot;  // flat / shadow counters live in the status block
   // every level's partition counters only for the survivor statistics (timed / diagnostic encodes)
   const bool all_counts = g_timing.load() != 0 || (g.flags & 4);
-  const Readback rb{hc, (kCounterSlot - kSelfcheckSlot + 2 * g.batch) * sizeof(unsigned long long), h_out,
-                    (size_t)g.R * sizeof(fic_mapping)};
+  // the status tail straight from record_kernel into hc (mapped page-locked memory) unless this
+  // encode reads the whole block back anyway
+  {
+    unsigned long long* dev = nullptr;
+    if (!all_counts && !std::getenv("FIC_STATUS_COPY") &&
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), hc + kSelfcheckSlot, 0) != cudaSuccess) {
+      (void)cudaGetLastError();
+      dev = nullptr;
+    }
+    ws.hstat_dev = all_counts ? nullptr : dev;
+  }
+  const Readback rb{hc, ws.hstat_dev ? 0 : (kCounterSlot - kSelfcheckSlot + 2 * g.batch) * sizeof(unsigned long long),
+                    h_out, (size_t)g.R * sizeof(fic_mapping)};
   const bool in_graph = enqueue_encode_graph(ws, d_img, g, b, d_out, d_counters, st, all_counts ? nullptr : &rb);
   for (int attempt = 0;; ++attempt) {
     // one read-back of the status block (and the records of a host-API encode), one synchronisation

@@ -2022,7 +2022,8 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
               fic_mapping* __restrict__ out, unsigned long long* __restrict__ selfcheck,
               const unsigned long long* __restrict__ full_counts, int parts, unsigned long long* __restrict__ need,
               unsigned long long* __restrict__ accum, unsigned long long* __restrict__ snap,
-              unsigned long long* __restrict__ ticket, int nslots, int snapshot) {
+              unsigned long long* __restrict__ ticket, int nslots, int snapshot,
+              volatile unsigned long long* __restrict__ hstat, int need_off, int cnt_off) {
   // the largest full-level list partition, for the host's overflow check (one status read-back):
   // one warp, its loads in flight together
   if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -2095,9 +2096,21 @@ record_kernel(const unsigned char* __restrict__ img, Geometry g, const unsigned 
     for (int i = threadIdx.x; i < nslots; i += blockDim.x) {
       const unsigned long long v = accum[i];
       accum[i] = 0ull;
-      if (snapshot) snap[i] = v;
+      if (snapshot) {
+        snap[i] = v;
+        if (hstat) hstat[cnt_off + i] = v;
+      }
     }
-    if (threadIdx.x == 0) *ticket = 0ull;
+    if (threadIdx.x == 0) {
+      *ticket = 0ull;
+      // the status the host checks, written straight into its page-locked copy (no read-back
+      // copy): self-check count and the largest full-level partition
+      if (hstat) {
+        hstat[0] = *(volatile unsigned long long*)selfcheck;
+        hstat[need_off] = *(volatile unsigned long long*)need;
+      }
+    }
+    if (hstat) __threadfence_system();
   }
 }
 
@@ -2431,12 +2444,12 @@ void launch_record(const unsigned char* img, const Geometry& g, const unsigned s
                    const unsigned long long* gbest, fic_mapping* out, unsigned long long* selfcheck,
                    const unsigned long long* full_counts, int parts, unsigned long long* need,
                    unsigned long long* accum, unsigned long long* snap, unsigned long long* ticket, int nslots,
-                   bool snapshot, cudaStream_t st) {
+                   bool snapshot, unsigned long long* hstat, int need_off, int cnt_off, cudaStream_t st) {
   const int blocks = (g.R + 63) / 64;  // 64-thread blocks: the per-range exact evaluations spread over more SMs
   const unsigned __int128* win = static_cast<const unsigned __int128*>(win_);
 #define FIC_REC(NN) \
   record_kernel<NN><<<blocks, 64, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, \
-                                           need, accum, snap, ticket, nslots, snapshot ? 1 : 0)
+                                           need, accum, snap, ticket, nslots, snapshot ? 1 : 0, hstat, need_off, cnt_off)
   if (g.N == 4) FIC_REC(4);
   else if (g.N == 16) FIC_REC(16);
   else FIC_REC(64);
