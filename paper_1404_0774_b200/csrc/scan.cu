@@ -1047,6 +1047,8 @@ struct WarpRecAppender {
   uint32_t left;
   uint32_t cur;      // first record of the warp's current chunk (kSentinel: none)
   EvalRing* ring;    // fused scan: finished chunks are published to the consumers
+  MaskRec* next = nullptr;  // record `base` (valid while base < cap): advanced by one per put,
+                            // so a put is two stores and no 64-bit index arithmetic
 
   // Warp-uniform: every lane passes its mask (0 for none).
   __device__ __forceinline__ void put(uint32_t bits, uint32_t r8, uint32_t d0) {
@@ -1058,12 +1060,13 @@ struct WarpRecAppender {
       base = __shfl_sync(0xffffffffu, nb, 0);
       cur = base;
       left = kRecChunk;
+      next = recs + base;
     }
     if (base < cap) {
-      MaskRec* rc = recs + base;
-      if (lane == 0) *reinterpret_cast<uint2*>(rc) = make_uint2(r8, d0);
-      rc->m[lane] = (uint8_t)bits;
+      if (lane == 0) *reinterpret_cast<uint2*>(next) = make_uint2(r8, d0);
+      next->m[lane] = (uint8_t)bits;
     }
+    ++next;
     ++base;
     --left;
   }
@@ -1502,24 +1505,31 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             }
             continue;
           }
-          if (MB == 1 && !allpass) {
-            __half2 m0 = __habs2(h[0]), m1 = __habs2(h[1]);
+          // per range: one 3-input and one 2-input half2 |max|
+          __half2 mxr[kEpiRanges];
 #pragma unroll
-            for (int c = 2; c < kEpiCols / 2; c += 4) {
-              m0 = __hmax2(m0, __hmax2(__habs2(h[c]), __habs2(h[c + 1])));
-              m1 = __hmax2(m1, __hmax2(__habs2(h[c + 2]), __habs2(h[c + 3])));
+          for (int k = 0; k < kEpiRanges; ++k)
+            mxr[k] = __hmax2(__hmax2(__hmax2(__habs2(h[4 * k]), __habs2(h[4 * k + 1])), __habs2(h[4 * k + 2])),
+                             __habs2(h[4 * k + 3]));
+          if (MB == 1 && !allpass) {
+            // whole-tile vote on the ranges' maxima (a 3-input tree: kEpiRanges / 2 more
+            // instructions); the per-range compares only for tiles where some lane hits
+            __half2 t[kEpiRanges];
+#pragma unroll
+            for (int k = 0; k < kEpiRanges; ++k) t[k] = mxr[k];
+#pragma unroll
+            for (int w = kEpiRanges; w > 1; w = (w + 1) / 2) {
+#pragma unroll
+              for (int k = 0; k < w / 2; ++k) t[k] = __hmax2(t[2 * k], t[2 * k + 1]);
+              if (w & 1) t[w / 2] = t[w - 1];
             }
-            if (!__any_sync(0xffffffffu, __hgt2_mask(__hmax2(m0, m1), one2) != 0u)) continue;
+            if (!__any_sync(0xffffffffu, __hgt2_mask(t[0], one2) != 0u)) continue;
           }
-          // per range: one 3-input and one 2-input half2 |max|, one half2 compare (a 0xFFFF mask
-          // per half) and one masked OR; both halves folded once at the end
+          // per range one half2 compare (a 0xFFFF mask per half) and one masked OR; both halves
+          // folded once at the end
           uint32_t g2 = 0u;
 #pragma unroll
-          for (int k = 0; k < kEpiRanges; ++k) {
-            const __half2 mx = __hmax2(__hmax2(__hmax2(__habs2(h[4 * k]), __habs2(h[4 * k + 1])), __habs2(h[4 * k + 2])),
-                                       __habs2(h[4 * k + 3]));
-            g2 |= __hgt2_mask(mx, one2) & (0x00010001u << k);
-          }
+          for (int k = 0; k < kEpiRanges; ++k) g2 |= __hgt2_mask(mxr[k], one2) & (0x00010001u << k);
           const uint32_t gmask = ((g2 | (g2 >> 16)) & ((1u << kEpiRanges) - 1u)) | allpass;
           const uint32_t groups = __reduce_or_sync(0xffffffffu, gmask);
           if constexpr (MB == 2) {
