@@ -234,6 +234,9 @@ void fic_set_matcher_timing(int32_t enabled);
 /* Average device time (ms) of the full-level tcgen05 scan kernel alone (the dominant kernel:
  * every range x domain x isometry correlation of the encode) and the number of timed launches. */
 int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset);
+/* The same launches timed from before the scan kernel to after its expand_kernel (the mask
+ * records turned into survivor entries).  Reading either accumulator with reset clears both. */
+int32_t fic_scan_expand_timing(double* avg_ms, uint64_t* launches, int32_t reset);
 /* Device time (ms) of the decode iterations of fic_decode calls without a convergence test
  * (decode_step kernels with the fused step-RMSE partials), their algorithmic bytes
  * (16 B per output pixel and iteration: the next raster written, the current one read) and

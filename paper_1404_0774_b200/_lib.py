@@ -48,6 +48,7 @@ def _declare(L):
     L.fic_matcher_timing.argtypes = [vp, vp, i32]
     L.fic_set_matcher_timing.argtypes = [i32]
     L.fic_scan_timing.argtypes = [vp, vp, i32]
+    L.fic_scan_expand_timing.argtypes = [vp, vp, i32]
     L.fic_last_survivors.argtypes = [vp, i32]
     L.fic_debug_trace.argtypes = [vp, i32]
     L.fic_decode_timing.argtypes = [vp, vp, vp, i32]
@@ -63,7 +64,7 @@ def _declare(L):
                  "fic_encode_range", "fic_encode_rows", "fic_encode_batch", "fic_encode_device",
                  "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
                  "fic_matcher_timing", "fic_set_device", "fic_device_count", "fic_scan_timing",
-                 "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace",
+                 "fic_scan_expand_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device", "fic_debug_trace",
                  "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
                  "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device", "fic_record_layout",
                  "fic_serialize", "fic_serialize_device", "fic_deserialize"]:
@@ -91,7 +92,7 @@ EXPORTS = [
     "fic_encode", "fic_encode_parallel", "fic_encode_range", "fic_encode_rows", "fic_encode_batch",
     "fic_encode_device", "fic_decode_step", "fic_decode", "fic_collage_error", "fic_decoded_error_bound",
     "fic_kernel_launch_count", "fic_matcher_timing", "fic_set_matcher_timing", "fic_set_device",
-    "fic_device_count", "fic_scan_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
+    "fic_device_count", "fic_scan_timing", "fic_scan_expand_timing", "fic_last_survivors", "fic_decode_timing", "fic_encode_batch_device",
     "fic_debug_trace", "fic_is_shadow", "fic_least_squares_fit", "fic_least_squares_clamped", "fic_least_squares",
     "fic_debug_pool", "fic_pool_timing", "fic_encode_rows_device", "fic_record_layout", "fic_serialize",
     "fic_serialize_device", "fic_deserialize",

@@ -444,6 +444,14 @@ def scan_timing(reset=False):
     return ms.value, n.value
 
 
+def scan_expand_timing(reset=False):
+    """(extension) (average ms of the full-level scan kernel + its expand_kernel, timed launches)."""
+    ms = ctypes.c_double()
+    n = ctypes.c_uint64()
+    lib().fic_scan_expand_timing(ctypes.byref(ms), ctypes.byref(n), int(reset))
+    return ms.value, n.value
+
+
 def decode_timing(reset=False):
     """(extension) (average ms, average algorithmic bytes, timed calls) of the decode iterations."""
     ms = ctypes.c_double()

@@ -55,7 +55,8 @@ bool scan_supported(const Geometry&);
 int scan_tiles(const Geometry&);
 long long scan_pool_domains(const Geometry&);
 void launch_pool_v3(const unsigned char*, const Geometry&, __half*, unsigned short*, DomainMetaI*,
-                    unsigned long long*, RangeMeta*, unsigned long long*, void*, double*, cudaStream_t);
+                    unsigned long long*, RangeMeta*, unsigned long long*, void*, double*, cudaStream_t,
+                    float* = nullptr, unsigned char* = nullptr, unsigned long long* = nullptr);
 void launch_fill_u64(unsigned long long*, long long, unsigned long long, cudaStream_t);
 void launch_seed_v3(const unsigned char*, const Geometry&, const unsigned short*, const DomainMetaI*,
                     const RangeMeta*, unsigned long long*, const double*, int, cudaStream_t);
@@ -65,7 +66,7 @@ int scan_grid(const Geometry&, int, int);
 cudaError_t launch_scan(const unsigned char*, const Geometry&, int, int, const __half*, const RangeMeta*,
                         const unsigned char*, const float*, uint2*, unsigned long long*, unsigned long long, void*,
                         unsigned long long*, const unsigned short*, const DomainMetaI*, unsigned long long*, void*,
-                        const double*, bool, cudaStream_t);
+                        const double*, bool, cudaStream_t, cudaEvent_t);
 bool scan_fused();
 int scan_level_launches(const Geometry&, int, int, bool);
 size_t scan_rec_bytes(unsigned long long, int);
@@ -108,6 +109,7 @@ double g_timing_ms = 0.0;
 unsigned long long g_timing_n = 0;
 double g_scan_ms = 0.0;            // the full-level scan kernel alone
 unsigned long long g_scan_n = 0;
+double g_scan_expand_ms = 0.0;     // the full-level scan kernel + expand_kernel
 double g_decode_ms = 0.0;          // decode iterations (decode_step + RMSE partials), device time
 unsigned long long g_decode_n = 0;
 double g_decode_bytes = 0.0;       // their algorithmic bytes
@@ -236,7 +238,7 @@ struct Workspace {
   int device = -1;
   int sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr, ev5 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr, ev4 = nullptr, ev5 = nullptr, ev6 = nullptr;
   bool scan_timed = false;
   double pool_bytes = 0.0;  // > 0: ev4/ev5 bracket a pool build of this many algorithmic bytes
   DevBuf img, pool, meta_f, meta_i, rmeta, partials, out, counters, xf, ra, rb, partial_sums, rmse, u8out, gbest,
@@ -287,6 +289,7 @@ Workspace& workspace() {
     CK(cudaEventCreate(&w->ev1));
     CK(cudaEventCreate(&w->ev2));
     CK(cudaEventCreate(&w->ev3));
+    CK(cudaEventCreate(&w->ev6));
     CK(cudaEventCreate(&w->ev4));
     CK(cudaEventCreate(&w->ev5));
     CK(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
@@ -421,7 +424,7 @@ ScanBufs scan_bufs(Workspace& ws, const Geometry& g) {
 // One scan level: tensor-core scan appending survivors to per-CTA list partitions, then
 // their exact evaluation.  cnt: the level's kPartSlots counters.
 void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g, const ScanBufs& b, int stride,
-                   unsigned long long* cnt, cudaStream_t st) {
+                   unsigned long long* cnt, cudaStream_t st, bool ops_prebuilt = false) {
   auto* list = static_cast<uint2*>(ws.list.get((size_t)ws.list_cap * sizeof(uint2)));
   auto* res = static_cast<double*>(ws.res.get((size_t)ws.list_cap * sizeof(double)));
   const int parts = scan_grid(g, stride, ws.sms);
@@ -436,20 +439,22 @@ void enqueue_level(Workspace& ws, const unsigned char* d_img, const Geometry& g,
   // thresholds and its scan)
   Geometry gl = g;
   gl.flags = scan_use_f16acc(g, stride, ws.sms, scan_levels(g).size() > 1) ? (g.flags | 256) : (g.flags & ~256);
-  launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, b.cnt + kPendSlot, final_level,
-                   final_level ? b.cnt + kSelfcheckSlot : nullptr, st);
+  // (the first level of an encode without a seed: built by the pool launch, no bar yet)
+  if (!ops_prebuilt)
+    launch_level_ops(d_img, gl, b.rm, b.gbest, b.thr, b.ropnd, b.cnt + kPendSlot, final_level,
+                     final_level ? b.cnt + kSelfcheckSlot : nullptr, st);
   const bool time_scan = stride == 1 && g_timing.load() != 0;
   if (time_scan) CK(cudaEventRecord(ws.ev2, st));
   void* recs = ws.recs.get(scan_rec_bytes(ws.list_cap, parts));
   auto* rcnt = static_cast<unsigned long long*>(ws.rcounts.get(kPartSlots * sizeof(unsigned long long)));
   const bool fused = scan_fused();
   CK(launch_scan(d_img, gl, stride, ws.sms, b.upool, b.rm, b.ropnd, b.thr, list, cnt, part, recs, rcnt, b.qpool,
-                 b.mi, b.gbest, b.win, b.deq, fused, st));
+                 b.mi, b.gbest, b.win, b.deq, fused, st, time_scan ? ws.ev6 : nullptr));
   if (time_scan) {
     CK(cudaEventRecord(ws.ev3, st));
     ws.scan_timed = true;
   }
-  g_launches += 1 + scan_level_launches(g, stride, ws.sms, fused);  // level ops, scan (+ expand)
+  g_launches += (ops_prebuilt ? 0 : 1) + scan_level_launches(g, stride, ws.sms, fused);  // level ops, scan (+ expand)
   if (fused) return;  // the scan evaluated its survivors itself
   const bool inl = eval_inline();
   // sparse levels only lower the bar: closed-form upper bounds (FIC_SPARSE_EXACT=1: exact residuals)
@@ -496,17 +501,6 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   // slots) and clears for the next encode (zeroed once when the block is allocated, scan_bufs)
   (void)d_counters;
   const bool time_pool = g_timing.load() != 0;
-  if (time_pool) CK(cudaEventRecord(ws.ev4, st));
-  // K1 pool + range pass + bar / winner init + dequantised tables in one launch
-  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, b.cnt + kAccumSlot, b.rm, b.gbest, b.win, b.deq, st);
-  if (time_pool) {
-    CK(cudaEventRecord(ws.ev5, st));
-    // algorithmic bytes: the image read once, the pool written once (fp16 operand 2K, exact
-    // cells 8 x N u16, meta 16 B per padded domain), and the preparations riding in the same
-    // launch: per range its N pixels read, RangeMeta (16 B), bar (8 B) and winner key (16 B)
-    const double Dt = (double)g.Dt * g.batch;
-    ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0) + (double)g.R * (g.N + 40.0);
-  }
   // The local seed gives the first scan level a bar (upper bounds of the range's 3 x 3 local
   // self-similar candidates) for large pools.  Small pools (<= 1024 tiles) start with a
   // per-lane-best selection level that keeps nearly every lane's best column whatever the bar,
@@ -518,11 +512,31 @@ void enqueue_encode_scan(Workspace& ws, const unsigned char* d_img, const Geomet
   const int seed_side =
       seed_env ? std::atoi(seed_env) : (scan_tiles(g) > 1024 || scan_levels(g).size() == 1 ? 3 : 0);
   const bool seed = seed_side > 0;
+  const std::vector<int> lv = scan_levels(g);
+  // without a seed the first (sparse) level scans with no bar: its range operands do not depend
+  // on any evaluation and are built by the pool launch (one launch fewer; FIC_PREOPS=0: off)
+  const char* pre_env = std::getenv("FIC_PREOPS");
+  const bool pre_ops = !seed && lv.size() > 1 && lv[0] != 1 && !(pre_env && pre_env[0] == '0');
+  if (time_pool) CK(cudaEventRecord(ws.ev4, st));
+  // K1 pool + range pass + bar / winner init + dequantised tables (+ the first level's range
+  // operands) in one launch
+  launch_pool_v3(d_img, g, b.upool, b.qpool, b.mi, b.cnt + kAccumSlot, b.rm, b.gbest, b.win, b.deq, st,
+                 pre_ops ? b.thr : nullptr, pre_ops ? b.ropnd : nullptr, pre_ops ? b.cnt + kPendSlot : nullptr);
+  if (time_pool) {
+    CK(cudaEventRecord(ws.ev5, st));
+    // algorithmic bytes: the image read once, the pool written once (fp16 operand 2K, exact
+    // cells 8 x N u16, meta 16 B per padded domain), and the preparations riding in the same
+    // launch: per range its N pixels read, RangeMeta (16 B), bar (8 B) and winner key (16 B)
+    const double Dt = (double)g.Dt * g.batch;
+    ws.pool_bytes = (double)g.W * g.H + Dt * (2.0 * g.K + 16.0 * g.N + 16.0) + (double)g.R * (g.N + 40.0);
+    // the first level's range operands (8 rows of K fp16 per range) and thresholds
+    if (pre_ops) ws.pool_bytes += (double)g.R * (16.0 * g.K + 4.0);
+  }
   if (seed) launch_seed_v3(d_img, g, b.qpool, b.mi, b.rm, b.gbest, b.deq, seed_side >= 3 ? 1 : 0, st);
   g_launches += seed ? 2 : 1;
   if (g_timing.load()) CK(cudaEventRecord(ws.ev0, st));
-  const std::vector<int> lv = scan_levels(g);
-  for (size_t l = 0; l + 1 < lv.size(); ++l) enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st);
+  for (size_t l = 0; l + 1 < lv.size(); ++l)
+    enqueue_level(ws, d_img, g, b, lv[l], b.cnt + l * kPartSlots, st, l == 0 && pre_ops);
   enqueue_final(ws, d_img, g, b, lv.size() - 1, d_out, st);
 }
 
@@ -593,7 +607,7 @@ std::vector<unsigned long long> encode_key(Workspace& ws, const unsigned char* d
   k.push_back(ws.list_cap);
   for (const char* name : {"FIC_LEVELS", "FIC_PREPASS", "FIC_SELECT", "FIC_MATCHER", "FIC_COARSE", "FIC_SEED",
                            "FIC_LANEBEST_MAX", "FIC_F16ACC", "FIC_F16SEL", "FIC_FUSED", "FIC_EVAL_SPLIT",
-                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP", "FIC_EVAL_PER", "FIC_ROTATE"}) {
+                           "FIC_SPARSE_EXACT", "FIC_LANE_GROUP", "FIC_EVAL_PER", "FIC_ROTATE", "FIC_PREOPS"}) {
     const char* e = std::getenv(name);
     unsigned long long h = 1469598103934665603ull;
     for (const char* c = e ? e : "\x01"; *c; ++c) h = (h ^ (unsigned char)*c) * 1099511628211ull;
@@ -823,9 +837,12 @@ void collect_timing(Workspace& ws) {
     g_timing_ms += ms;
     g_timing_n += 1;
   }
-  if (ws.scan_timed && cudaEventElapsedTime(&ms, ws.ev2, ws.ev3) == cudaSuccess) {
+  float ms2 = 0.f;
+  if (ws.scan_timed && cudaEventElapsedTime(&ms, ws.ev2, ws.ev6) == cudaSuccess &&
+      cudaEventElapsedTime(&ms2, ws.ev2, ws.ev3) == cudaSuccess) {
     std::lock_guard<std::mutex> lock(g_timing_mu);
     g_scan_ms += ms;
+    g_scan_expand_ms += ms2;
     g_scan_n += 1;
   }
   ws.scan_timed = false;
@@ -1563,6 +1580,19 @@ int32_t fic_scan_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
   if (launches) *launches = g_scan_n;
   if (reset) {
     g_scan_ms = 0.0;
+    g_scan_expand_ms = 0.0;
+    g_scan_n = 0;
+  }
+  return FIC_OK;
+}
+
+int32_t fic_scan_expand_timing(double* avg_ms, uint64_t* launches, int32_t reset) {
+  std::lock_guard<std::mutex> lock(g_timing_mu);
+  if (avg_ms) *avg_ms = g_scan_n ? g_scan_expand_ms / (double)g_scan_n : 0.0;
+  if (launches) *launches = g_scan_n;
+  if (reset) {
+    g_scan_ms = 0.0;
+    g_scan_expand_ms = 0.0;
     g_scan_n = 0;
   }
   return FIC_OK;

@@ -90,11 +90,19 @@ struct PrepAux {
   unsigned long long* win;  // 2 words per range
   double* deq;              // 2^s_bits s values, then 2^o_bits o values
   int pool_blocks;
+  int aux_blocks;
+  // first scan level's range operands (no bar yet: every range allpass), built by the blocks
+  // past the aux ones when the encode starts with a sparse level and no seed (else nullptr)
+  float* thr;
+  unsigned char* ropnd;
+  unsigned long long* pend_count;
 };
+__device__ void range_op_first_level(const unsigned char* __restrict__ img, const Geometry& g, const PrepAux& a,
+                                     int mt);
 
 __device__ void prep_aux(const unsigned char* __restrict__ img, const Geometry& g, const PrepAux& a) {
   const int tid = (blockIdx.x - a.pool_blocks) * blockDim.x + threadIdx.x;
-  const int nthreads = (gridDim.x - a.pool_blocks) * blockDim.x;
+  const int nthreads = a.aux_blocks * blockDim.x;
   for (int r = tid; r < g.R; r += nthreads) {
     int x0, y0;
     range_origin(g, r, x0, y0);
@@ -126,6 +134,10 @@ __global__ void __launch_bounds__(kPoolThreads)
 pool_v3_kernel(const unsigned char* __restrict__ img, Geometry g, __half* __restrict__ upool,
                unsigned short* __restrict__ qpool, DomainMetaI* __restrict__ meta_i,
                unsigned long long* __restrict__ flat_count, PrepAux aux) {
+  if ((int)blockIdx.x >= aux.pool_blocks + aux.aux_blocks) {
+    range_op_first_level(img, g, aux, (int)blockIdx.x - aux.pool_blocks - aux.aux_blocks);
+    return;
+  }
   if ((int)blockIdx.x >= aux.pool_blocks) {
     prep_aux(img, g, aux);
     return;
@@ -932,6 +944,57 @@ range_op_kernel(const unsigned char* __restrict__ img, Geometry g, const RangeMe
   else
     build_ranges_n<NN>(dst, img, g, rmeta, t, blockIdx.x, blockIdx.y * per + threadIdx.x, blockDim.x,
                        blockIdx.y * per + per);
+}
+
+// range_op_kernel for the first scan level of an encode that starts without a bar (no seed),
+// riding in the pool launch: every range is allpass (scan_threshold against +inf is -1) or
+// shadow / padding (1e30), so the level's operands only need the range's own sums, computed
+// here from its pixels as the range pass does (RangeMeta is written by other blocks of the same
+// launch).  One block per m-tile, all K/8 chunks.
+__device__ void range_op_first_level(const unsigned char* __restrict__ img, const Geometry& g, const PrepAux& a,
+                                     int mt) {
+  __shared__ float s_thr[kScanRanges];
+  __shared__ RangeMeta s_rm[kScanRanges];
+  if (threadIdx.x < kScanRanges) {
+    const int r = mt * kScanRanges + threadIdx.x;
+    float t = 1e30f;
+    RangeMeta rm{0, 1, 0};
+    if (r < g.R) {
+      int x0, y0;
+      range_origin(g, r, x0, y0);
+      long long sb = 0, sbb = 0;
+      for (int i = 0; i < g.n; ++i) {
+        const unsigned char* row = img + (long long)(y0 + i) * g.W + x0;
+        for (int j = 0; j < g.n; ++j) {
+          const int v = row[j];
+          sb += v;
+          sbb += v * v;
+        }
+      }
+      const long long var = (long long)g.N * sbb - sb * sb;
+      rm = RangeMeta{(int)sb, (double)var <= g.shadow_eps, var};
+      if (!rm.shadow) t = -1.f;  // range_threshold with the bar at +inf (and the flags & 1 mode)
+    }
+    s_rm[threadIdx.x] = rm;
+    s_thr[threadIdx.x] = t;
+    a.thr[r] = t;
+    const unsigned ap = __ballot_sync(0xffffffffu, range_allpass(t));
+    if (threadIdx.x == 0) scan_allpass_masks(a.thr, g)[mt] = ap;
+  }
+  if (mt == 0 && threadIdx.x == 0) *a.pend_count = 0;
+  __syncthreads();
+  unsigned char* dst = a.ropnd + (long long)mt * kScanRows * g.K * 2;
+  const float* t = s_thr - mt * kScanRanges;
+  const RangeMeta* rm = s_rm - mt * kScanRanges;
+  const int chunks = kScanRows * (g.K / 8);
+  if (g.N == 4 && g.K == 16)
+    build_ranges_n<4>(dst, img, g, rm, t, mt, threadIdx.x, blockDim.x, chunks);
+  else if (g.N == 16 && g.K == 16)
+    build_ranges_n<16>(dst, img, g, rm, t, mt, threadIdx.x, blockDim.x, chunks);
+  else if (g.N == 64 && g.K == 64)
+    build_ranges_n<64>(dst, img, g, rm, t, mt, threadIdx.x, blockDim.x, chunks);
+  else
+    build_ranges(dst, img, g, rm, t, mt, threadIdx.x, blockDim.x, chunks);
 }
 
 // Survivor appender of one warp: entries go straight to the CTA's list partition, into
@@ -2175,12 +2238,15 @@ int scan_rows_per_cta() { return kScanRanges; }
 // (pool only: the read-back probe).
 void launch_pool_v3(const unsigned char* img, const Geometry& g, __half* upool, unsigned short* qpool,
                     DomainMetaI* meta_i, unsigned long long* counters, RangeMeta* rmeta, unsigned long long* gbest,
-                    void* win, double* deq, cudaStream_t st) {
+                    void* win, double* deq, cudaStream_t st, float* thr, unsigned char* ropnd,
+                    unsigned long long* pend_count) {
   const int blocks = (int)((long long)g.Dt * g.batch / kPoolBlock);
   const int aux_blocks = rmeta ? (g.R + kPoolThreads - 1) / kPoolThreads : 0;
-  const PrepAux aux{rmeta, counters + g.batch, gbest, static_cast<unsigned long long*>(win), deq, blocks};
-  pool_v3_kernel<<<blocks + aux_blocks, kPoolThreads, 2 * kPoolBlock * g.N * sizeof(unsigned short), st>>>(
-      img, g, upool, qpool, meta_i, counters, aux);
+  const int ro_blocks = rmeta && ropnd ? (g.R + kScanRanges - 1) / kScanRanges : 0;
+  const PrepAux aux{rmeta, counters + g.batch, gbest, static_cast<unsigned long long*>(win), deq, blocks,
+                    aux_blocks, thr, ropnd, pend_count};
+  pool_v3_kernel<<<blocks + aux_blocks + ro_blocks, kPoolThreads, 2 * kPoolBlock * g.N * sizeof(unsigned short),
+                   st>>>(img, g, upool, qpool, meta_i, counters, aux);
 }
 
 void launch_fill_u64(unsigned long long* p, long long n, unsigned long long v, cudaStream_t st) {
@@ -2320,7 +2386,7 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
                         const RangeMeta* rmeta, const unsigned char* ropnd, const float* thr, SurvEntry* list,
                         unsigned long long* counts, unsigned long long part, void* recs, unsigned long long* rcounts,
                         const unsigned short* qpool, const DomainMetaI* meta_i, unsigned long long* gbest,
-                        void* win, const double* deq, bool fused, cudaStream_t st) {
+                        void* win, const double* deq, bool fused, cudaStream_t st, cudaEvent_t after_scan) {
   const int grid = scan_grid(g, stride, sms);
   const ScanLevel lv = make_level(g, stride, grid);
   const ScanSmem L = scan_smem_layout(g.K, fused);
@@ -2339,6 +2405,7 @@ cudaError_t launch_scan(const unsigned char* img, const Geometry& g, int stride,
   kern<<<grid, fused ? kFusedThreads : kScanThreads, L.total, st>>>(img, g, lv, upool, rmeta, ropnd, thr, R, rcounts,
                                                                     rcap, list, part, counts, ev);
   e = cudaGetLastError();
+  if (e == cudaSuccess && after_scan) e = cudaEventRecord(after_scan, st);  // timing: the scan kernel alone
   // sparse levels append their selected entries directly (no mask records to expand)
   if (e != cudaSuccess || fused || lv.select != 0) return e;
   expand_kernel<<<grid * 8, 256, 0, st>>>(R, rcounts, rcap, list, counts, part, 8);
