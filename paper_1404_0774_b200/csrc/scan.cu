@@ -681,6 +681,14 @@ __device__ long long g_trace[kTraceTiles * kTraceSlots];
 
 // Compiled in only with -DFIC_TRACE (FIC_TRACE=1 python -m paper_1404_0774_b200.build): the
 // stamps cost ~10% of the scan even when disabled at run time.
+// The scan's decomposition switches (FIC_DEBUG 8 / 16 / 128: no test, no MMAs, no TMEM reads;
+// DESIGN.md section 5).  Compiling them out (-DFIC_SCAN_DEBUG=0) removes a few instructions per
+// tile but measured SLOWER (cfg2 full level 96.4 -> 101.5 us, cfg3 1071 -> 1127 us: the
+// schedule of the epilogue loop changes), so they stay in.
+#ifndef FIC_SCAN_DEBUG
+#define FIC_SCAN_DEBUG 1
+#endif
+constexpr bool kScanDebug = FIC_SCAN_DEBUG != 0;
 __device__ __forceinline__ void trace_stamp(const Geometry& g, int tile, int slot) {
 #ifdef FIC_TRACE
   if ((g.flags & 32) && blockIdx.x == 0 && tile < kTraceTiles) g_trace[tile * kTraceSlots + slot] = clock64();
@@ -1101,6 +1109,11 @@ struct MaskRec {
   uint8_t m[32];    // lane l: isometry mask of domain d0 + l
 };
 constexpr uint32_t kRecChunk = 16;
+#ifndef FIC_REC_GROUP
+#define FIC_REC_GROUP 1  // full-level fp16 epilogue: one record reservation per tile (0: per record)
+#endif
+static_assert((kRecChunk & (kRecChunk - 1)) == 0, "record chunks: a power of two");
+static_assert(kEpiRanges <= (int)kRecChunk, "one tile's records of a warp fit one chunk");
 
 struct WarpRecAppender {
   MaskRec* recs;
@@ -1132,6 +1145,29 @@ struct WarpRecAppender {
     ++next;
     ++base;
     --left;
+  }
+  // Room for `nh` (<= kRecChunk) more records of one tile in the warp's chunk, written by the
+  // caller at next .. next + nh - 1 (valid: the chunk lies inside the partition, whose size is a
+  // multiple of kRecChunk); a chunk too short for the group is padded with sentinels and a new
+  // one reserved.  Separate scan only (a fused scan publishes chunks to its consumers as they
+  // fill).  Returns the group's first record.
+  __device__ __forceinline__ MaskRec* group(uint32_t nh, bool& valid) {
+    if (nh > left) {
+      const uint32_t lane = threadIdx.x & 31;
+      if (lane < left && base + lane < cap) next[lane].r8 = kSentinel;
+      uint32_t nb = 0;
+      if (lane == 0) nb = atomicAdd(count, kRecChunk);
+      base = __shfl_sync(0xffffffffu, nb, 0);
+      cur = base;
+      left = kRecChunk;
+      next = recs + base;
+    }
+    valid = base < cap;
+    MaskRec* at = next;
+    next += nh;
+    base += nh;
+    left -= nh;
+    return at;
   }
   __device__ __forceinline__ void close() {
     const uint32_t lane = threadIdx.x & 31;
@@ -1422,7 +1458,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     // MMAs and commits.  The issuing thread is on the scan's critical path.
     {
       const uint32_t idesc = F16 ? ptx::idesc_f16_f16(128, kScanRows) : ptx::idesc_f16_f32(128, kScanRows);
-      const bool do_mma = !(g.flags & 16);  // debug: flags & 16 skips the MMAs
+      const bool do_mma = !(kScanDebug && (g.flags & 16));  // debug: flags & 16 skips the MMAs
       // descriptors: the start address field (bits 0-13, 16-byte units) advances by 16 per
       // K=16 step (256 bytes) and by p_bytes/16 per ring stage; everything else is constant
       const uint64_t p_desc0 = ptx::smem_desc(ptx::smem_addr(sP), 128, K * 16);
@@ -1510,7 +1546,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
         const uint32_t d = dslice + (uint32_t)(j * lv.stride * kScanTileDom + quarter * 32 + lane);
         ptx::mbar_wait_sleep(&tfull_bar[buf], kTBufs == 2 ? ((i >> 1) & 1) : (i & 1));
         ptx::tc_fence_after();
-        if (g.flags & 128) {  // debug: no TMEM reads at all (MMA + producer throughput)
+        if (kScanDebug && (g.flags & 128)) {  // debug: no TMEM reads at all (MMA + producer throughput)
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&tempty_bar[buf]);
           continue;
@@ -1541,7 +1577,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             trace_stamp(g, i, 3 + e);
           }
         }
-        if (g.flags & 8) continue;                          // debug: skip the test
+        if (kScanDebug && (g.flags & 8)) continue;          // debug: skip the test
         const uint32_t ap = (allpass >> (hc * kCR)) & ((1u << kCR) - 1u);  // the chunk's ranges
         const uint32_t rb = rowbase + 8u * (uint32_t)(hc * kCR);
         if constexpr (F16) {
@@ -1638,6 +1674,10 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             continue;
           }
           if (groups) {
+            // one slot reservation for the tile's records (no per-record chunk bookkeeping)
+            constexpr bool kPut = FUSED || !FIC_REC_GROUP;
+            bool valid = false;
+            MaskRec* rc = kPut ? nullptr : app.group((uint32_t)__popc(groups), valid);
 #pragma unroll
             for (int k = 0; k < kEpiRanges; ++k) {
               if ((groups >> k) & 1u) {
@@ -1652,7 +1692,15 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                   for (int j = 0; j < 4; ++j) x |= __hgt2_mask(__habs2(h[4 * k + j]), one2) & (0x00020001u << (2 * j));
                   bits = (x | (x >> 16)) & 0xFFu;
                 }
-                app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
+                if constexpr (kPut) {
+                  app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
+                } else {
+                  if (valid) {
+                    if (lane == 0) *reinterpret_cast<uint2*>(rc) = make_uint2(rowbase + 8u * (uint32_t)k, d);
+                    rc->m[lane] = (uint8_t)bits;
+                  }
+                  ++rc;
+                }
               }
             }
           }
@@ -2339,7 +2387,9 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
 
 // counts[c] = survivors of scan CTA c; its entries are list[c * part, c * part + min(counts[c], part)).
 // Record partition size for entry partitions of `part` entries (see expand_kernel).
-unsigned long long scan_rec_part(unsigned long long part) { return (part / 2 + 2) & ~1ull; }  // even: 16-byte aligned partitions
+// a multiple of kRecChunk: every reserved chunk lies wholly inside or wholly outside its partition
+// (and partitions stay 16-byte aligned)
+unsigned long long scan_rec_part(unsigned long long part) { return (part / 2 + kRecChunk) & ~(unsigned long long)(kRecChunk - 1); }
 size_t scan_rec_bytes(unsigned long long list_cap, int parts) {
   return (size_t)scan_rec_part(list_cap / (unsigned long long)parts) * parts * sizeof(MaskRec);
 }

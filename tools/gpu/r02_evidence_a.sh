@@ -1,6 +1,6 @@
 # round-2 evidence, part A (small outputs): GPU suite, smoke, bench lines, launch list, timelines
 mkdir -p gpurun_out/ev
-O=gpurun_out/ev
+O=${EV_DIR:-gpurun_out/ev}; mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 timeout 900 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err

@@ -1,7 +1,7 @@
 # round-2 evidence, part B: ncu --set full of the dominant kernels, summarised on the box (the
 # reports themselves are kept only when small)
 mkdir -p gpurun_out/ncu
-O=gpurun_out/ncu
+O=${NCU_DIR:-gpurun_out/ncu}; mkdir -p $O
 cap() {  # name, kernel regex, ncu extra args, command...
   n=$1; k=$2; x=$3; shift 3
   timeout 1200 ncu --set full --import-source on --clock-control none $x -k regex:$k -o $O/$n -f "$@" > /dev/null 2>&1
