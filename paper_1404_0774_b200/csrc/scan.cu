@@ -1681,17 +1681,13 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
 #pragma unroll
             for (int k = 0; k < kEpiRanges; ++k) {
               if ((groups >> k) & 1u) {
-                uint32_t bits = 0;
-                if ((allpass >> k) & 1u) {
-                  bits = 0xFFu;
-                } else {
-                  // column c = 2j + half of register j: half2 compares give 0xFFFF masks, bit
-                  // 2j of the low half and bit 2j + 1 of the high half are kept, then folded
-                  uint32_t x = 0u;
+                // column c = 2j + half of register j: half2 compares give 0xFFFF masks, bit 2j of
+                // the low half and bit 2j + 1 of the high half are kept, then folded; an allpass
+                // range keeps every column (no branch: the low byte is what is stored)
+                uint32_t x = 0u;
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) x |= __hgt2_mask(__habs2(h[4 * k + j]), one2) & (0x00020001u << (2 * j));
-                  bits = (x | (x >> 16)) & 0xFFu;
-                }
+                for (int j = 0; j < 4; ++j) x |= __hgt2_mask(__habs2(h[4 * k + j]), one2) & (0x00020001u << (2 * j));
+                const uint32_t bits = (x | (x >> 16) | (0u - ((allpass >> k) & 1u))) & 0xFFu;
                 if constexpr (kPut) {
                   app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
                 } else {
