@@ -1125,6 +1125,8 @@ struct WarpRecAppender {
   EvalRing* ring;    // fused scan: finished chunks are published to the consumers
   MaskRec* next = nullptr;  // record `base` (valid while base < cap): advanced by one per put,
                             // so a put is two stores and no 64-bit index arithmetic
+  MaskRec* trash = nullptr;  // this CTA's scratch chunk past every partition (group() of an
+                             // overflowed partition: the stores need no branch)
 
   // Warp-uniform: every lane passes its mask (0 for none).
   __device__ __forceinline__ void put(uint32_t bits, uint32_t r8, uint32_t d0) {
@@ -1147,11 +1149,11 @@ struct WarpRecAppender {
     --left;
   }
   // Room for `nh` (<= kRecChunk) more records of one tile in the warp's chunk, written by the
-  // caller at next .. next + nh - 1 (valid: the chunk lies inside the partition, whose size is a
-  // multiple of kRecChunk); a chunk too short for the group is padded with sentinels and a new
-  // one reserved.  Separate scan only (a fused scan publishes chunks to its consumers as they
+  // caller at the returned record and the nh - 1 after it (the chunk lies wholly inside the
+  // partition, whose size is a multiple of kRecChunk, or the scratch chunk is returned); a chunk
+  // too short for the group is padded with sentinels and a new one reserved.  Separate scan only (a fused scan publishes chunks to its consumers as they
   // fill).  Returns the group's first record.
-  __device__ __forceinline__ MaskRec* group(uint32_t nh, bool& valid) {
+  __device__ __forceinline__ MaskRec* group(uint32_t nh) {
     if (nh > left) {
       const uint32_t lane = threadIdx.x & 31;
       if (lane < left && base + lane < cap) next[lane].r8 = kSentinel;
@@ -1162,8 +1164,8 @@ struct WarpRecAppender {
       left = kRecChunk;
       next = recs + base;
     }
-    valid = base < cap;
-    MaskRec* at = next;
+    // an overflowed partition (the host re-runs the level) writes to the scratch chunk
+    MaskRec* at = base < cap ? next : trash;
     next += nh;
     base += nh;
     left -= nh;
@@ -1514,6 +1516,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     // range (many hits) take turns instead of pacing every tile
     const bool rotate = MB != 4 && lv.rotate;
     WarpRecAppender app{recs, count, (uint32_t)rcap, 0u, 0u, kSentinel, ring};
+    app.trash = recs_all + (unsigned long long)G * rcap + (unsigned long long)cta * kRecChunk;
     constexpr bool sel = MB >= 2;
     SurvEntry* elist = elist_cta;
     const uint32_t ecap = (uint32_t)cap;
@@ -1676,8 +1679,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
           if (groups) {
             // one slot reservation for the tile's records (no per-record chunk bookkeeping)
             constexpr bool kPut = FUSED || !FIC_REC_GROUP;
-            bool valid = false;
-            MaskRec* rc = kPut ? nullptr : app.group((uint32_t)__popc(groups), valid);
+            MaskRec* rc = kPut ? nullptr : app.group((uint32_t)__popc(groups));
 #pragma unroll
             for (int k = 0; k < kEpiRanges; ++k) {
               if ((groups >> k) & 1u) {
@@ -1691,10 +1693,8 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 if constexpr (kPut) {
                   app.put(bits, rowbase + 8u * (uint32_t)k, d - (uint32_t)lane);
                 } else {
-                  if (valid) {
-                    if (lane == 0) *reinterpret_cast<uint2*>(rc) = make_uint2(rowbase + 8u * (uint32_t)k, d);
-                    rc->m[lane] = (uint8_t)bits;
-                  }
+                  if (lane == 0) *reinterpret_cast<uint2*>(rc) = make_uint2(rowbase + 8u * (uint32_t)k, d);
+                  rc->m[lane] = (uint8_t)bits;
                   ++rc;
                 }
               }
@@ -2387,7 +2387,8 @@ static ScanLevel make_level(const Geometry& g, int stride, int G) {
 // (and partitions stay 16-byte aligned)
 unsigned long long scan_rec_part(unsigned long long part) { return (part / 2 + kRecChunk) & ~(unsigned long long)(kRecChunk - 1); }
 size_t scan_rec_bytes(unsigned long long list_cap, int parts) {
-  return (size_t)scan_rec_part(list_cap / (unsigned long long)parts) * parts * sizeof(MaskRec);
+  // the partitions, then one scratch chunk per scan CTA
+  return ((size_t)scan_rec_part(list_cap / (unsigned long long)parts) + kRecChunk) * parts * sizeof(MaskRec);
 }
 
 // Hit-first sparse levels with an fp16 accumulator (scan mode 7): a sparse level only lowers
