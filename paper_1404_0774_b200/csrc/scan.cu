@@ -1641,6 +1641,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
             // tree yields the best column AND its isometry; key = that half << 5 | 31 - lane,
             // one warp max per range, one chunk reservation per tile, lane k writes range k's
             // entry (as the fp32 selection)
+            // every range of `groups` has a lane above the threshold (or is allpass), so its warp
+            // maximum is that range's entry: hits == groups, no per-lane threshold in the key (a
+            // best |x| within 2^-7 of the threshold still yields an entry: a sparse level only
+            // lowers the bar, any evaluated candidate is a valid one)
+            if (!groups) continue;
             uint32_t wm[kEpiRanges];
 #pragma unroll
             for (int k = 0; k < kEpiRanges; ++k) {
@@ -1654,17 +1659,15 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 }
                 const __half2 m2 = __hmax2(__hmax2(__hmax2(t[0], t[1]), t[2]), t[3]);
                 const uint32_t m = __half_as_ushort(__hmax(__low2half(m2), __high2half(m2)));
-                key = (m > 0x3C07u || ((allpass >> k) & 1u)) ? (m << 5) | (31u - (uint32_t)lane) : 0u;
+                key = (m << 5) | (31u - (uint32_t)lane) | 0x200000u;  // nonzero even for lane 31 at |x| = 0
               }
               wm[k] = __reduce_max_sync(0xffffffffu, key);
             }
-            uint32_t hits = 0u, mine = 0u;
+            const uint32_t hits = groups;
+            uint32_t mine = 0u;
 #pragma unroll
-            for (int k = 0; k < kEpiRanges; ++k) {
-              hits |= (uint32_t)(wm[k] != 0u) << k;
-              if (lane == k) mine = wm[k];
-            }
-            if (!hits) continue;
+            for (int k = 0; k < kEpiRanges; ++k)
+              if (lane == k) mine = (groups >> k) & 1u ? wm[k] : 0u;
             const uint32_t nh = (uint32_t)__popc(hits);
             ech.reserve(nh);
             if (mine != 0u) {
@@ -1763,19 +1766,17 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 for (int c = 0; c < 8; ++c)
                   m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
               }
-              const uint32_t mk = (__float_as_uint(m) & 0x7FFFFF00u) | ((__float_as_uint(m) & 7u) << 5) |
-                                  (31u - (uint32_t)lane);
-              key = (m > 1.0f || ((ap >> k) & 1u)) ? mk : 0u;
+              // (hits == groups, as in the fp16 selection; bit 8 keeps the key nonzero)
+              key = (__float_as_uint(m) & 0x7FFFFE00u) | 0x100u | ((__float_as_uint(m) & 7u) << 5) |
+                    (31u - (uint32_t)lane);
             }
             wm[k] = __reduce_max_sync(0xffffffffu, key);
           }
-          uint32_t hits = 0u, mine = 0u;
+          const uint32_t hits = groups;
+          uint32_t mine = 0u;
 #pragma unroll
-          for (int k = 0; k < kCR; ++k) {
-            hits |= (uint32_t)(wm[k] != 0u) << k;
-            if (lane == k) mine = wm[k];
-          }
-          if (!hits) continue;
+          for (int k = 0; k < kCR; ++k)
+            if (lane == k) mine = (groups >> k) & 1u ? wm[k] : 0u;
           const uint32_t nh = (uint32_t)__popc(hits);
           ech.reserve(nh);  // pads the rest of the chunk and takes a new one when it is short
           if (mine != 0u) {
