@@ -1522,6 +1522,11 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     const uint32_t ecap = (uint32_t)cap;
     EntryChunks ech{elist, ecount, ecap, 0u, 0u, kSentinel, ring};
     const uint32_t tlane = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    // fp16 selection tags (7 - isometry in each half's low 3 bits) held in registers: with the
+    // mask an immediate, (v & mask) | tag is ONE LOP3 (two immediates would take two); the
+    // runtime zero keeps the compiler from folding them back into immediates
+    const uint32_t t1 = 1u + ((uint32_t)lv.stride >> 30);  // 1 (strides < 2^30)
+    const uint32_t tagr[4] = {0x00060007u * t1, 0x00040005u * t1, 0x00020003u * t1, 0x00000001u * t1};
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const Segment S = seg_at(lv, cta, G, sg);
@@ -1598,7 +1603,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
               __half2 t[4];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const uint32_t u = (v[4 * k + q] & 0x7FF87FF8u) | ((7u - 2u * q) | ((6u - 2u * q) << 16));
+                const uint32_t u = (v[4 * k + q] & 0x7FF87FF8u) | tagr[q];
                 t[q] = *reinterpret_cast<const __half2*>(&u);
               }
               const __half2 m2 = __hmax2(__hmax2(__hmax2(t[0], t[1]), t[2]), t[3]);
@@ -1654,7 +1659,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
                 __half2 t[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  const uint32_t u = (v[4 * k + j] & 0x7FF87FF8u) | ((7u - 2u * j) | ((6u - 2u * j) << 16));
+                  const uint32_t u = (v[4 * k + j] & 0x7FF87FF8u) | tagr[j];
                   t[j] = *reinterpret_cast<const __half2*>(&u);
                 }
                 const __half2 m2 = __hmax2(__hmax2(__hmax2(t[0], t[1]), t[2]), t[3]);
