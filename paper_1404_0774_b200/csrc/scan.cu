@@ -1527,6 +1527,10 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
     // runtime zero keeps the compiler from folding them back into immediates
     const uint32_t t1 = 1u + ((uint32_t)lv.stride >> 30);  // 1 (strides < 2^30)
     const uint32_t tagr[4] = {0x00060007u * t1, 0x00040005u * t1, 0x00020003u * t1, 0x00000001u * t1};
+    // (the fp32 selection's tags 7 - isometry likewise, for the hit ranges of sparse levels)
+    uint32_t tagf[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) tagf[c] = (uint32_t)(7 - c) * t1;
     int i = 0;
     for (int sg = 0; sg < nseg; ++sg) {
       const Segment S = seg_at(lv, cta, G, sg);
@@ -1741,7 +1745,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
               float m = 0.f;
 #pragma unroll
               for (int c = 0; c < 8; ++c)
-                m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
+                m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | tagf[c]));
               pk[k] = __float_as_uint(m);
               gmask |= (uint32_t)(m > 1.0f) << k;
             } else {
@@ -1769,7 +1773,7 @@ scan_kernel(const unsigned char* __restrict__ img, Geometry g, ScanLevel lv, con
               } else {
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                  m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | (uint32_t)(7 - c)));
+                  m = fmaxf(m, __uint_as_float((v[8 * k + c] & 0x7FFFFFF8u) | tagf[c]));
               }
               // (hits == groups, as in the fp16 selection; bit 8 keeps the key nonzero)
               key = (__float_as_uint(m) & 0x7FFFFE00u) | 0x100u | ((__float_as_uint(m) & 7u) << 5) |
