@@ -2579,10 +2579,12 @@ void launch_record(const unsigned char* img, const Geometry& g, const unsigned s
                    const unsigned long long* full_counts, int parts, unsigned long long* need,
                    unsigned long long* accum, unsigned long long* snap, unsigned long long* ticket, int nslots,
                    bool snapshot, unsigned long long* hstat, int need_off, int cnt_off, cudaStream_t st) {
-  const int blocks = (g.R + 63) / 64;  // 64-thread blocks: the per-range exact evaluations spread over more SMs
+  // small blocks: the per-range exact evaluations (a latency chain each) spread over more SMs
+  constexpr int kRecThreads = 32;
+  const int blocks = (g.R + kRecThreads - 1) / kRecThreads;
   const unsigned __int128* win = static_cast<const unsigned __int128*>(win_);
 #define FIC_REC(NN) \
-  record_kernel<NN><<<blocks, 64, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, \
+  record_kernel<NN><<<blocks, kRecThreads, 0, st>>>(img, g, qpool, meta_i, rmeta, win, gbest, out, selfcheck, full_counts, parts, \
                                            need, accum, snap, ticket, nslots, snapshot ? 1 : 0, hstat, need_off, cnt_off)
   if (g.N == 4) FIC_REC(4);
   else if (g.N == 16) FIC_REC(16);
